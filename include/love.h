@@ -1,0 +1,196 @@
+/*
+ * love.h -- C ABI of the B200-native LOVE / KISS-GP hot path (arXiv 1803.06058).
+ *
+ * LOVE ("LanczOs Variance Estimates", §3) caches a rank-k factor of
+ *   C = K_UU W_X (W_X^T K_UU W_X + sigma^2 I)^{-1} W_X^T K_UU          (Eq. 8)
+ * from k Lanczos steps on K_hat = W_X^T K_UU W_X + sigma^2 I (KISS-GP, Eq. 5) and
+ * answers predictive (co)variances in O(k) (Eq. 10) and posterior samples in
+ * O(k(t+m)) per sample (Eqs. 11-15).  Algorithm 1 maps onto
+ * love_build_cache (lines P:391-399) and love_predict_var / love_predict_covar.
+ *
+ * Conventions (all entry points):
+ *   - Every data pointer is a DEVICE pointer on the current CUDA device unless stated
+ *     otherwise.  Every call is stream-ordered on `stream` (a cudaStream_t passed as void*;
+ *     NULL = the legacy default stream).
+ *   - Matrices are row-major unless stated otherwise; inputs X are fp64 (reading A3: the
+ *     cell index floor((x-lo)/h) must be taken in fp64).
+ *   - "V" below is the vector precision chosen by love_opts.precision: float for
+ *     LOVE_FP32, double for LOVE_FP64.
+ *   - Errors are status codes, never exceptions; love_last_error() returns a thread-local
+ *     message for the last non-OK status of the calling thread.
+ *   - Ownership: the caller owns every buffer it passes in and every output buffer.  The
+ *     library copies what it needs during the call and keeps no reference to caller
+ *     memory after the call returns.  A love_cache owns all of its device memory until
+ *     love_free().
+ *   - Thread safety: a built cache is immutable; concurrent queries on different streams
+ *     are safe.  Diagnostic counters are updated with device atomics.
+ */
+#ifndef LOVE_H_
+#define LOVE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LOVE_ABI_VERSION 1
+
+typedef struct love_cache love_cache;   /* opaque */
+
+typedef enum {
+    LOVE_OK = 0,
+    LOVE_ERR_ARG = 1,         /* NULL pointer, bad shape, k < 1, sigma^2 <= 0, m_d < 4, d not in 1..3 */
+    LOVE_ERR_RANGE = 2,       /* a training point needs a grid node outside [0, m_d-1] (reading A4) */
+    LOVE_ERR_NOT_PD = 3,      /* a pivot of the Cholesky of T_k is <= 0 (reading A13) */
+    LOVE_ERR_ZERO_PROBE = 4,  /* the Lanczos probe vector is zero */
+    LOVE_ERR_CUDA = 5,        /* a CUDA runtime error (message in love_last_error) */
+    LOVE_ERR_NCCL = 6,        /* NCCL could not be loaded / initialised / failed */
+    LOVE_ERR_OOM = 7,         /* device allocation failed */
+    LOVE_ERR_STATE = 8        /* e.g. love_sample on a cache built with k_sample = 0 */
+} love_status;
+
+enum { LOVE_FP32 = 0, LOVE_FP64 = 1 };
+enum { LOVE_PROBE_Y = 0, LOVE_PROBE_AVGCOL = 1 };
+enum { LOVE_PRIOR_SKI = 0, LOVE_PRIOR_EXACT = 1 };
+
+/* Regular (Kronecker) grid of inducing points: u_{d,i} = lo[d] + i*h[d],
+ * i = 0..m[d]-1, flat index row-major (last dimension fastest).  d in 1..3, m[d] >= 4. */
+typedef struct {
+    int32_t d;
+    int32_t reserved;
+    int64_t m[3];
+    double lo[3];
+    double h[3];
+} love_grid;
+
+/* Product RBF kernel k(x,x') = outputscale * prod_d exp(-(x_d-x'_d)^2 / (2 l_d^2))
+ * (reading A6); the grid kernel matrix is K_UU = outputscale * kron_d T(c_d)
+ * with Toeplitz columns c_d[i] = exp(-(i h_d)^2/(2 l_d^2)). */
+typedef struct {
+    double outputscale;
+    double lengthscale[3];
+} love_rbf;
+
+typedef struct {
+    int32_t precision;      /* LOVE_FP32 (V = float, reductions in fp64) | LOVE_FP64 (V = double) */
+    int32_t probe;          /* LOVE_PROBE_Y (default: b = y, reading A1) | LOVE_PROBE_AVGCOL (reserved) */
+    int32_t prior;          /* LOVE_PRIOR_SKI (w*^T K_UU w*, default) | LOVE_PRIOR_EXACT (k(x*,x*)) */
+    int32_t reorth_passes;  /* full reorthogonalisation passes per step: 0 => 1 (fp32) / 2 (fp64) */
+    double breakdown_tol;   /* tau of the breakdown rule (reading A12); 0 => 1e-6 (fp32) / 1e-10 (fp64) */
+    int32_t k_sample;       /* k' of the sampling cache; 0 => no sampling cache */
+    int32_t reserved;
+} love_opts;
+
+/* Data-parallel sharding of the training points.  Every rank calls
+ * love_build_cache with its own X/y shard and identical grid/kernel/sigma^2/k/opts; the
+ * returned caches are identical replicas.  nccl_unique_id: 128 bytes (HOST memory) from
+ * love_nccl_unique_id on rank 0, broadcast by the caller.  NULL love_dist => one GPU. */
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    const void* nccl_unique_id;
+} love_dist;
+
+typedef struct {
+    int32_t k_eff;          /* Lanczos steps kept (< k after breakdown, reading A12) */
+    int32_t k_pad;          /* row stride of the cache Rc (k_eff rounded up to a multiple of 4) */
+    int32_t k_sample_eff;   /* columns of the sampling root S (0 if none) */
+    int32_t precision;
+    int64_t n_local;        /* training points on this rank */
+    int64_t n_global;       /* training points over all ranks */
+    int64_t m_total;        /* inducing points */
+    int64_t n_items;        /* interpolation work items (cells split into <= 32-point chunks) */
+    double b_norm;          /* ||b|| of the probe (global) */
+    const double* alpha;    /* HOST, k_eff entries: diagonal of T_k (owned by the cache) */
+    const double* beta;     /* HOST, k_eff-1 entries: off-diagonal of T_k */
+    int64_t n_negative_var; /* variance queries that returned < 0 (returned raw, reading A20) */
+    int64_t n_out_of_range; /* query points outside the grid (NaN returned) */
+} love_info;
+
+/* ---------------------------------------------------------------------------------------
+ * love_build_cache -- Algorithm 1 pre-computation on this rank's shard.
+ *   grid, rbf, opts : HOST structs (opts may be NULL => defaults).
+ *   sigma2          : observation noise variance sigma^2 > 0.
+ *   X               : n_local x d fp64, row-major.  y : n_local fp64.
+ *   k               : Lanczos steps (1 <= k <= n_global).
+ *   dist            : HOST struct or NULL.
+ *   out             : HOST pointer receiving the new cache.
+ * Runs: interpolation indices/weights, cell sort, K_UU setup, k steps
+ * of Lanczos with full reorthogonalisation, streamed Cholesky of
+ * T_k, the cache Rc = K_UU W_X Q_k L^{-T} (so Rc Rc^T = R^T R'),
+ * the mean cache a (Eq. 6), and the sampling root if opts->k_sample > 0.
+ * Synchronises `stream` before returning.  Breakdown is not an error (k_eff < k).
+ * On error *out is NULL and nothing is leaked. */
+love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2,
+                             const double* X, const double* y, int64_t n_local, int32_t k,
+                             const love_opts* opts, const love_dist* dist, void* stream,
+                             love_cache** out);
+
+/* Predictive variances (Eq. 10 with x*_i = x*_j; Alg. 1):
+ *   var(x*) = prior(x*) - || Rc^T w_{x*} ||^2,   prior = w*^T K_UU w* (SKI) or k(x*,x*).
+ *   Xs       : t x d fp64 (device).  var_out : t values of V (device).
+ *   mean_out : NULL or t values of V: mu(x*) = w*^T a (Eq. 6).
+ * Asynchronous.  Out-of-range points give NaN and bump n_out_of_range. */
+love_status love_predict_var(const love_cache* cache, const double* Xs, int64_t t,
+                             void* var_out, void* mean_out, void* stream);
+
+/* Predictive covariances of t pairs (Xa[i], Xb[i]) (Eq. 10):
+ *   cov = prior(x_a, x_b) - (Rc^T w_a) . (Rc^T w_b).   cov_out : t values of V. */
+love_status love_predict_covar(const love_cache* cache, const double* Xa, const double* Xb,
+                               int64_t t, void* cov_out, void* stream);
+
+/* s joint posterior samples at t points (Eq. 11):
+ *   F = mu(X*) 1^T + W_{X*}^T S zeta,   S S^T ~= K_UU - R^T R' (Eqs. 13-15).
+ *   zeta : NULL (draw N(0,1) with Philox4x32-10 keyed by `seed`, reading A24) or
+ *          k_sample_eff x s fp64 column-major (sample j = column j), for shared-draw parity.
+ *   out  : t x s values of V, column-major (sample j is contiguous: out[j*t + i]).
+ * Requires a cache built with k_sample > 0 (else LOVE_ERR_STATE). */
+love_status love_sample(const love_cache* cache, const double* Xs, int64_t t, int64_t s,
+                        uint64_t seed, const double* zeta, void* out, void* stream);
+
+/* Copies diagnostics into *info (HOST).  Synchronises the device to read the counters. */
+love_status love_cache_info(const love_cache* cache, love_info* info);
+
+/* Releases every device buffer of the cache.  NULL is a no-op. */
+void love_free(love_cache* cache);
+
+/* Thread-local message of the last non-OK status on the calling thread ("" if none). */
+const char* love_last_error(void);
+
+/* --------------------------------------------------------------------------------------
+ * Operators of the cached model, for unit parity and for users who need them.
+ * Vectors are in the caller's ORIGINAL training-point order.
+ * ------------------------------------------------------------------------------------ */
+
+/* out = (W_X^T K_UU W_X + sigma^2 I) v on this rank's points (mvm_K_XX, Alg. 1).
+ * v, out : n_local values of V.  Single-rank caches only (else LOVE_ERR_STATE). */
+love_status love_ski_mvm(const love_cache* cache, const void* v, void* out, void* stream);
+
+/* out = K_UU u (Toeplitz / Kronecker-of-Toeplitz MVM).  u, out : m_total of V. */
+love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void* stream);
+
+enum {
+    LOVE_EXPORT_RC = 0,        /* m_total x k_pad of V, row-major: Rc = K_UU W_X Q L^{-T} */
+    LOVE_EXPORT_MEAN = 1,      /* m_total of V: mean cache a */
+    LOVE_EXPORT_S = 2,         /* m_total x k_sample_eff of V, row-major: sampling root */
+    LOVE_EXPORT_PERM = 3       /* n_local int32: sorted position -> original point index */
+};
+/* Copies an internal array into the caller's DEVICE buffer `dst` of `capacity` bytes.
+ * *bytes (HOST, may be NULL) receives the size; dst == NULL only queries the size. */
+love_status love_cache_export(const love_cache* cache, int32_t what, void* dst,
+                              int64_t capacity, int64_t* bytes, void* stream);
+
+/* Writes a fresh 128-byte NCCL unique id into `out` (HOST).  Call on rank 0 only. */
+love_status love_nccl_unique_id(void* out);
+
+/* Number of kernels this library has launched since it was loaded (all threads). */
+int64_t love_launch_count(void);
+
+/* LOVE_ABI_VERSION of the loaded library. */
+int32_t love_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOVE_H_ */

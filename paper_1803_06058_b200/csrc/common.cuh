@@ -1,0 +1,75 @@
+// common.cuh -- shared device helpers of the LOVE sm_100a library (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+namespace love {
+
+extern std::atomic<int64_t> g_launch_count;
+
+#define LOVE_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+    do {                                                                            \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                 \
+        ::love::g_launch_count.fetch_add(1, std::memory_order_relaxed);              \
+    } while (0)
+
+constexpr int kWarp = 32;
+constexpr int kItemMax = 32;  // max points per interpolation work item (one cell chunk)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Keys cubic-convolution weights, a = -1/2 (reading A2): for a point at u_j + f*h
+// the nodes j-1, j, j+1, j+2 get u(1+f), u(f), u(1-f), u(2-f).  Written as the cubic
+// polynomials in f that these evaluate to (same values, fewer operations):
+//   u(1+f) = -0.5 f^3 +     f^2 - 0.5 f
+//   u(f)   =  1.5 f^3 - 2.5 f^2         + 1
+//   u(1-f) = -1.5 f^3 + 2   f^2 + 0.5 f
+//   u(2-f) =  0.5 f^3 - 0.5 f^2
+template <typename T>
+__device__ __forceinline__ void keys4(T f, T w[4]) {
+    const T f2 = f * f, f3 = f2 * f;
+    w[0] = T(-0.5) * f3 + f2 - T(0.5) * f;
+    w[1] = T(1.5) * f3 - T(2.5) * f2 + T(1);
+    w[2] = T(-1.5) * f3 + T(2) * f2 + T(0.5) * f;
+    w[3] = T(0.5) * f3 - T(0.5) * f2;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide sum (blockDim.x multiple of 32, <= 1024); result valid in thread 0.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem32) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) smem32[wid] = v;
+    __syncthreads();
+    T r = T(0);
+    if (wid == 0) {
+        r = (lane < (int)(blockDim.x >> 5)) ? smem32[lane] : T(0);
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+template <typename V> struct Vec4;
+template <> struct Vec4<float> { using type = float4; };
+template <> struct Vec4<double> { using type = double4; };
+
+}  // namespace love

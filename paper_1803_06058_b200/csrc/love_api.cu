@@ -1,0 +1,466 @@
+// love_api.cu -- the extern "C" boundary (include/love.h) and the build orchestration of
+// Algorithm 1's pre-computation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "love_internal.h"
+
+namespace love {
+
+std::atomic<int64_t> g_launch_count{0};
+
+namespace {
+thread_local std::string t_err;
+}
+
+void set_error(const std::string& msg) { t_err = msg; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    (void)cudaGetLastError();
+    throw LoveError{e == cudaErrorMemoryAllocation ? LOVE_ERR_OOM : LOVE_ERR_CUDA,
+                    std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+void* dalloc(Cache& c, size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    bytes = std::max<size_t>(bytes, 16);
+    cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    c.allocs.push_back(p);
+    cuda_check(cudaMemsetAsync(p, 0, bytes, s), "cudaMemsetAsync");
+    return p;
+}
+
+namespace {
+
+void release(Cache* c) {
+    if (!c) return;
+    for (void* p : c->allocs) cudaFree(p);
+    c->allocs.clear();
+    nccl_comm_destroy(*c);
+    delete c;
+}
+
+struct TempPool {                   // stream-ordered temporaries of one call
+    cudaStream_t s;
+    std::vector<void*> ps;
+    explicit TempPool(cudaStream_t st) : s(st) {}
+    void* get(size_t bytes) {
+        void* p = nullptr;
+        cuda_check(cudaMallocAsync(&p, std::max<size_t>(bytes, 16), s), "cudaMallocAsync(tmp)");
+        ps.push_back(p);
+        return p;
+    }
+    ~TempPool() {
+        for (void* p : ps) cudaFreeAsync(p, s);
+    }
+};
+
+void keep_pool_memory(int dev) {
+    static bool done[64] = {false};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
+__global__ void init_state_kernel(int* flags, int k, double* one) {
+    if (threadIdx.x == 0) {
+        flags[0] = 0;
+        flags[1] = k;
+        flags[2] = 0;
+        flags[3] = 0;
+        one[0] = 1.0;
+    }
+}
+
+love_status fail(const LoveError& e) {
+    set_error(e.msg);
+    return e.status;
+}
+
+void validate_build(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
+                    const double* y, int64_t n_local, int32_t k, love_cache** out) {
+    if (!grid || !rbf || !out) throw LoveError{LOVE_ERR_ARG, "NULL grid/rbf/out"};
+    if (grid->d < 1 || grid->d > 3) throw LoveError{LOVE_ERR_ARG, "grid.d must be 1..3"};
+    int64_t mt = 1;
+    for (int d = 0; d < grid->d; ++d) {
+        if (grid->m[d] < 4) throw LoveError{LOVE_ERR_ARG, "grid.m[d] must be >= 4"};
+        if (!(grid->h[d] > 0.0) || !std::isfinite(grid->lo[d]))
+            throw LoveError{LOVE_ERR_ARG, "grid.h[d] must be > 0 and lo finite"};
+        if (!(rbf->lengthscale[d] > 0.0)) throw LoveError{LOVE_ERR_ARG, "lengthscale must be > 0"};
+        mt *= grid->m[d];
+    }
+    if (mt >= (int64_t(1) << 30)) throw LoveError{LOVE_ERR_ARG, "m_total too large"};
+    if (!(rbf->outputscale > 0.0)) throw LoveError{LOVE_ERR_ARG, "outputscale must be > 0"};
+    if (!(sigma2 > 0.0)) throw LoveError{LOVE_ERR_ARG, "sigma^2 must be > 0"};
+    if (k < 1) throw LoveError{LOVE_ERR_ARG, "k must be >= 1"};
+    if (n_local < 0 || n_local >= (int64_t(1) << 31)) throw LoveError{LOVE_ERR_ARG, "bad n_local"};
+    if (n_local > 0 && (!X || !y)) throw LoveError{LOVE_ERR_ARG, "NULL X/y"};
+}
+
+}  // namespace
+
+}  // namespace love
+
+using namespace love;
+
+extern "C" {
+
+const char* love_last_error(void) { return t_err.c_str(); }
+int64_t love_launch_count(void) { return g_launch_count.load(); }
+int32_t love_abi_version(void) { return LOVE_ABI_VERSION; }
+
+love_status love_nccl_unique_id(void* out) {
+    if (!out) {
+        set_error("NULL out");
+        return LOVE_ERR_ARG;
+    }
+    return nccl_get_unique_id(out);
+}
+
+love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
+                             const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                             const love_dist* dist, void* stream, love_cache** out) {
+    Cache* c = nullptr;
+    cudaStream_t s = (cudaStream_t)stream;
+    try {
+        if (out) *out = nullptr;
+        validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
+        love_opts o{};
+        o.precision = LOVE_FP32;
+        if (opts) o = *opts;
+        if (o.precision != LOVE_FP32 && o.precision != LOVE_FP64) throw LoveError{LOVE_ERR_ARG, "bad precision"};
+        if (o.probe != LOVE_PROBE_Y) throw LoveError{LOVE_ERR_ARG, "only LOVE_PROBE_Y is implemented"};
+        if (o.prior != LOVE_PRIOR_SKI && o.prior != LOVE_PRIOR_EXACT) throw LoveError{LOVE_ERR_ARG, "bad prior"};
+        if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
+
+        c = new Cache();
+        cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
+        keep_pool_memory(c->device);
+        GridDev& g = c->g;
+        g.d = grid->d;
+        g.m_total = 1;
+        for (int d = 0; d < 3; ++d) {
+            g.m[d] = d < g.d ? (int)grid->m[d] : 1;
+            g.lo[d] = d < g.d ? grid->lo[d] : 0.0;
+            g.h[d] = d < g.d ? grid->h[d] : 1.0;
+        }
+        for (int d = g.d - 1, st = 1; d >= 0; --d) {
+            g.stride[d] = st;
+            st *= g.m[d];
+        }
+        for (int d = g.d; d < 3; ++d) g.stride[d] = 0;
+        for (int d = 0; d < g.d; ++d) g.m_total *= g.m[d];
+        c->rbf = *rbf;
+        c->sigma2 = sigma2;
+        c->precision = o.precision;
+        c->vsize = o.precision == LOVE_FP64 ? 8 : 4;
+        c->probe = o.probe;
+        c->prior = o.prior;
+        c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (o.precision == LOVE_FP64 ? 2 : 1);
+        c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
+        c->k_sample_req = o.k_sample;
+        c->n = n_local;
+        if (dist && dist->world > 1) {
+            if (dist->rank < 0 || dist->rank >= dist->world || !dist->nccl_unique_id)
+                throw LoveError{LOVE_ERR_ARG, "bad love_dist"};
+            c->world = dist->world;
+            c->rank = dist->rank;
+            nccl_comm_init(*c, dist->nccl_unique_id);
+        }
+        TempPool tmp(s);
+        // global n (k <= n_global)
+        {
+            int64_t* dn = (int64_t*)tmp.get(sizeof(int64_t));
+            cuda_check(cudaMemcpyAsync(dn, &c->n, sizeof(int64_t), cudaMemcpyHostToDevice, s), "n h2d");
+            allreduce_sum_i64(*c, dn, 1, s);
+            cuda_check(cudaMemcpyAsync(&c->n_global, dn, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "n d2h");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+        }
+        if (k > c->n_global) throw LoveError{LOVE_ERR_ARG, "k exceeds the number of training points"};
+        c->k_req = k;
+        const int M = g.m_total;
+        const size_t vs = c->vsize;
+        c->ldq = round_up(std::max<int64_t>(c->n, 1), 4);
+
+        // ---- interpolation records + cell sort
+        int* cell = (int*)tmp.get(sizeof(int) * std::max<int64_t>(c->n, 1));
+        double* frac64 = (double*)tmp.get(sizeof(double) * std::max<int64_t>(c->n, 1) * g.d);
+        int* dflag = (int*)tmp.get(sizeof(int) * 2);
+        cuda_check(cudaMemsetAsync(dflag, 0, sizeof(int) * 2, s), "memset");
+        c->perm = (int*)dalloc(*c, sizeof(int) * std::max<int64_t>(c->n, 1), s);
+        c->cell_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
+        c->cell_item_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
+        for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * std::max<int64_t>(c->n, 1), s);
+        c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);
+        {   // the range check is global: every rank must agree before continuing
+            float fl = 0.f;
+            int hflag = 0;
+            cuda_check(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+            if (c->world > 1) {
+                float* df = (float*)tmp.get(sizeof(float));
+                fl = (float)hflag;
+                cuda_check(cudaMemcpyAsync(df, &fl, sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
+                allreduce_sum(*c, df, 1, false, s);
+                cuda_check(cudaMemcpyAsync(&fl, df, sizeof(float), cudaMemcpyDeviceToHost, s), "d2h");
+                cuda_check(cudaStreamSynchronize(s), "sync");
+                hflag = fl > 0.f;
+            }
+            if (hflag) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
+        }
+        launch_counting_sort(*c, cell, frac64, y, c->n, c->Q, s);
+        c->n_items = count_items_host(*c, s);
+        c->item_cell = (int*)dalloc(*c, sizeof(int) * std::max<int64_t>(c->n_items, 1), s);
+        c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 1), s);
+        launch_build_items(*c, s);
+        c->M = dalloc(*c, vs * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
+
+        // ---- K_UU
+        setup_kuu(*c, s);
+
+        // ---- Lanczos state
+        c->r = dalloc(*c, vs * c->ldq, s);
+        c->u = dalloc(*c, vs * M, s);
+        c->z[0] = dalloc(*c, vs * M, s);
+        c->z[1] = dalloc(*c, vs * M, s);
+        c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
+        c->a = dalloc(*c, sizeof(double) * M, s);
+        c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
+        {
+            const size_t K = k;
+            const size_t nd = K + K + 2 * K * (K + 1) + 1 + (K + 1) + 5 * K + 2 + 1;
+            c->scal = (double*)dalloc(*c, sizeof(double) * nd, s);
+            double* p = c->scal;
+            LanczosState& st = c->st;
+            st.alpha_acc = p; p += K;
+            st.beta2_acc = p; p += K;
+            st.c_acc = p; p += 2 * K * (K + 1);
+            st.bnorm2 = p; p += 1;
+            st.qscale = p; p += K + 1;
+            st.alpha = p; p += K;
+            st.beta = p; p += K;
+            st.Ld = p; p += K;
+            st.Ls = p; p += K;
+            st.g = p; p += K;
+            st.amax_bmax = p; p += 2;
+            c->one = p; p += 1;
+            st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
+            st.rc_done = st.flags + 4;
+            LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
+        }
+
+        // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
+        run_lanczos(*c, s);
+        int hfl[4];
+        double bn2 = 0;
+        cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
+        cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+        cuda_check(cudaStreamSynchronize(s), "lanczos sync");
+        cuda_check(cudaGetLastError(), "lanczos kernels");
+        if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
+        if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
+        c->k_eff = hfl[1];
+        c->b_norm = std::sqrt(bn2);
+        c->h_alpha.resize(c->k_eff);
+        c->h_beta.resize(std::max(c->k_eff - 1, 0));
+        cuda_check(cudaMemcpy(c->h_alpha.data(), c->st.alpha, sizeof(double) * c->k_eff, cudaMemcpyDeviceToHost),
+                   "alpha d2h");
+        if (c->k_eff > 1)
+            cuda_check(cudaMemcpy(c->h_beta.data(), c->st.beta, sizeof(double) * (c->k_eff - 1),
+                                  cudaMemcpyDeviceToHost), "beta d2h");
+        finish_cache(*c, s);
+        if (c->k_sample_req > 0) build_sampling_cache(*c, s);
+        cuda_check(cudaStreamSynchronize(s), "build sync");
+        cuda_check(cudaGetLastError(), "build kernels");
+        *out = reinterpret_cast<love_cache*>(c);
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        if (c) {
+            cudaStreamSynchronize(s);
+            release(c);
+        }
+        return fail(e);
+    }
+}
+
+void love_free(love_cache* cache) { release(reinterpret_cast<Cache*>(cache)); }
+
+love_status love_cache_info(const love_cache* cache, love_info* info) {
+    try {
+        if (!cache || !info) throw LoveError{LOVE_ERR_ARG, "NULL cache/info"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        cuda_check(cudaDeviceSynchronize(), "sync");
+        unsigned long long cnt[2];
+        cuda_check(cudaMemcpy(cnt, c->counters, sizeof(cnt), cudaMemcpyDeviceToHost), "counters d2h");
+        std::memset(info, 0, sizeof(*info));
+        info->k_eff = c->k_eff;
+        info->k_pad = c->k_pad;
+        info->k_sample_eff = c->k_sample_eff;
+        info->precision = c->precision;
+        info->n_local = c->n;
+        info->n_global = c->n_global;
+        info->m_total = c->g.m_total;
+        info->n_items = c->n_items;
+        info->b_norm = c->b_norm;
+        info->alpha = c->h_alpha.data();
+        info->beta = c->h_beta.data();
+        info->n_negative_var = (int64_t)cnt[0];
+        info->n_out_of_range = (int64_t)cnt[1];
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_predict_var(const love_cache* cache, const double* Xs, int64_t t, void* var_out, void* mean_out,
+                             void* stream) {
+    try {
+        if (!cache || (t > 0 && (!Xs || !var_out)) || t < 0) throw LoveError{LOVE_ERR_ARG, "bad arguments"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (c->precision == LOVE_FP64)
+            launch_predict<double>(*c, Xs, nullptr, t, (double*)var_out, (double*)mean_out, s);
+        else
+            launch_predict<float>(*c, Xs, nullptr, t, (float*)var_out, (float*)mean_out, s);
+        cuda_check(cudaGetLastError(), "predict_var launch");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_predict_covar(const love_cache* cache, const double* Xa, const double* Xb, int64_t t,
+                               void* cov_out, void* stream) {
+    try {
+        if (!cache || (t > 0 && (!Xa || !Xb || !cov_out)) || t < 0) throw LoveError{LOVE_ERR_ARG, "bad arguments"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        cudaStream_t s = (cudaStream_t)stream;
+        if (c->precision == LOVE_FP64)
+            launch_predict<double>(*c, Xa, Xb, t, (double*)cov_out, nullptr, s);
+        else
+            launch_predict<float>(*c, Xa, Xb, t, (float*)cov_out, nullptr, s);
+        cuda_check(cudaGetLastError(), "predict_covar launch");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_sample(const love_cache* cache, const double* Xs, int64_t t, int64_t ns, uint64_t seed,
+                        const double* zeta, void* out, void* stream) {
+    try {
+        if (!cache || t < 0 || ns < 0 || ((t > 0 && ns > 0) && (!Xs || !out)))
+            throw LoveError{LOVE_ERR_ARG, "bad arguments"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        if (c->k_sample_eff <= 0 || c->S == nullptr)
+            throw LoveError{LOVE_ERR_STATE, "cache was built without a sampling root (k_sample = 0)"};
+        cudaStream_t s = (cudaStream_t)stream;
+        if (c->precision == LOVE_FP64) launch_sample<double>(*c, Xs, t, ns, seed, zeta, (double*)out, s);
+        else launch_sample<float>(*c, Xs, t, ns, seed, zeta, (float*)out, s);
+        cuda_check(cudaGetLastError(), "sample launch");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_ski_mvm(const love_cache* cache, const void* v, void* out, void* stream) {
+    try {
+        if (!cache || !v || !out) throw LoveError{LOVE_ERR_ARG, "NULL argument"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        if (c->world > 1) throw LoveError{LOVE_ERR_STATE, "love_ski_mvm needs a single-rank cache"};
+        cudaStream_t s = (cudaStream_t)stream;
+        TempPool tmp(s);
+        Cache w = *c;   // shallow copy with private scratch
+        w.allocs.clear();
+        const size_t vs = c->vsize;
+        void* vsrt = tmp.get(vs * c->ldq);
+        void* rs = tmp.get(vs * c->ldq);
+        void* u = tmp.get(vs * c->g.m_total);
+        void* z = tmp.get(vs * c->g.m_total);
+        w.M = tmp.get(vs * (size_t)(1 << (2 * c->g.d)) * std::max<int64_t>(c->n_items, 1));
+        if (c->fft_buf) w.fft_buf = tmp.get(2 * vs * c->fft_N);
+        if (c->ktmp[0]) {
+            w.ktmp[0] = tmp.get(vs * c->g.m_total);
+            w.ktmp[1] = tmp.get(vs * c->g.m_total);
+        }
+        if (c->precision == LOVE_FP64) {
+            launch_permute<double>(w, (const double*)v, (double*)vsrt, true, s);
+            launch_scatter<double>(w, (const double*)vsrt, c->one, (double*)u, s);
+            launch_kuu<double>(w, (const double*)u, (double*)z, s);
+            launch_gather<double>(w, (const double*)z, (const double*)vsrt, c->one, (double*)rs, nullptr, s);
+            launch_permute<double>(w, (const double*)rs, (double*)out, false, s);
+        } else {
+            launch_permute<float>(w, (const float*)v, (float*)vsrt, true, s);
+            launch_scatter<float>(w, (const float*)vsrt, c->one, (float*)u, s);
+            launch_kuu<float>(w, (const float*)u, (float*)z, s);
+            launch_gather<float>(w, (const float*)z, (const float*)vsrt, c->one, (float*)rs, nullptr, s);
+            launch_permute<float>(w, (const float*)rs, (float*)out, false, s);
+        }
+        cuda_check(cudaGetLastError(), "ski_mvm launch");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void* stream) {
+    try {
+        if (!cache || !u || !out) throw LoveError{LOVE_ERR_ARG, "NULL argument"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        cudaStream_t s = (cudaStream_t)stream;
+        TempPool tmp(s);
+        Cache w = *c;
+        w.allocs.clear();
+        const size_t vs = c->vsize;
+        if (c->fft_buf) w.fft_buf = tmp.get(2 * vs * c->fft_N);
+        if (c->ktmp[0]) {
+            w.ktmp[0] = tmp.get(vs * c->g.m_total);
+            w.ktmp[1] = tmp.get(vs * c->g.m_total);
+        }
+        if (c->precision == LOVE_FP64) launch_kuu<double>(w, (const double*)u, (double*)out, s);
+        else launch_kuu<float>(w, (const float*)u, (float*)out, s);
+        cuda_check(cudaGetLastError(), "kuu_mvm launch");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+love_status love_cache_export(const love_cache* cache, int32_t what, void* dst, int64_t capacity, int64_t* bytes,
+                              void* stream) {
+    try {
+        if (!cache) throw LoveError{LOVE_ERR_ARG, "NULL cache"};
+        const Cache* c = reinterpret_cast<const Cache*>(cache);
+        const void* src = nullptr;
+        int64_t nb = 0;
+        switch (what) {
+            case LOVE_EXPORT_RC: src = c->Rc; nb = (int64_t)c->vsize * c->g.m_total * c->k_pad; break;
+            case LOVE_EXPORT_MEAN: src = c->a; nb = (int64_t)sizeof(double) * c->g.m_total; break;
+            case LOVE_EXPORT_S: src = c->S; nb = (int64_t)c->vsize * c->g.m_total * c->ks_pad; break;
+            case LOVE_EXPORT_PERM: src = c->perm; nb = (int64_t)sizeof(int) * c->n; break;
+            default: throw LoveError{LOVE_ERR_ARG, "unknown export"};
+        }
+        if (bytes) *bytes = nb;
+        if (!dst) return LOVE_OK;
+        if (capacity < nb) throw LoveError{LOVE_ERR_ARG, "destination too small"};
+        if (!src || nb == 0) return LOVE_OK;
+        cuda_check(cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "export copy");
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        return fail(e);
+    }
+}
+
+}  // extern "C"

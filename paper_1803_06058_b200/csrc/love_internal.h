@@ -1,0 +1,152 @@
+// love_internal.h -- the cache object, device state layout and kernel launchers (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/love.h"
+#include "common.cuh"
+
+namespace love {
+
+// ---------------------------------------------------------------------------------------
+// Grid geometry.  Flat node index is row-major, last dimension fastest.
+// ---------------------------------------------------------------------------------------
+struct GridDev {
+    int d;
+    int m[3];
+    int stride[3];          // stride[d-1] = 1
+    double lo[3], h[3];
+    int m_total;
+};
+
+// Device-resident Lanczos state (fp64).  Written only by lanczos_scalars_kernel / the
+// finalize kernel; the accumulators are summed into with atomics by the step kernels and
+// (multi-GPU) all-reduced between kernels.
+struct LanczosState {
+    double* alpha_acc;     // [k]        q_j^T A q_j partial sums
+    double* beta2_acc;     // [k]        ||q~_{j+1}||^2 partial sums
+    double* c_acc;         // [2][k][k+1] reorthogonalisation dots (pass 0 and pass 1)
+    double* bnorm2;        // [1]        ||b||^2
+    double* qscale;        // [k+1]      1/||q~_j|| (lazy normalisation of Q's columns)
+    double* alpha;         // [k]
+    double* beta;          // [k]
+    double* Ld;            // [k]        L_jj
+    double* Ls;            // [k]        L_{j+1,j}
+    double* g;             // [k]        L^{-1} e_1
+    double* amax_bmax;     // [2]
+    int* flags;            // [4]        done, k_eff, notpd, zero_probe
+    int* rc_done;          // [1]        Rc columns written
+};
+
+struct Cache {
+    // ---------------- configuration
+    GridDev g;
+    love_rbf rbf;
+    double sigma2 = 0;
+    int precision = LOVE_FP32;
+    int probe = LOVE_PROBE_Y, prior = LOVE_PRIOR_SKI, reorth_passes = 1;
+    double tol = 0;
+    int k_req = 0, k_sample_req = 0;
+    int rank = 0, world = 1;
+    void* comm = nullptr;               // ncclComm_t
+    int device = 0;
+    size_t vsize = 4;                   // sizeof(V)
+
+    // ---------------- training points (sorted by flat cell)
+    int64_t n = 0, n_global = 0, ldq = 0;
+    int64_t n_items = 0;
+    void* frac[3] = {nullptr, nullptr, nullptr};   // V[n] per dim (sorted order)
+    int* perm = nullptr;                 // [n] sorted -> original
+    int* cell_start = nullptr;           // [m_total+1]
+    int* cell_item_start = nullptr;      // [m_total+1]
+    int* item_cell = nullptr;            // [n_items]
+    int* item_start = nullptr;           // [n_items+1]
+
+    // ---------------- K_UU
+    double* cols64 = nullptr;            // [sum m_d] Toeplitz first columns (fp64)
+    void* cols = nullptr;                // same in V
+    int fft_N = 0, fft_N1 = 0, fft_N2 = 0;
+    void* lam = nullptr;                 // V[N] eigenvalues * s^2/N in pass-B layout
+    void* fft_buf = nullptr;             // complex V[N]
+    void* ktmp[2] = {nullptr, nullptr};  // V[m] scratch for axis passes
+
+    // ---------------- Lanczos
+    int k_alloc = 0;
+    void* Q = nullptr;                   // V[ldq * (k+1)] column-major, unnormalised columns
+    void* r = nullptr;                   // V[ldq]
+    void* u = nullptr;                   // V[m]
+    void* z[2] = {nullptr, nullptr};     // V[m]
+    void* M = nullptr;                   // V[4^d * n_items] per-item stencil moments
+    void* Rc_col = nullptr;              // double[m * k] column-major (build only)
+    void* Rc = nullptr;                  // V[m * k_pad] row-major
+    void* a = nullptr;                   // double[m] mean cache
+    double* one = nullptr;               // device 1.0 (scale of un-normalised MVMs)
+    double* scal = nullptr;              // backing store of LanczosState
+    LanczosState st;
+    unsigned long long* counters = nullptr;   // [2] negative variances, out-of-range queries
+
+    // ---------------- results
+    int k_eff = 0, k_pad = 0;
+    int k_sample_eff = 0, ks_pad = 0;
+    void* S = nullptr;                   // V[m * ks_pad] row-major sampling root
+    double b_norm = 0;
+    std::vector<double> h_alpha, h_beta;
+
+    std::vector<void*> allocs;           // everything to release
+};
+
+// ---------------------------------------------------------------------------------------
+// Error plumbing
+// ---------------------------------------------------------------------------------------
+void set_error(const std::string& msg);
+struct LoveError {
+    love_status status;
+    std::string msg;
+};
+void cuda_check(cudaError_t e, const char* what);
+void* dalloc(Cache& c, size_t bytes, cudaStream_t s);   // zero-filled, owned by the cache
+
+// ---------------------------------------------------------------------------------------
+// Launchers (each file defines its own kernels; V = float | double)
+// ---------------------------------------------------------------------------------------
+// interp.cu
+void launch_interp_points(const Cache& c, const double* X, int64_t n, int* cell, double* frac64,
+                          int* range_flag, cudaStream_t s);
+void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const double* y,
+                          int64_t n, void* b_out, cudaStream_t s);   // fills perm, frac, cells
+void launch_build_items(Cache& c, cudaStream_t s);                 // after n_items known
+int64_t count_items_host(Cache& c, cudaStream_t s);                 // syncs
+// ski.cu
+template <typename V> void launch_scatter(const Cache& c, const V* q, const double* scale,
+                                          V* u, cudaStream_t s);
+template <typename V> void launch_gather(const Cache& c, const V* z, const V* q,
+                                         const double* qscale, V* r, double* alpha_acc,
+                                         cudaStream_t s);
+template <typename V> void launch_permute(const Cache& c, const V* in, V* out, bool to_sorted,
+                                          cudaStream_t s);
+// kuu.cu
+void setup_kuu(Cache& c, cudaStream_t s);
+template <typename V> void launch_kuu(const Cache& c, const V* u, V* z, cudaStream_t s);
+// lanczos.cu
+void run_lanczos(Cache& c, cudaStream_t s);
+void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
+// query.cu
+template <typename V> void launch_predict(const Cache& c, const double* Xa, const double* Xb,
+                                          int64_t t, V* out, V* mean_out, cudaStream_t s);
+// sample.cu
+void build_sampling_cache(Cache& c, cudaStream_t s);
+template <typename V> void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns,
+                                         uint64_t seed, const double* zeta, V* out,
+                                         cudaStream_t s);
+// nccl_shim.cpp
+bool nccl_available(std::string* why);
+love_status nccl_get_unique_id(void* out128);
+love_status nccl_comm_init(Cache& c, const void* id128);
+void nccl_comm_destroy(Cache& c);
+void allreduce_sum(const Cache& c, void* buf, int64_t count, bool is_double, cudaStream_t s);
+void allreduce_sum_i64(const Cache& c, int64_t* buf, int64_t count, cudaStream_t s);
+
+}  // namespace love

@@ -1,0 +1,118 @@
+// nccl_shim.cpp -- the NCCL sharding layer: per Lanczos step one m-length
+// all-reduce of the scattered vector u = W_X q (each rank scatters its own points) and the
+// scalar / j-length all-reduces of alpha, the reorthogonalisation dots and beta^2.
+// NCCL is loaded at run time (dlopen) so single-GPU use never needs it; the torch-bundled
+// libnccl.so.2 is already resident when the Python binding runs.
+#include <dlfcn.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "love_internal.h"
+
+namespace love {
+
+namespace {
+
+typedef struct { char internal[128]; } NcclUniqueId;
+typedef void* NcclComm;
+typedef int NcclResult;
+enum { kNcclInt64 = 4, kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclSum = 0 };
+
+struct NcclApi {
+    NcclResult (*GetUniqueId)(NcclUniqueId*) = nullptr;
+    NcclResult (*CommInitRank)(NcclComm*, int, NcclUniqueId, int) = nullptr;
+    NcclResult (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    NcclResult (*CommDestroy)(NcclComm) = nullptr;
+    const char* (*GetErrorString)(NcclResult) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+NcclApi& api() {
+    static NcclApi a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* env = std::getenv("LOVE_NCCL_LIB");
+        const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+        void* h = nullptr;
+        for (const char* nm : names) {
+            if (nm == nullptr || !*nm) continue;
+            h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) {
+            a.why = "could not dlopen libnccl.so.2 (set LOVE_NCCL_LIB)";
+            return;
+        }
+        a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+        a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+        a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+        a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.AllReduce && a.CommDestroy && a.GetErrorString;
+        if (!a.ok) a.why = "libnccl is missing a required symbol";
+    });
+    return a;
+}
+
+void nccl_check(NcclResult r, const char* what) {
+    if (r != 0) throw LoveError{LOVE_ERR_NCCL, std::string(what) + ": " + api().GetErrorString(r)};
+}
+
+}  // namespace
+
+bool nccl_available(std::string* why) {
+    NcclApi& a = api();
+    if (!a.ok && why) *why = a.why;
+    return a.ok;
+}
+
+love_status nccl_get_unique_id(void* out128) {
+    NcclApi& a = api();
+    if (!a.ok) {
+        set_error(a.why);
+        return LOVE_ERR_NCCL;
+    }
+    NcclUniqueId id;
+    const NcclResult r = a.GetUniqueId(&id);
+    if (r != 0) {
+        set_error(std::string("ncclGetUniqueId: ") + a.GetErrorString(r));
+        return LOVE_ERR_NCCL;
+    }
+    std::memcpy(out128, &id, sizeof(id));
+    return LOVE_OK;
+}
+
+love_status nccl_comm_init(Cache& c, const void* id128) {
+    NcclApi& a = api();
+    if (!a.ok) throw LoveError{LOVE_ERR_NCCL, a.why};
+    NcclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    NcclComm comm = nullptr;
+    nccl_check(a.CommInitRank(&comm, c.world, id, c.rank), "ncclCommInitRank");
+    c.comm = comm;
+    return LOVE_OK;
+}
+
+void nccl_comm_destroy(Cache& c) {
+    if (c.comm && api().ok) api().CommDestroy((NcclComm)c.comm);
+    c.comm = nullptr;
+}
+
+void allreduce_sum(const Cache& c, void* buf, int64_t count, bool is_double, cudaStream_t s) {
+    if (c.world <= 1 || count <= 0) return;
+    nccl_check(api().AllReduce(buf, buf, (size_t)count, is_double ? kNcclFloat64 : kNcclFloat32, kNcclSum,
+                               (NcclComm)c.comm, s),
+               "ncclAllReduce");
+}
+
+void allreduce_sum_i64(const Cache& c, int64_t* buf, int64_t count, cudaStream_t s) {
+    if (c.world <= 1 || count <= 0) return;
+    nccl_check(api().AllReduce(buf, buf, (size_t)count, kNcclInt64, kNcclSum, (NcclComm)c.comm, s),
+               "ncclAllReduce");
+}
+
+}  // namespace love

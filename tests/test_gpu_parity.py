@@ -1,0 +1,217 @@
+"""Parity of the CUDA path (through the C ABI) with the fp64 oracle, element by element on the
+same seeded inputs.  Tolerances (reading A21):
+  fp64 mode: |v - v_or| <= 1e-9 |v_or| + 1e-13 P(x*)
+  fp32 mode: |v - v_or| <= 1e-3 |v_or| + 1e-6  P(x*)
+where P(x*) is the prior variance.  Operators (K_UU, SKI MVM) are compared in relative 2-norm.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import CONFIGS, make_inputs, scaled_config, tiny_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _love():
+    from paper_1803_06058_b200 import LoveCache, LoveError
+    return LoveCache, LoveError
+
+
+def _model(p, inp):
+    return O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+
+
+def _build(p, inp, **kw):
+    LoveCache, _ = _love()
+    kw.setdefault("precision", p.precision)
+    return LoveCache.build(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2,
+                           kw.pop("k", p.k), **kw)
+
+
+def _prior(model, X):
+    ia, wa = O.interp(X, model.m, model.lo, model.h)
+    return O.prior_ski(model, ia, wa, ia, wa)
+
+
+def _assert_var(got, want, prior, fp64):
+    a, b = (1e-9, 1e-13) if fp64 else (1e-3, 1e-6)
+    err = np.abs(got - want)
+    bound = a * np.abs(want) + b * prior
+    worst = np.argmax(err / bound)
+    assert np.all(err <= bound), (f"max err/bound {np.max(err / bound):.3g} at {worst}: got {got[worst]} "
+                                  f"want {want[worst]} prior {prior[worst]}; "
+                                  f"max rel {np.max(err / np.abs(want)):.3g}")
+
+
+def _rel2(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+# ------------------------------------------------------------------ K_UU MVM
+@pytest.mark.parametrize("case", [
+    ("cfg1", 1, None, "fp64"), ("cfg1_fp32", 1, None, "fp32"), ("cfg5m", 5, None, "fp32"),
+    ("cfg2m", 2, None, "fp32"), ("cfg3m", 3, None, "fp32"), ("cfg4m", 4, None, "fp32"),
+    ("1d_4096", 1, (4096,), "fp32"), ("1d_2049_fp64", 1, (2049,), "fp64"), ("3d_odd", 4, (9, 10, 11), "fp64"),
+])
+def test_kuu_mvm(case):
+    name, ci, m, prec = case
+    p = scaled_config(ci, n=64, t=10, precision=prec, m=m, k=2)
+    # training points only need to be valid: put them in the middle of the grid
+    from synth.inputs import Inputs
+    ctr = np.array([lo + (mm // 2 + 0.25) * h for lo, mm, h in zip(p.lo, p.m, p.h)])
+    X = np.repeat(ctr[None, :], p.n, 0)
+    y = np.random.default_rng(1).normal(size=p.n)
+    c = _build(p, Inputs(X, y, X[:2]))
+    rng = np.random.default_rng(7)
+    u = rng.normal(size=p.m_total)
+    got = c.kuu_mvm(torch.tensor(u, dtype=c.vdtype, device="cuda")).double().cpu().numpy()
+    cols = [O.rbf_column(p.m[d], p.h[d], p.lengthscale[d]) for d in range(p.d)]
+    want = O.kuu_matvec(cols, p.outputscale, u)
+    tol = 1e-12 if prec == "fp64" else 2e-6 * max(1.0, np.log2(p.m_total))
+    assert _rel2(got, want) < tol, _rel2(got, want)
+
+
+# ------------------------------------------------------------------ SKI MVM
+@pytest.mark.parametrize("case", [("1d_n40", "fp64"), ("1d_n200", "fp32"), ("2d", "fp64"), ("3d", "fp64"),
+                                  ("2d", "fp32"), ("3d", "fp32")])
+def test_ski_mvm_tiny(case):
+    kind, prec = case
+    p, inp = tiny_problem(kind)
+    c = _build(p, inp, precision=prec, k=2)
+    model = _model(p, inp)
+    v = np.random.default_rng(3).normal(size=p.n)
+    got = c.ski_mvm(torch.tensor(v, dtype=c.vdtype, device="cuda")).double().cpu().numpy()
+    want = O.ski_mvm(model, v)
+    assert _rel2(got, want) < (1e-12 if prec == "fp64" else 1e-5)
+
+
+@pytest.mark.parametrize("ci,n,m", [(2, 50_003, (5000,)), (3, 40_001, (64, 64)), (4, 100_003, (24, 24, 24))])
+def test_ski_mvm_scaled(ci, n, m):
+    p = scaled_config(ci, n=n, m=m, k=2)
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    model = _model(p, inp)
+    v = np.random.default_rng(5).normal(size=p.n)
+    got = c.ski_mvm(torch.tensor(v, dtype=torch.float32, device="cuda")).double().cpu().numpy()
+    want = O.ski_mvm(model, v)
+    assert _rel2(got, want) < 1e-5
+
+
+# ------------------------------------------------------------------ full LOVE pipeline
+def test_cfg1_fp64_end_to_end():
+    """Config 1 exactly as BASELINE.json states it (fp64, n=1000, m=256, k=50, t=1000)."""
+    p = CONFIGS[1]
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    var, mean = c.predict_var(inp.Xs, return_mean=True)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    info = c.info()
+    assert info["k_eff"] == oc.lanczos.k_eff
+    k = info["k_eff"]
+    np.testing.assert_allclose(info["alpha"], oc.lanczos.alpha[:k], rtol=1e-9)
+    np.testing.assert_allclose(info["beta"][:k - 2], oc.lanczos.beta[:k - 2], rtol=1e-6)
+    ov = O.predict_var(model, oc, inp.Xs)
+    _assert_var(var.cpu().numpy(), ov, _prior(model, inp.Xs), fp64=True)
+    om = O.predict_mean(model, oc, inp.Xs)
+    np.testing.assert_allclose(mean.cpu().numpy(), om, atol=1e-9 * np.abs(om).max())
+
+
+@pytest.mark.parametrize("ci,n,m,k,t", [
+    (2, 60_001, (6000,), 40, 3001),          # 1-D four-step FFT, ragged n and t
+    (3, 30_007, (48, 48), 40, 2003),         # 2-D Kronecker
+    (4, 60_013, (20, 20, 20), 40, 2005),     # 3-D Kronecker
+    (5, 20_011, (2000,), 30, 1999),          # config-5 data, shorter grid
+])
+def test_scaled_fp32_variances_and_covariances(ci, n, m, k, t):
+    p = scaled_config(ci, n=n, m=m, k=k, t=t)
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    var, mean = c.predict_var(inp.Xs, return_mean=True)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    info = c.info()
+    assert info["k_eff"] == oc.lanczos.k_eff == k
+    np.testing.assert_allclose(info["alpha"], oc.lanczos.alpha, rtol=2e-4)
+    ov = O.predict_var(model, oc, inp.Xs)
+    prior = _prior(model, inp.Xs)
+    _assert_var(var.cpu().numpy().astype(np.float64), ov, prior, fp64=False)
+    om = O.predict_mean(model, oc, inp.Xs)
+    assert np.max(np.abs(mean.cpu().numpy() - om)) < 1e-3 * np.abs(om).max()
+    # covariances on pairs (Xs[i], Xs[perm i])
+    Xb = inp.Xs[np.random.default_rng(1).permutation(t)]
+    cov = c.predict_covar(inp.Xs, Xb).cpu().numpy().astype(np.float64)
+    ocov = O.predict_covar(model, oc, inp.Xs, Xb)
+    scale = np.sqrt(prior * _prior(model, Xb))
+    assert np.all(np.abs(cov - ocov) <= 1e-3 * np.abs(ocov) + 1e-6 * scale)
+    # symmetry cov(a,b) == cov(b,a)
+    cov2 = c.predict_covar(Xb, inp.Xs).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(cov - cov2)) <= 1e-6 * scale.max()
+
+
+@pytest.mark.parametrize("kind", ["1d_n40", "1d_n200", "2d", "3d"])
+def test_full_krylov_equals_dense_gp(kind):
+    """fp64 GPU run to breakdown reproduces the dense-Cholesky SKI GP (north_star <= 1e-4 at k=n)."""
+    p, inp = tiny_problem(kind)
+    c = _build(p, inp, precision="fp64")
+    var = c.predict_var(inp.Xs).cpu().numpy()
+    model = _model(p, inp)
+    _, dvar = O.dense_ski_gp(model, inp.Xs)
+    assert c.info()["k_eff"] < p.k
+    assert np.max(np.abs(var - dvar) / dvar) < 1e-6
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_cases():
+    LoveCache, LoveError = _love()
+    p = scaled_config(1, n=301, t=5, k=10)
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    assert c.predict_var(np.zeros((0, 1))).numel() == 0                 # empty query batch
+    bad = np.array([[-1.0], [0.5], [2.0]])                               # outside the grid
+    v = c.predict_var(bad).cpu().numpy()
+    assert np.isnan(v[0]) and np.isnan(v[2]) and np.isfinite(v[1])
+    assert c.info()["n_out_of_range"] == 2
+    with pytest.raises(LoveError) as e:                                   # training point off-grid
+        LoveCache.build(np.array([[0.5], [1.2]]), np.ones(2), p.m, p.lo, p.h, p.lengthscale, 1.0, 0.01, 1)
+    assert e.value.status == 2
+    with pytest.raises(LoveError) as e:                                   # zero probe
+        LoveCache.build(inp.X, np.zeros(p.n), p.m, p.lo, p.h, p.lengthscale, 1.0, 0.01, 3)
+    assert e.value.status == 4
+    c1 = _build(p, inp, k=1)                                              # k = 1
+    assert c1.info()["k_eff"] == 1
+    model = _model(p, inp)
+    oc = O.love_precompute(model, 1)
+    _assert_var(c1.predict_var(inp.Xs).cpu().numpy(), O.predict_var(model, oc, inp.Xs),
+                _prior(model, inp.Xs), fp64=True)
+
+
+def test_identity_like_breakdown():
+    """All training points in one cell with equal weights -> the Krylov space of y under
+    K_hat = W^T K W + s2 I has dimension <= 2: breakdown must stop at k_eff <= 2 (A12)."""
+    p = scaled_config(1, n=64, t=4, k=10)
+    X = np.full((64, 1), 0.5)
+    y = np.random.default_rng(0).normal(size=64)
+    LoveCache, _ = _love()
+    c = LoveCache.build(X, y, p.m, p.lo, p.h, p.lengthscale, 1.0, 0.01, 10, precision="fp64")
+    assert c.info()["k_eff"] <= 2
+    from synth.inputs import Inputs
+    model = _model(p, Inputs(X, y, X[:4]))
+    oc = O.love_precompute(model, 10)
+    assert oc.lanczos.k_eff == c.info()["k_eff"]
+    _assert_var(c.predict_var(np.array([[0.3], [0.5]])).cpu().numpy(),
+                O.predict_var(model, oc, np.array([[0.3], [0.5]])),
+                _prior(model, np.array([[0.3], [0.5]])), fp64=True)
+
+
+def test_prior_exact_mode():
+    p = scaled_config(1, n=500, t=200, k=30)
+    inp = make_inputs(p)
+    c = _build(p, inp, prior="exact")
+    var = c.predict_var(inp.Xs).cpu().numpy()
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    ov = O.predict_var(model, oc, inp.Xs, prior="exact")
+    _assert_var(var, ov, np.full(len(ov), p.outputscale), fp64=True)
