@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""LOVE / KISS-GP hot-path benchmark (contract: one JSON line on rank 0).
+
+A step = one pass of the whole hot path of SURVEY.md §8(a) over one batch of synthetic
+input: love_build_cache (interpolation + sort, k Lanczos steps with full
+reorthogonalisation, streamed Cholesky / Rc / mean cache) followed by predict_var on the
+t test points.  Workload at N=1: BASELINE.json configs[1] (config 2: n=1e6, m=1e5, k=100,
+t=1e6, fp32 with fp64 reductions).  N>1 (torchrun, one rank per GPU): weak scaling -- every
+rank holds its own n-point shard (seeded by rank) of one global training set and its own
+t test points; the per-step exchange is NCCL over NVLink inside the library.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl love|reference] [--config 2]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "predictive variances/sec + LOVE cache-build ms at n,m,k; % of HBM roofline"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0      # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="love", choices=["love", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def reorth_bytes(n_local: int, k: int, vsize: int, passes: int = 1) -> dict:
+    """Algorithmic bytes of the reorthogonalisation kernels over one build:
+    step j (0-based, j < k-1) with c = j+1 stored columns:
+      dots   : c*n*s_v (Q~ columns) + n*s_v (r)
+      update : c*n*s_v (Q~ columns) + n*s_v (r) + n*s_v (new column written)"""
+    dots = upd = 0
+    for j in range(k - 1):
+        ccols = j + 1
+        dots += passes * (ccols * n_local * vsize + n_local * vsize)
+        upd += passes * (ccols * n_local * vsize + 2 * n_local * vsize)
+    return {"dots": dots, "update": upd}
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle arm
+def run_oracle_step(p, inp, t_sample):
+    """One step of the fp64 CPU oracle: paper-literal build + variance queries on t_sample
+    points.  Returns (build_s, query_s)."""
+    import oracle as O
+    t0 = time.perf_counter()
+    model = O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+    cache = O.love_precompute(model, p.k)
+    t1 = time.perf_counter()
+    O.predict_var(model, cache, inp.Xs[:t_sample])
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(p, inp, t_sample=50_000):
+    """The oracle as it stands, on this host's cores, full build + a bounded query sample;
+    the step time is scaled to the full t (queries are independent and O(k) each)."""
+    b, q = run_oracle_step(p, inp, t_sample)
+    step = b + q * (p.t / t_sample)
+    return {"value": p.t / step, "unit": "variances/s", "cores": oracle_threads(), "kind": "oracle",
+            "sample": f"full {p.name} build (n={p.n}, m={p.m_total}, k={p.k}) + predict_var on {t_sample} "
+                      f"of {p.t} test points, query time scaled x{p.t / t_sample:.0f}",
+            "build_s": round(b, 3), "query_s_sample": round(q, 3)}
+
+
+def reference_arm(args, p):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth import make_inputs
+    inp = make_inputs(p)
+    budget_s = 200.0
+    est = sum(run_oracle_step(p, inp, 20_000))       # calibration, untimed
+    per_step_budget = budget_s / max(1, args.steps + args.warmup)
+    t_sample = p.t
+    if est * 1.5 > per_step_budget:
+        t_sample = 20_000
+    for _ in range(args.warmup):
+        run_oracle_step(p, inp, t_sample)
+    times = []
+    for _ in range(args.steps):
+        b, q = run_oracle_step(p, inp, t_sample)
+        times.append(b + q * (p.t / t_sample))
+    step = float(np.mean(times))
+    value = p.t / step
+    sample = (f"full {p.name} build + predict_var on {t_sample} of {p.t} test points"
+              + (f", query time scaled x{p.t / t_sample:.0f}" if t_sample < p.t else ""))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "variances/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.name, "n": p.n, "m": p.m_total, "k": p.k, "t": p.t},
+        "cpu_baseline": {"kind": "oracle", "cores": oracle_threads(), "sample": sample, "value": value,
+                         "unit": "variances/s"},
+        "e2e": {"value": value, "unit": "variances/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- LOVE arm
+def main():
+    args = parse()
+    from synth import get_config
+    p = get_config(args.config)
+    if args.impl == "reference":
+        reference_arm(args, p)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1803_06058_b200 import LoveCache, launch_count, nccl_unique_id
+    from paper_1803_06058_b200 import _abi
+    from synth import make_inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    inp = make_inputs(p, seed=p.seed + rank)           # this rank's shard (weak scaling)
+    X = torch.from_numpy(inp.X).to(dev)
+    y = torch.from_numpy(inp.y).to(dev)
+    Xs = torch.from_numpy(inp.Xs).to(dev)
+    kw = dict(m=p.m, lo=p.lo, h=p.h, lengthscale=p.lengthscale, outputscale=p.outputscale, sigma2=p.sigma2,
+              k=p.k, precision=p.precision, rank=rank, world=world, nccl_id=nccl_id)
+    lib = _abi.load()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
+
+    def step(Xd, yd, Xsd, e2e=False):
+        c = LoveCache.build(Xd, yd, **kw)
+        var = c.predict_var(Xsd)
+        if e2e:
+            var = var.cpu()
+        c.free()
+        return var
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step(X, y, Xs)
+    barrier()
+
+    # ---------------- timed region: K steps, device events, L2 flushed between steps
+    stream = torch.cuda.current_stream()
+    lib.love_profile_read(None, None, 1)
+    lib.love_profile_enable(1)
+    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                          else local_rank)
+    clocks.start()
+    launches0 = launch_count()
+    total_ms = 0.0
+    build_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.zero_()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        c = LoveCache.build(X, y, **kw)
+        e1.record(stream)
+        c.predict_var(Xs)
+        e2.record(stream)
+        e2.synchronize()
+        total_ms += e0.elapsed_time(e2)
+        build_ms.append(e0.elapsed_time(e1))
+        c.free()
+    barrier()
+    launches = launch_count() - launches0
+    clk = clocks.stop()
+    lib.love_profile_enable(0)
+    import ctypes
+    ms_arr = (ctypes.c_double * len(_abi.PROF_NAMES))()
+    calls_arr = (ctypes.c_int64 * len(_abi.PROF_NAMES))()
+    lib.love_profile_read(ms_arr, calls_arr, 1)
+    prof_ms = {nm: ms_arr[i] / args.steps for i, nm in enumerate(_abi.PROF_NAMES)}
+    t_step = torch.tensor([total_ms / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t_step.item())
+    value = world * p.t / (ms_per_step / 1e3)
+
+    # ---------------- roofline of the dominant kernels (reorthogonalisation)
+    peak, peak_src = hbm_peak()
+    vs = 8 if p.precision == "fp64" else 4
+    rb = reorth_bytes(p.n, p.k, vs)
+    reorth_ms = prof_ms["reorth_dots"] + prof_ms["reorth_update"]
+    achieved = (rb["dots"] + rb["update"]) / (reorth_ms / 1e3) / 1e9 if reorth_ms > 0 else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic_r01.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(p.name)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": "reorth_dots + reorth_update (full reorthogonalisation)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src,
+                "algorithmic_bytes_per_build": rb["dots"] + rb["update"],
+                "share_of_step": reorth_ms / ms_per_step if ms_per_step else None}
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(inp.X).pin_memory()
+        yh = torch.from_numpy(inp.y).pin_memory()
+        Xsh = torch.from_numpy(inp.Xs).pin_memory()
+        barrier()
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step(Xh, yh, Xsh, e2e=True)
+            b.record(stream)
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        te = torch.tensor([tot / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * p.t / (float(te.item()) / 1e3), "unit": "variances/s",
+               "h2d_bytes_per_step": int(inp.X.nbytes + inp.y.nbytes + inp.Xs.nbytes),
+               "d2h_bytes_per_step": int(p.t * vs), "ms_per_step": float(te.item())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(p, inp)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "variances/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if p.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": p.name, "n_per_gpu": p.n, "m": p.m_total, "k": p.k, "t_per_gpu": p.t,
+                       "d": p.d, "l2": "flushed (256 MB write) between timed steps",
+                       "parallelism": f"dp{world} (training + test points sharded, NCCL all-reduce per step)"},
+            "build_ms": float(np.mean(build_ms)),
+            "query_variances_per_s": p.t / ((ms_per_step - float(np.mean(build_ms))) / 1e3),
+            "phase_ms_per_step": {k: round(v, 4) for k, v in prof_ms.items() if v > 0},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

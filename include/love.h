@@ -113,7 +113,7 @@ typedef struct {
  *   grid, rbf, opts : HOST structs (opts may be NULL => defaults).
  *   sigma2          : observation noise variance sigma^2 > 0.
  *   X               : n_local x d fp64, row-major.  y : n_local fp64.
- *   k               : Lanczos steps (1 <= k <= n_global).
+ *   k               : Lanczos steps, k >= 1 (k > n_global is clamped to n_global).
  *   dist            : HOST struct or NULL.
  *   out             : HOST pointer receiving the new cache.
  * Runs: interpolation indices/weights, cell sort, K_UU setup, k steps
@@ -172,7 +172,7 @@ love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void
 
 enum {
     LOVE_EXPORT_RC = 0,        /* m_total x k_pad of V, row-major: Rc = K_UU W_X Q L^{-T} */
-    LOVE_EXPORT_MEAN = 1,      /* m_total of V: mean cache a */
+    LOVE_EXPORT_MEAN = 1,      /* m_total fp64: mean cache a */
     LOVE_EXPORT_S = 2,         /* m_total x k_sample_eff of V, row-major: sampling root */
     LOVE_EXPORT_PERM = 3       /* n_local int32: sorted position -> original point index */
 };
@@ -189,6 +189,32 @@ int64_t love_launch_count(void);
 
 /* LOVE_ABI_VERSION of the loaded library. */
 int32_t love_abi_version(void);
+
+/* --------------------------------------------------------------------------------------
+ * Phase timing (tracing).  When enabled, the library brackets each phase's kernels with
+ * CUDA events on the launching stream; love_profile_read synchronises the device,
+ * accumulates the elapsed times and returns per-phase totals (ms) and launch-group counts.
+ * Process-global, meant for single-threaded benchmarking.
+ * ------------------------------------------------------------------------------------ */
+enum {
+    LOVE_PROF_SETUP = 0,         /* interpolation records, cell sort, items, K_UU setup */
+    LOVE_PROF_SCATTER = 1,       /* u = W q (moments + node pull) */
+    LOVE_PROF_KUU = 2,           /* z = K_UU u */
+    LOVE_PROF_GATHER = 3,        /* r = W^T z + sigma^2 q, alpha */
+    LOVE_PROF_REORTH_DOTS = 4,   /* c = Q^T r' */
+    LOVE_PROF_REORTH_UPDATE = 5, /* q~ = r' - Q c, beta^2 */
+    LOVE_PROF_SCALARS = 6,       /* tridiagonal Cholesky / breakdown bookkeeping, Rc and a streaming */
+    LOVE_PROF_FINISH = 7,        /* Rc transpose */
+    LOVE_PROF_QUERY = 8,         /* predict_var / predict_covar */
+    LOVE_PROF_SAMPLE_CACHE = 9,  /* sampling root */
+    LOVE_PROF_SAMPLE = 10,       /* sample draws */
+    LOVE_PROF_COMM = 11,         /* NCCL all-reduces */
+    LOVE_PROF_N = 12
+};
+void love_profile_enable(int32_t on);
+/* ms_out, calls_out: HOST arrays of LOVE_PROF_N entries (either may be NULL); reset != 0
+ * clears the totals after reading. */
+love_status love_profile_read(double* ms_out, int64_t* calls_out, int32_t reset);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,8 @@ LOVE_FP32, LOVE_FP64 = 0, 1
 LOVE_PROBE_Y, LOVE_PROBE_AVGCOL = 0, 1
 LOVE_PRIOR_SKI, LOVE_PRIOR_EXACT = 0, 1
 LOVE_EXPORT_RC, LOVE_EXPORT_MEAN, LOVE_EXPORT_S, LOVE_EXPORT_PERM = 0, 1, 2, 3
+PROF_NAMES = ["setup", "scatter", "kuu", "gather", "reorth_dots", "reorth_update", "scalars_rc",
+              "finish", "query", "sample_cache", "sample", "comm"]
 
 
 class love_grid(ctypes.Structure):
@@ -69,6 +71,8 @@ SIGNATURES = {
     "love_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "love_launch_count": (ctypes.c_int64, []),
     "love_abi_version": (ctypes.c_int32, []),
+    "love_profile_enable": (None, [ctypes.c_int32]),
+    "love_profile_read": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]),
 }
 
 _lib = None

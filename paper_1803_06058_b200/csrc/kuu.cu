@@ -1,13 +1,17 @@
-// kuu.cu -- structured K_UU MVMs on the regular grid.
+// kuu.cu -- structured K_UU MVMs on the regular grid, fp64 on the m side.
 //
-// d = 1 (Toeplitz): K_UU u = first m entries of IFFT(lambda * FFT([u; 0])) with the circulant
+// The m-sized side of the SKI MVM (u = W q, z = K_UU u) is always computed and stored in
+// fp64, also in LOVE_FP32 mode: it is cheap (m << n) and it is what keeps fp32-mode
+// variances inside the parity bound when var << prior ("Precision plan").
+//
+// d = 1 (Toeplitz): z = first m entries of IFFT(lambda * FFT([u; 0])) with the circulant
 //   embedding of length N = 2^ceil(log2(2m-1)) (reading A25).  Hand-written shared-memory
-//   radix-2 Stockham FFTs: one CTA for N <= 4096 (fp32) / 2048 (fp64), otherwise the
+//   Stockham FFTs with radix-8 register butterflies: one CTA for N <= 4096, otherwise the
 //   four-step factorisation N = N1 * N2 in three passes whose middle pass does
-//   forward FFT -> multiply by lambda -> inverse FFT on the same smem lines (no transposes).
-//   lambda (scaled by s^2/N) is computed once per build with the same kernels in fp64.
+//   forward FFT -> multiply by lambda -> inverse FFT on the same lines (no transposes).
+//   lambda (times s^2 / N) is computed once per build with the same kernels.
 // d > 1 (Kronecker of Toeplitz): T(c_d) applied along each axis by a dense per-axis
-//   product from shared memory (m_d <= 1024: m * m_d FMAs per axis, exact, no FFT round-off).
+//   product from shared memory (m_d <= 1024: m * m_d FMAs per axis, no FFT round-off).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -18,244 +22,328 @@ namespace love {
 
 namespace {
 
-template <typename R> struct Cx;
-template <> struct Cx<float> { using T = float2; };
-template <> struct Cx<double> { using T = double2; };
+using C = double2;
 
-template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
-    C r;
-    r.x = a.x * b.x - a.y * b.y;
-    r.y = a.x * b.y + a.y * b.x;
-    return r;
+__device__ __forceinline__ C cmul(C a, C b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ C cadd(C a, C b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ C csub(C a, C b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ C cconj(C a) { return make_double2(a.x, -a.y); }
+// multiply by -i (SIGN < 0) or +i (SIGN > 0)
+template <int SIGN> __device__ __forceinline__ C mul_i(C a) {
+    return SIGN < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
 }
 
-__device__ __forceinline__ void sincospi_t(float x, float* s, float* c) { sincospif(x, s, c); }
-__device__ __forceinline__ void sincospi_t(double x, double* s, double* c) { sincospi(x, s, c); }
-
-// exp(sign * 2 pi i * num / den) for integers 0 <= num < den (den a power of two), exact
-// argument reduction in integer arithmetic.
-template <typename R>
-__device__ __forceinline__ typename Cx<R>::T twiddle(int64_t num, int64_t den, int sign) {
-    typename Cx<R>::T w;
-    R s, c;
-    sincospi_t((R)(2.0 * (double)num / (double)den), &s, &c);
-    w.x = c;
-    w.y = sign < 0 ? -s : s;
-    return w;
+template <int SIGN> __device__ __forceinline__ void dft2(C* v) {
+    const C a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
 }
 
-// Radix-2 Stockham autosort FFT of G lines of length L (= 1 << logL) stored contiguously in
-// `a` (line g at a + g*L), `b` same-size scratch, tw[k] = exp(-2 pi i k / L), k < L/2.
-// sign = -1 forward, +1 inverse (unnormalised).  Returns the buffer holding the result.
-template <typename C>
-__device__ C* stockham(C* a, C* b, const C* tw, int G, int L, int logL, int sign) {
-    const int half = L >> 1;
-    for (int Ns = 1, s = 0; Ns < L; Ns <<= 1, ++s) {
-        const int tstep = L / (2 * Ns);   // twiddle table stride for this stage
-        for (int t = threadIdx.x; t < G * half; t += blockDim.x) {
-            const int line = t >> (logL - 1);
-            const int j = t & (half - 1);
-            const C* src = a + line * L;
-            C* dst = b + line * L;
-            const int k = j & (Ns - 1);
-            const C v0 = src[j];
-            C w = tw[k * tstep];
-            if (sign > 0) w.y = -w.y;
-            const C v1 = cmul(src[j + half], w);
-            const int idxD = ((j - k) << 1) + k;
-            C o0, o1;
-            o0.x = v0.x + v1.x; o0.y = v0.y + v1.y;
-            o1.x = v0.x - v1.x; o1.y = v0.y - v1.y;
-            dst[idxD] = o0;
-            dst[idxD + Ns] = o1;
+template <int SIGN> __device__ __forceinline__ void dft4(C& v0, C& v1, C& v2, C& v3) {
+    const C t0 = cadd(v0, v2), t1 = csub(v0, v2), t2 = cadd(v1, v3), t3 = mul_i<SIGN>(csub(v1, v3));
+    v0 = cadd(t0, t2);
+    v1 = cadd(t1, t3);
+    v2 = csub(t0, t2);
+    v3 = csub(t1, t3);
+}
+
+template <int SIGN> __device__ __forceinline__ void dft8(C* v) {
+    C e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+    C o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+    dft4<SIGN>(e0, e1, e2, e3);
+    dft4<SIGN>(o0, o1, o2, o3);
+    const double r = 0.70710678118654752440;
+    // w^k = exp(SIGN * 2 pi i k / 8)
+    const C w1 = make_double2(r, SIGN * r), w3 = make_double2(-r, SIGN * r);
+    o1 = cmul(o1, w1);
+    o2 = mul_i<SIGN>(o2);
+    o3 = cmul(o3, w3);
+    v[0] = cadd(e0, o0); v[4] = csub(e0, o0);
+    v[1] = cadd(e1, o1); v[5] = csub(e1, o1);
+    v[2] = cadd(e2, o2); v[6] = csub(e2, o2);
+    v[3] = cadd(e3, o3); v[7] = csub(e3, o3);
+}
+
+// Shared-memory index with one double2 of padding every 8: the radix-8 Stockham stores of the
+// first stage hit addresses 8 double2 (128 B) apart, which would all map to one bank group.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+inline size_t padded(size_t n) { return n + n / 8 + 1; }
+
+// One radix-R stage of an in-place Stockham FFT over G lines of length L in shared memory
+// (padded indices), run by a block of exactly G*L/8 threads (8/R butterflies per thread).
+// Every index into the register array is a compile-time constant (no local memory).
+template <int SIGN, int R>
+__device__ __forceinline__ void fft_stage(C* buf, int L, int Ns, const C* tw) {
+    constexpr int PER = 8 / R;
+    const int nb = L / R;                        // butterflies per line
+    const int step = L / (Ns * R);               // twiddle stride
+    C v[PER][R];
+    int dst[PER];
+#pragma unroll
+    for (int c = 0; c < PER; ++c) {
+        const int b = threadIdx.x + c * blockDim.x;
+        const int line = b / nb, j = b - line * nb;
+        const int k = j & (Ns - 1);
+        const int base = line * L;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            C x = buf[pad(base + j + r * nb)];
+            if (r > 0) {
+                C w = tw[r * k * step];
+                if (SIGN > 0) w = cconj(w);
+                x = cmul(x, w);
+            }
+            v[c][r] = x;
         }
-        __syncthreads();
-        C* tmp = a; a = b; b = tmp;
-    }
-    return a;
-}
-
-template <typename R>
-__device__ void fill_twiddles(typename Cx<R>::T* tw, int L) {
-    for (int k = threadIdx.x; k < L / 2; k += blockDim.x) tw[k] = twiddle<R>(k, L, -1);
-}
-
-// ---- single-CTA convolution / forward transform (N small)
-// mode 0: z[n] = Re IFFT(lam * FFT([u;0]))[n], n < m   (lam already holds s^2/N)
-// mode 1: outc[k] = FFT(u)[k] (u has N entries)                      (lambda setup)
-template <typename R>
-__global__ void fft_small_kernel(const R* __restrict__ u, int m, int N, int logN,
-                                 const R* __restrict__ lam, R* __restrict__ z,
-                                 typename Cx<R>::T* __restrict__ outc, int mode) {
-    using C = typename Cx<R>::T;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C* a = (C*)smraw;
-    C* b = a + N;
-    C* tw = b + N;
-    fill_twiddles<R>(tw, N);
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        C v;
-        v.x = i < m ? u[i] : R(0);
-        v.y = R(0);
-        a[i] = v;
+        dst[c] = base + (j - k) * R + k;
     }
     __syncthreads();
-    C* x = stockham<C>(a, b, tw, 1, N, logN, -1);
+#pragma unroll
+    for (int c = 0; c < PER; ++c) {
+        if (R == 8) dft8<SIGN>(v[c]);
+        else if (R == 4) dft4<SIGN>(v[c][0], v[c][1], v[c][2], v[c][3]);
+        else dft2<SIGN>(v[c]);
+#pragma unroll
+        for (int r = 0; r < R; ++r) buf[pad(dst[c] + r * Ns)] = v[c][r];
+    }
+    __syncthreads();
+}
+
+// In-place Stockham FFT of G lines of length L (contiguous in shared memory), run by a block
+// of exactly G*L/8 threads: radix-8 stages while 8 divides the remaining length, then one
+// radix-4 or radix-2 stage.  tw[k] = exp(-2 pi i k / L), k < L, in shared memory.
+// SIGN = -1 forward, +1 inverse (unnormalised).
+template <int SIGN>
+__device__ void line_fft(C* buf, int L, const C* tw) {
+    int Ns = 1;
+    for (; Ns * 8 <= L; Ns *= 8) fft_stage<SIGN, 8>(buf, L, Ns, tw);
+    if (Ns * 4 == L) fft_stage<SIGN, 4>(buf, L, Ns, tw);
+    else if (Ns * 2 == L) fft_stage<SIGN, 2>(buf, L, Ns, tw);
+}
+
+// copy a line-length twiddle table from global to shared memory
+__device__ __forceinline__ void load_tw(C* dst, const C* __restrict__ src, int L) {
+    #pragma unroll 8
+    for (int i = threadIdx.x; i < L; i += blockDim.x) dst[i] = src[i];
+}
+
+// exp(sign 2 pi i a / N) for 0 <= a < N = N1*N2 from two tables: twN2[i] = exp(-2 pi i i/N2)
+// = exp(-2 pi i (N1 i)/N) and twF[i] = exp(-2 pi i i / N), i < N1.
+template <int SIGN>
+__device__ __forceinline__ C twiddleN(int a, int N1, const C* __restrict__ twN2, const C* __restrict__ twF) {
+    C w = cmul(__ldg(&twN2[a / N1]), __ldg(&twF[a % N1]));
+    return SIGN > 0 ? cconj(w) : w;
+}
+
+// ---- single-CTA convolution (mode 0) / forward transform (mode 1), N <= 4096
+__global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, const C* __restrict__ tw,
+                                 const double* __restrict__ lam, double* __restrict__ z, C* __restrict__ outc,
+                                 int mode) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* tws = (C*)smraw;
+    C* buf = tws + N;
+    load_tw(tws, tw, N);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int i = threadIdx.x + e * blockDim.x;
+        buf[pad(i)] = make_double2(i < m ? u[i] : 0.0, 0.0);
+    }
+    __syncthreads();
+    line_fft<-1>(buf, N, tws);
     if (mode == 1) {
-        for (int i = threadIdx.x; i < N; i += blockDim.x) outc[i] = x[i];
+        #pragma unroll 8
+        for (int i = threadIdx.x; i < N; i += blockDim.x) outc[i] = buf[pad(i)];
         return;
     }
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-        const R l = lam[i];
-        x[i].x *= l;
-        x[i].y *= l;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int i = threadIdx.x + e * blockDim.x;
+        const double l = lam[i];
+        buf[pad(i)].x *= l;
+        buf[pad(i)].y *= l;
     }
     __syncthreads();
-    C* y = stockham<C>(x, x == a ? b : a, tw, 1, N, logN, +1);
-    for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] = y[i].x;
+    line_fft<+1>(buf, N, tws);
+    #pragma unroll 8
+    for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] = buf[pad(i)].x;
 }
 
 // ---- four-step pass A: for each n1, FFT over n2 of x[n1 + N1 n2], times w_N^{n1 k2}
-template <typename R, int G>
-__global__ void fft_passA_kernel(const R* __restrict__ u, int m, int N1, int N2, int logN2,
-                                 typename Cx<R>::T* __restrict__ Y) {
-    using C = typename Cx<R>::T;
+template <int G>
+__global__ void fft_passA_kernel(const double* __restrict__ u, int m, int N1, int N2, const C* __restrict__ tw2,
+                                 const C* __restrict__ twF, C* __restrict__ Y) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    C* a = (C*)smraw;
-    C* b = a + G * N2;
-    C* tw = b + G * N2;
-    fill_twiddles<R>(tw, N2);
+    C* tws = (C*)smraw;
+    C* buf = tws + N2;
+    load_tw(tws, tw2, N2);
     const int n1_0 = blockIdx.x * G;
-    const int64_t N = (int64_t)N1 * N2;
-    for (int t = threadIdx.x; t < G * N2; t += blockDim.x) {
+    const int N = N1 * N2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n2 = t / G;
-        const int64_t idx = n1_0 + g + (int64_t)N1 * n2;
-        C v;
-        v.x = idx < m ? u[idx] : R(0);
-        v.y = R(0);
-        a[g * N2 + n2] = v;
+        const int idx = n1_0 + g + N1 * n2;
+        buf[pad(g * N2 + n2)] = make_double2(idx < m ? u[idx] : 0.0, 0.0);
     }
     __syncthreads();
-    C* x = stockham<C>(a, b, tw, G, N2, logN2, -1);
-    for (int t = threadIdx.x; t < G * N2; t += blockDim.x) {
+    line_fft<-1>(buf, N2, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N2, k2 = t % N2;
         const int n1 = n1_0 + g;
-        const C w = twiddle<R>(((int64_t)n1 * k2) % N, N, -1);
-        Y[(int64_t)n1 * N2 + k2] = cmul(x[g * N2 + k2], w);
+        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(t)], twiddleN<-1>((n1 * k2) & (N - 1), N1, tw2, twF));
     }
 }
 
 // ---- four-step pass B: for each k2, FFT over n1 -> X[N2 k1 + k2];
-// mode 0: multiply by lamB[k2*N1 + k1], inverse FFT over k1, times w_N^{-n1 k2}, store back
+// mode 0: times lamB[k2*N1 + k1], inverse FFT over k1, times w_N^{-n1 k2}, store back
 // mode 1: store X in natural order into outc
-template <typename R, int G>
-__global__ void fft_passB_kernel(typename Cx<R>::T* __restrict__ Y, int N1, int N2, int logN1,
-                                 const R* __restrict__ lamB, typename Cx<R>::T* __restrict__ outc,
-                                 int mode) {
-    using C = typename Cx<R>::T;
+template <int G>
+__global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
+                                 const C* __restrict__ tw2, const C* __restrict__ twF,
+                                 const double* __restrict__ lamB, C* __restrict__ outc, int mode) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    C* a = (C*)smraw;
-    C* b = a + G * N1;
-    C* tw = b + G * N1;
-    fill_twiddles<R>(tw, N1);
+    C* tws = (C*)smraw;
+    C* buf = tws + N1;
+    load_tw(tws, tw1, N1);
     const int k2_0 = blockIdx.x * G;
-    const int64_t N = (int64_t)N1 * N2;
-    for (int t = threadIdx.x; t < G * N1; t += blockDim.x) {
+    const int N = N1 * N2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n1 = t / G;
-        a[g * N1 + n1] = Y[(int64_t)n1 * N2 + k2_0 + g];
+        buf[pad(g * N1 + n1)] = Y[(int64_t)n1 * N2 + k2_0 + g];
     }
     __syncthreads();
-    C* x = stockham<C>(a, b, tw, G, N1, logN1, -1);
+    line_fft<-1>(buf, N1, tws);
     if (mode == 1) {
-        for (int t = threadIdx.x; t < G * N1; t += blockDim.x) {
+    #pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
             const int g = t % G, k1 = t / G;
-            outc[(int64_t)N2 * k1 + k2_0 + g] = x[g * N1 + k1];
+            outc[(int64_t)N2 * k1 + k2_0 + g] = buf[pad(g * N1 + k1)];
         }
         return;
     }
-    for (int t = threadIdx.x; t < G * N1; t += blockDim.x) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N1, k1 = t % N1;
-        const R l = lamB[(int64_t)(k2_0 + g) * N1 + k1];
-        x[t].x *= l;
-        x[t].y *= l;
+        const double l = lamB[(int64_t)(k2_0 + g) * N1 + k1];
+        buf[pad(t)].x *= l;
+        buf[pad(t)].y *= l;
     }
     __syncthreads();
-    C* y = stockham<C>(x, x == a ? b : a, tw, G, N1, logN1, +1);
-    for (int t = threadIdx.x; t < G * N1; t += blockDim.x) {
+    line_fft<+1>(buf, N1, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n1 = t / G;
         const int k2 = k2_0 + g;
-        const C w = twiddle<R>(((int64_t)n1 * k2) % N, N, +1);
-        Y[(int64_t)n1 * N2 + k2] = cmul(y[g * N1 + n1], w);
+        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(g * N1 + n1)], twiddleN<+1>((n1 * k2) & (N - 1), N1, tw2, twF));
     }
 }
 
-// ---- four-step pass A': for each n1, inverse FFT over k2; z[n1 + N1 n2] = Re(.)
-template <typename R, int G>
-__global__ void fft_passC_kernel(const typename Cx<R>::T* __restrict__ Y, int m, int N1, int N2,
-                                 int logN2, R* __restrict__ z) {
-    using C = typename Cx<R>::T;
+// ---- four-step pass C: for each n1, inverse FFT over k2; z[n1 + N1 n2] = Re(.)
+template <int G>
+__global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
+                                 double* __restrict__ z) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    C* a = (C*)smraw;
-    C* b = a + G * N2;
-    C* tw = b + G * N2;
-    fill_twiddles<R>(tw, N2);
+    C* tws = (C*)smraw;
+    C* buf = tws + N2;
+    load_tw(tws, tw2, N2);
     const int n1_0 = blockIdx.x * G;
-    for (int t = threadIdx.x; t < G * N2; t += blockDim.x) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N2, k2 = t % N2;
-        a[t] = Y[(int64_t)(n1_0 + g) * N2 + k2];
+        buf[pad(t)] = Y[(int64_t)(n1_0 + g) * N2 + k2];
     }
     __syncthreads();
-    C* x = stockham<C>(a, b, tw, G, N2, logN2, +1);
-    for (int t = threadIdx.x; t < G * N2; t += blockDim.x) {
+    line_fft<+1>(buf, N2, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+        const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n2 = t / G;
-        const int64_t idx = n1_0 + g + (int64_t)N1 * n2;
-        if (idx < m) z[idx] = x[g * N2 + n2].x;
+        const int idx = n1_0 + g + N1 * n2;
+        if (idx < m) z[idx] = buf[pad(g * N2 + n2)].x;
     }
 }
 
-// ---- dense per-axis Toeplitz products (d > 1)
-// layout (outer O, length L, inner I): out(o,l,i) = scale * sum_l' c[|l-l'|] in(o,l',i)
-template <typename V>
-__global__ void axis_inner_kernel(const V* __restrict__ in, V* __restrict__ out,
-                                  const V* __restrict__ c, int L, int I, int RL, V scale) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V* cs = (V*)smraw;           // [L]
-    V* tile = cs + L;            // [L][32]
-    const int i0 = blockIdx.x * 32;
-    const int r0 = blockIdx.y * RL;
+// ---- dense per-axis Toeplitz products (d > 1), fp64
+// layout (outer O, length L, inner I): out(o,l,i) = scale * sum_l' c[|l-l'|] in(o,l',i).
+// Strided axes (I > 1): a CTA computes a 16 (rows) x 32 (inner) output tile, looping over
+// 32-row chunks of the input staged in shared memory; 4 independent accumulators/thread.
+constexpr int kAxRows = 16, kAxInner = 32, kAxK = 32;
+__global__ void __launch_bounds__(128) axis_inner_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                         const double* __restrict__ c, int L, int I, double scale) {
+    __shared__ double cs[1024];
+    __shared__ double tile[kAxK][kAxInner + 1];
+    const int i0 = blockIdx.x * kAxInner;
+    const int r0 = blockIdx.y * kAxRows;
     const int64_t ob = (int64_t)blockIdx.z * L * I;
+    #pragma unroll 8
     for (int t = threadIdx.x; t < L; t += blockDim.x) cs[t] = c[t];
-    for (int t = threadIdx.x; t < L * 32; t += blockDim.x) {
-        const int l = t >> 5, ii = t & 31;
-        tile[t] = (i0 + ii < I) ? in[ob + (int64_t)l * I + i0 + ii] : V(0);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 4 row groups of 4 rows
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l0 = 0; l0 < L; l0 += kAxK) {
+        __syncthreads();
+        #pragma unroll 8
+        for (int t = threadIdx.x; t < kAxK * kAxInner; t += blockDim.x) {
+            const int l = t >> 5, ii = t & 31;
+            tile[l][ii] = (l0 + l < L && i0 + ii < I) ? in[ob + (int64_t)(l0 + l) * I + i0 + ii] : 0.0;
+        }
+        __syncthreads();
+        const int lmax = min(kAxK, L - l0);
+        for (int l = 0; l < lmax; ++l) {
+            const double v = tile[l][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = r0 + ty * 4 + q;
+                acc[q] += cs[abs(r - (l0 + l)) & 1023] * v;
+            }
+        }
     }
-    __syncthreads();
-    const int ii = threadIdx.x & 31;
-    for (int r = r0 + (threadIdx.x >> 5); r < min(L, r0 + RL); r += blockDim.x >> 5) {
-        V acc = V(0);
-        for (int l = 0; l < L; ++l) acc += cs[abs(r - l)] * tile[l * 32 + ii];
-        if (i0 + ii < I) out[ob + (int64_t)r * I + i0 + ii] = acc * scale;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int r = r0 + ty * 4 + q;
+        if (r < L && i0 + tx < I) out[ob + (int64_t)r * I + i0 + tx] = acc[q] * scale;
     }
 }
 
-template <typename V>
-__global__ void axis_line_kernel(const V* __restrict__ in, V* __restrict__ out,
-                                 const V* __restrict__ c, int O, int L, int LPB, V scale) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V* cs = (V*)smraw;           // [L]
-    V* lines = cs + L;           // [LPB][L]
-    const int64_t o0 = (int64_t)blockIdx.x * LPB;
-    const int nl = (int)(((int64_t)LPB < (int64_t)O - o0) ? (int64_t)LPB : (int64_t)O - o0);
+// Contiguous axis (I = 1): one output per thread, 256 outputs per CTA (256/L lines, or a
+// 256-row slice of one line), 4 partial sums per output.
+__global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                        const double* __restrict__ c, int64_t O, int L,
+                                                        double scale) {
+    __shared__ double cs[1024];
+    __shared__ double lines[2 * 1024 + 256];
+    const int64_t first = (int64_t)blockIdx.x * 256;           // first output of this CTA
+    const int64_t o0 = first / L;
+    const int span = 2 * L + 256;                               // covers every line the CTA touches
+    #pragma unroll 8
     for (int t = threadIdx.x; t < L; t += blockDim.x) cs[t] = c[t];
-    for (int t = threadIdx.x; t < nl * L; t += blockDim.x) lines[t] = in[o0 * L + t];
-    __syncthreads();
-    for (int t = threadIdx.x; t < nl * L; t += blockDim.x) {
-        const int ln = t / L, r = t % L;
-        const V* x = lines + ln * L;
-        V acc = V(0);
-        for (int l = 0; l < L; ++l) acc += cs[abs(r - l)] * x[l];
-        out[o0 * L + t] = acc * scale;
+    #pragma unroll 8
+    for (int t = threadIdx.x; t < span; t += blockDim.x) {
+        const int64_t e = o0 * L + t;
+        lines[t] = e < O * L ? in[e] : 0.0;
     }
+    __syncthreads();
+    const int64_t o = first + threadIdx.x;
+    if (o >= O * L) return;
+    const int ln = (int)(o / L - o0), r = (int)(o % L);
+    const double* x = lines + ln * L;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int l = 0;
+    for (; l + 4 <= L; l += 4) {
+        a0 += cs[abs(r - l)] * x[l];
+        a1 += cs[abs(r - l - 1)] * x[l + 1];
+        a2 += cs[abs(r - l - 2)] * x[l + 2];
+        a3 += cs[abs(r - l - 3)] * x[l + 3];
+    }
+    for (; l < L; ++l) a0 += cs[abs(r - l)] * x[l];
+    out[o] = ((a0 + a1) + (a2 + a3)) * scale;
 }
 
 __global__ void rbf_columns_kernel(GridDev g, double l0, double l1, double l2, double* __restrict__ cols) {
@@ -270,6 +358,15 @@ __global__ void rbf_columns_kernel(GridDev g, double l0, double l1, double l2, d
     }
 }
 
+__global__ void twiddle_table_kernel(C* __restrict__ tw, int L, int den) {
+    // tw[k] = exp(-2 pi i k / den), k < L
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi(2.0 * (double)k / (double)den, &s, &c);
+        tw[k] = make_double2(c, -s);
+    }
+}
+
 __global__ void embed_kernel(const double* __restrict__ c, int m, int N, double* __restrict__ col) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
         double v = 0.0;
@@ -279,23 +376,17 @@ __global__ void embed_kernel(const double* __restrict__ c, int m, int N, double*
     }
 }
 
-template <typename V>
-__global__ void lambda_store_kernel(const double2* __restrict__ X, int N, int N1, int N2, int four_step,
-                                    double scale, V* __restrict__ lam) {
+__global__ void lambda_store_kernel(const C* __restrict__ X, int N, int N1, int N2, int four_step,
+                                    double scale, double* __restrict__ lam) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         const double v = X[k].x * scale;
         if (four_step) {
             const int k1 = k / N2, k2 = k % N2;   // k = N2 k1 + k2
-            lam[(int64_t)k2 * N1 + k1] = (V)v;
+            lam[(int64_t)k2 * N1 + k1] = v;
         } else {
-            lam[k] = (V)v;
+            lam[k] = v;
         }
     }
-}
-
-template <typename V>
-__global__ void cast_kernel(const double* __restrict__ a, V* __restrict__ b, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = (V)a[i];
 }
 
 inline int ilog2(int64_t x) {
@@ -304,68 +395,50 @@ inline int ilog2(int64_t x) {
     return l;
 }
 
-template <typename R> constexpr int lines_per_cta() { return sizeof(R) == 4 ? 4 : 2; }
-template <typename R> int small_fft_max() { return sizeof(R) == 4 ? 4096 : 2048; }
-
-template <typename R>
-size_t fft_line_smem(int G, int L) {
-    return sizeof(typename Cx<R>::T) * (size_t)(2 * G * L + L / 2);
-}
-
-template <typename R>
-void set_smem_attr(const void* fn, size_t bytes) {
-    if (bytes > 48 * 1024) cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                           (int)bytes), "smem attr");
-}
+constexpr int kSmallFFT = 4096;
+constexpr int kLinesPerCta = 2;
 
 // convolution (mode 0) of u (m entries) or forward FFT (mode 1) of u (N entries)
-template <typename R>
-void fft_run(int N, int N1, int N2, const R* u, int m, const R* lam, R* z,
-             typename Cx<R>::T* work, typename Cx<R>::T* outc, int mode, cudaStream_t s) {
-    using C = typename Cx<R>::T;
+void fft_run(const Cache& c, const double* u, int m, double* z, C* work, C* outc, int mode, cudaStream_t s) {
+    const int N = c.fft_N, N1 = c.fft_N1, N2 = c.fft_N2;
+    const C* tw1 = (const C*)c.tw1;
+    const C* tw2 = (const C*)c.tw2;
+    const C* twF = (const C*)c.twF;
+    const double* lam = (const double*)c.lam;
     if (N1 == 0) {
-        const size_t sm = fft_line_smem<R>(1, N);
-        set_smem_attr<R>((const void*)fft_small_kernel<R>, sm);
-        LOVE_LAUNCH(fft_small_kernel<R>, 1, 1024, sm, s, u, m, N, ilog2(N), lam, z, outc, mode);
+        const size_t sm = sizeof(C) * (padded(N) + N);
+        ensure_smem((const void*)fft_small_kernel, sm);
+        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, m, N, tw1, lam, z, outc, mode);
         return;
     }
-    constexpr int G = lines_per_cta<R>();
-    const size_t smA = fft_line_smem<R>(G, N2), smB = fft_line_smem<R>(G, N1);
-    set_smem_attr<R>((const void*)fft_passA_kernel<R, G>, smA);
-    set_smem_attr<R>((const void*)fft_passB_kernel<R, G>, smB);
-    set_smem_attr<R>((const void*)fft_passC_kernel<R, G>, smA);
-    LOVE_LAUNCH((fft_passA_kernel<R, G>), N1 / G, 256, smA, s, u, m, N1, N2, ilog2(N2), work);
-    LOVE_LAUNCH((fft_passB_kernel<R, G>), N2 / G, 256, smB, s, work, N1, N2, ilog2(N1), lam, outc, mode);
-    if (mode == 0)
-        LOVE_LAUNCH((fft_passC_kernel<R, G>), N1 / G, 256, smA, s, (const C*)work, m, N1, N2, ilog2(N2), z);
+    constexpr int G = kLinesPerCta;
+    const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
+    ensure_smem((const void*)fft_passA_kernel<G>, smA);
+    ensure_smem((const void*)fft_passB_kernel<G>, smB);
+    ensure_smem((const void*)fft_passC_kernel<G>, smA);
+    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, m, N1, N2, tw2, twF, work);
+    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode);
+    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z);
 }
 
-template <typename V>
-void kuu_axes(const Cache& c, const V* u, V* z, cudaStream_t s) {
+void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
     const GridDev& g = c.g;
-    const V* in = u;
+    const double* in = u;
     int off = 0;
     for (int d = 0; d < g.d; ++d) {
         const int L = g.m[d];
         int O = 1, I = 1;
         for (int e = 0; e < d; ++e) O *= g.m[e];
         for (int e = d + 1; e < g.d; ++e) I *= g.m[e];
-        V* out = (d == g.d - 1) ? z : (V*)c.ktmp[d & 1];
-        const V scale = (d == g.d - 1) ? (V)c.rbf.outputscale : V(1);
-        const V* col = (const V*)c.cols + off;
+        double* out = (d == g.d - 1) ? z : (double*)c.ktmp[d & 1];
+        const double scale = (d == g.d - 1) ? c.rbf.outputscale : 1.0;
+        const double* col = c.cols64 + off;
         if (I == 1) {
-            const int LPB = std::max(1, 2048 / L);
-            const size_t sm = sizeof(V) * (size_t)(L + LPB * L);
-            set_smem_attr<V>((const void*)axis_line_kernel<V>, sm);
-            LOVE_LAUNCH(axis_line_kernel<V>, (int)ceil_div(O, LPB), 256, sm, s, in, out, col, O, L, LPB, scale);
+            const int64_t total = (int64_t)O * L;
+            LOVE_LAUNCH(axis_line_kernel, (int)ceil_div(total, 256), 256, 0, s, in, out, col, (int64_t)O, L, scale);
         } else {
-            const int tiles = (int)ceil_div(I, 32);
-            int RL = L;
-            while (RL > 8 && (int64_t)tiles * O * ceil_div(L, RL) < 2 * 148) RL /= 2;
-            const size_t sm = sizeof(V) * (size_t)(L + L * 32);
-            set_smem_attr<V>((const void*)axis_inner_kernel<V>, sm);
-            dim3 grid(tiles, (unsigned)ceil_div(L, RL), O);
-            LOVE_LAUNCH(axis_inner_kernel<V>, grid, 256, sm, s, in, out, col, L, I, RL, scale);
+            dim3 grid((unsigned)ceil_div(I, kAxInner), (unsigned)ceil_div(L, kAxRows), (unsigned)O);
+            LOVE_LAUNCH(axis_inner_kernel, grid, 128, 0, s, in, out, col, L, I, scale);
         }
         in = out;
         off += L;
@@ -379,75 +452,58 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     int msum = 0;
     for (int d = 0; d < g.d; ++d) msum += g.m[d];
     c.cols64 = (double*)dalloc(c, sizeof(double) * msum, s);
-    c.cols = dalloc(c, c.vsize * msum, s);
     LOVE_LAUNCH(rbf_columns_kernel, 64, 256, 0, s, g, c.rbf.lengthscale[0], c.rbf.lengthscale[1],
                 c.rbf.lengthscale[2], c.cols64);
-    if (c.precision == LOVE_FP64) LOVE_LAUNCH(cast_kernel<double>, 64, 256, 0, s, c.cols64, (double*)c.cols, msum);
-    else LOVE_LAUNCH(cast_kernel<float>, 64, 256, 0, s, c.cols64, (float*)c.cols, msum);
-
+    for (int d = 0; d < g.d; ++d)     // c_d[0..3] on the host for the variance-query prior
+        for (int i = 0; i < 4; ++i) {
+            const double r = (double)i * g.h[d];
+            c.h_cols64[d][i] = std::exp(-(r * r) / (2.0 * c.rbf.lengthscale[d] * c.rbf.lengthscale[d]));
+        }
     if (g.d > 1) {
         for (int d = 0; d < g.d; ++d)
             if (g.m[d] > 1024) throw LoveError{LOVE_ERR_ARG, "Kronecker grids need m_d <= 1024 per axis"};
-        c.ktmp[0] = dalloc(c, c.vsize * g.m_total, s);
-        c.ktmp[1] = dalloc(c, c.vsize * g.m_total, s);
+        c.ktmp[0] = dalloc(c, sizeof(double) * g.m_total, s);
+        c.ktmp[1] = dalloc(c, sizeof(double) * g.m_total, s);
         return;
     }
-    // d = 1: circulant embedding and its eigenvalues (fp64), stored * s^2 / N
+    // d = 1: circulant embedding and its eigenvalues, stored * s^2 / N
     const int m = g.m[0];
-    int N = 1;
+    int N = 8;
     while (N < 2 * m - 1) N *= 2;
     if (N > (1 << 22)) throw LoveError{LOVE_ERR_ARG, "1-D grid too long (m <= 2^21)"};
     c.fft_N = N;
-    const int small = (c.precision == LOVE_FP64) ? small_fft_max<double>() : small_fft_max<float>();
-    if (N <= small) {
+    if (N <= kSmallFFT) {
         c.fft_N1 = c.fft_N2 = 0;
+        c.tw1 = dalloc(c, sizeof(C) * N, s);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(N, 256), 256, 0, s, (C*)c.tw1, N, N);
     } else {
         const int lg = ilog2(N);
         c.fft_N1 = 1 << (lg / 2);
         c.fft_N2 = N / c.fft_N1;
+        c.tw1 = dalloc(c, sizeof(C) * c.fft_N1, s);
+        c.tw2 = dalloc(c, sizeof(C) * c.fft_N2, s);
+        c.twF = dalloc(c, sizeof(C) * c.fft_N1, s);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(c.fft_N1, 256), 256, 0, s, (C*)c.tw1, c.fft_N1, c.fft_N1);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(c.fft_N2, 256), 256, 0, s, (C*)c.tw2, c.fft_N2, c.fft_N2);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(c.fft_N1, 256), 256, 0, s, (C*)c.twF, c.fft_N1, N);
     }
-    c.lam = dalloc(c, c.vsize * N, s);
-    c.fft_buf = dalloc(c, 2 * c.vsize * N, s);
+    c.lam = dalloc(c, sizeof(double) * N, s);
+    c.fft_buf = dalloc(c, sizeof(C) * N, s);
     double* col = nullptr;
-    double2* X = nullptr;
-    double2* work = nullptr;
+    C* X = nullptr;
     cuda_check(cudaMallocAsync((void**)&col, sizeof(double) * N, s), "lam alloc");
-    cuda_check(cudaMallocAsync((void**)&X, sizeof(double2) * N, s), "lam alloc");
-    cuda_check(cudaMallocAsync((void**)&work, sizeof(double2) * N, s), "lam alloc");
+    cuda_check(cudaMallocAsync((void**)&X, sizeof(C) * N, s), "lam alloc");
     LOVE_LAUNCH(embed_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, c.cols64, m, N, col);
-    // fp64 N1 may differ from the fp32 split only through the small-FFT threshold
-    int N1 = c.fft_N1, N2 = c.fft_N2;
-    if (N1 == 0 && N > small_fft_max<double>()) {
-        const int lg = ilog2(N);
-        N1 = 1 << (lg / 2);
-        N2 = N / N1;
-    }
-    fft_run<double>(N, N1, N2, col, N, nullptr, nullptr, work, X, 1, s);
-    const double scale = c.rbf.outputscale / (double)N;
-    // the stored layout follows the split used by the vector-precision kernels
-    const int four = c.fft_N1 != 0;
-    if (c.precision == LOVE_FP64)
-        LOVE_LAUNCH(lambda_store_kernel<double>, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N,
-                    c.fft_N1, c.fft_N2, four, scale, (double*)c.lam);
-    else
-        LOVE_LAUNCH(lambda_store_kernel<float>, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N,
-                    c.fft_N1, c.fft_N2, four, scale, (float*)c.lam);
+    fft_run(c, col, N, nullptr, (C*)c.fft_buf, X, 1, s);
+    LOVE_LAUNCH(lambda_store_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N, c.fft_N1,
+                c.fft_N2, c.fft_N1 != 0, c.rbf.outputscale / (double)N, (double*)c.lam);
     cuda_check(cudaFreeAsync(col, s), "lam free");
     cuda_check(cudaFreeAsync(X, s), "lam free");
-    cuda_check(cudaFreeAsync(work, s), "lam free");
 }
 
-template <typename V>
-void launch_kuu(const Cache& c, const V* u, V* z, cudaStream_t s) {
-    if (c.g.d > 1) {
-        kuu_axes<V>(c, u, z, s);
-        return;
-    }
-    using C = typename Cx<V>::T;
-    fft_run<V>(c.fft_N, c.fft_N1, c.fft_N2, u, c.g.m[0], (const V*)c.lam, z, (C*)c.fft_buf, nullptr, 0, s);
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s) {
+    if (c.g.d > 1) kuu_axes(c, u, z, s);
+    else fft_run(c, u, c.g.m[0], z, (C*)c.fft_buf, nullptr, 0, s);
 }
-
-template void launch_kuu<float>(const Cache&, const float*, float*, cudaStream_t);
-template void launch_kuu<double>(const Cache&, const double*, double*, cudaStream_t);
 
 }  // namespace love

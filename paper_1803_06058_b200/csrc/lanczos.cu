@@ -13,6 +13,8 @@
 // probe y): a = ||y|| Rc L^{-1} e_1, also streamed.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "love_internal.h"
 
 namespace love {
@@ -40,48 +42,66 @@ __device__ __forceinline__ void vstore(V* p, const V in[VecT<V>::W]) {
     *reinterpret_cast<T*>(p) = v;
 }
 
-// ---- per-step scalar bookkeeping (one thread).  Finalises index i = j-1: alpha_i, the
-// Cholesky row i of T, g_i, then beta_i, the breakdown test and the scale of q_j.
-__global__ void lanczos_scalars_kernel(LanczosState st, int j, int k, double tol) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// ---- step prologue (launched at the start of step j, and once with j = k after the loop).
+// Finalises index i = j-1 from the reduced accumulators: alpha_i, row i of the Cholesky of
+// T (L_ii), g_i = (L^{-1} e_1)_i, then beta_i, the breakdown test (reading A12)
+// and the scale 1/beta_i of q_j.  Every thread recomputes the scalars it needs (they only
+// depend on state written by earlier launches); block 0 / thread 0 persists them.  The
+// same launch streams column i of the cache:
+//   Rc[:, i] = (z_i - L_{i,i-1} Rc[:, i-1]) / L_ii ;  a += ||b|| g_i Rc[:, i]      (fp64)
+__global__ void step_prologue_kernel(LanczosState st, int k, double tol, int m,
+                                     const double* __restrict__ z0, const double* __restrict__ z1,
+                                     double* __restrict__ Rc, double* __restrict__ a, int mean_y) {
     int* fl = st.flags;
+    const int j = *st.jdev;
+    const double* __restrict__ z = ((j - 1) & 1) ? z1 : z0;     // z_{j-1}
+    const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
     if (j == 0) {
-        const double b2 = st.bnorm2[0];
-        if (!(b2 > 0.0)) { fl[3] = 1; fl[0] = 1; fl[1] = 0; return; }
-        st.qscale[0] = 1.0 / sqrt(b2);
+        if (writer) {
+            const double b2 = st.bnorm2[0];
+            if (!(b2 > 0.0)) { fl[3] = 1; fl[0] = 1; fl[1] = 0; }
+            else st.qscale[0] = 1.0 / sqrt(b2);
+        }
         return;
     }
-    if (fl[0]) return;
     const int i = j - 1;
-    const double a = st.alpha_acc[i];
-    st.alpha[i] = a;
-    st.amax_bmax[0] = fmax(st.amax_bmax[0], fabs(a));
+    if (fl[1] <= i || fl[2] || fl[3]) return;           // stopped at an earlier step
+    const double al = st.alpha_acc[i];
+    const double amax = fmax(st.amax_bmax[0], fabs(al));
     const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
-    const double piv = a - lsub * lsub;
-    if (!(piv > 0.0)) { fl[2] = 1; fl[0] = 1; fl[1] = i; return; }
+    const double piv = al - lsub * lsub;
+    if (!(piv > 0.0)) {
+        if (writer) { fl[2] = 1; fl[0] = 1; fl[1] = i; }
+        return;
+    }
     const double ld = sqrt(piv);
-    st.Ld[i] = ld;
-    st.g[i] = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
-    if (j == k) { fl[0] = 1; fl[1] = k; return; }
-    const double b = sqrt(st.beta2_acc[i]);
-    st.amax_bmax[1] = fmax(st.amax_bmax[1], b);
-    if (!(b >= tol * (st.amax_bmax[0] + 2.0 * st.amax_bmax[1]))) { fl[0] = 1; fl[1] = j; return; }
-    st.beta[i] = b;
-    st.Ls[i] = b / ld;
-    st.qscale[j] = 1.0 / b;
-}
-
-// Rc[:, i] = (z_i - L_{i,i-1} Rc[:, i-1]) / L_ii ;  a += ||b|| g_i Rc[:, i]    (fp64)
-template <typename V>
-__global__ void rc_update_kernel(LanczosState st, int i, int m, const V* __restrict__ z,
-                                 double* __restrict__ Rc, double* __restrict__ a, int mean_y) {
-    if (i >= st.flags[1] || st.flags[2] || st.flags[3]) return;
-    const double ld = st.Ld[i];
-    const double ls = i > 0 ? st.Ls[i - 1] : 0.0;
-    const double ag = sqrt(st.bnorm2[0]) * st.g[i];
+    const double gi = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
+    if (writer) {
+        st.alpha[i] = al;
+        st.Ld[i] = ld;
+        st.g[i] = gi;
+        st.amax_bmax[0] = amax;
+        if (j == k) {
+            fl[0] = 1;
+            fl[1] = k;
+        } else {
+            const double b = sqrt(st.beta2_acc[i]);
+            const double bmax = fmax(st.amax_bmax[1], b);
+            st.amax_bmax[1] = bmax;
+            if (!(b >= tol * (amax + 2.0 * bmax))) {
+                fl[0] = 1;
+                fl[1] = j;
+            } else {
+                st.beta[i] = b;
+                st.Ls[i] = b / ld;
+                st.qscale[j] = 1.0 / b;
+            }
+        }
+    }
+    const double ag = sqrt(st.bnorm2[0]) * gi;
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x) {
         const double prev = i > 0 ? Rc[(int64_t)(i - 1) * m + p] : 0.0;
-        const double v = ((double)z[p] - ls * prev) / ld;
+        const double v = (z[p] - lsub * prev) / ld;
         Rc[(int64_t)i * m + p] = v;
         if (mean_y) a[p] += ag * v;
     }
@@ -124,24 +144,28 @@ __device__ __forceinline__ void load_src(const V* __restrict__ Q, int64_t ldq, c
 }
 
 // ---- reorthogonalisation dots: c[i] += q_i^T src over this CTA's rows, i = 0..j.
-// One row tile per CTA (tiles sized so the grid is ~2 CTAs per SM); warps own columns and
-// stream Q~[tile, col] with 16-byte loads against the tile of src staged in shared memory.
+// One row tile per CTA (~4 CTAs per SM).  Work units (column, row split) are spread over the
+// warps -- a column gets several warps while j is small -- and each lane keeps U 16-byte
+// loads of Q~ in flight against the tile of src staged in shared memory.
 template <typename V>
 __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ Q, int64_t ldq,
-                                                          int64_t tile_rows, int j,
-                                                          const V* __restrict__ r, int from_r,
-                                                          LanczosState st, double* __restrict__ c_out) {
+                                                          int64_t tile_rows, int k, int pass,
+                                                          const V* __restrict__ r, LanczosState st) {
     constexpr int W = VecT<V>::W;
-    constexpr int U = 4;
+    constexpr int U = 8;
     extern __shared__ __align__(16) double smd[];
-    if (st.flags[0]) return;
+    const int j = *st.jdev;
+    if (st.flags[0] || j >= k - 1) return;
+    const int from_r = pass == 0;
+    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
     const int ncols = j + 1;
-    double* csum = smd;                                   // [ncols]
-    V* src = reinterpret_cast<V*>(smd + round_up(ncols, 2));   // [tile_rows]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int S = ncols < nw ? nw / ncols : 1;            // row splits per column
+    double* csum = smd;                                   // [S][ncols]
+    V* src = reinterpret_cast<V*>(smd + round_up(max(k + 1, nw), 2));   // [tile_rows]
     const int64_t row0 = (int64_t)blockIdx.x * tile_rows;
     const int64_t rows = min(tile_rows, ldq - row0);
     if (rows <= 0) return;
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) csum[i] = 0.0;
     const double sj = st.qscale[j];
     const double aj = st.alpha_acc[j] * sj;
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
@@ -153,45 +177,54 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
         for (int e = 0; e < W; ++e) src[q * W + e] = (V)v[e];
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int col = wid; col < ncols; col += nw) {
+    for (int unit = wid; unit < ncols * S; unit += nw) {
+        const int col = unit % ncols, sp = unit / ncols;
+        const int lo = (int)((int64_t)nchunk * sp / S), hi = (int)((int64_t)nchunk * (sp + 1) / S);
         const V* qc = Q + (int64_t)col * ldq + row0;
         V part = V(0);
-        for (int q0 = lane; q0 < nchunk; q0 += 32 * U) {
-            V a[U][W], b[U][W];
+        for (int q0 = lo + lane; q0 < hi; q0 += 32 * U) {
+            V a[U][W];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int q = q0 + 32 * u;
-                if (q < nchunk) {
-                    vload<V>(qc + q * W, a[u]);
-                    vload<V>(src + q * W, b[u]);
-                } else {
+                if (q < hi) vload<V>(qc + q * W, a[u]);
+                else
 #pragma unroll
-                    for (int e = 0; e < W; ++e) a[u][e] = b[u][e] = V(0);
-                }
+                    for (int e = 0; e < W; ++e) a[u][e] = V(0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int u = 0; u < U; ++u) {
+                const int q = min(q0 + 32 * u, hi - 1);
+                V b[W];
+                vload<V>(src + q * W, b);
 #pragma unroll
-                for (int e = 0; e < W; ++e) part += a[u][e] * b[u][e];
+                for (int e = 0; e < W; ++e) part += a[u][e] * b[e];
+            }
         }
         const double dp = warp_sum((double)part);
-        if (lane == 0) csum[col] = dp;
+        if (lane == 0) csum[sp * ncols + col] = dp;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) atomicAdd(&c_out[i], csum[i] * st.qscale[i]);
+    for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+        double tot = 0.0;
+        for (int sp = 0; sp < S; ++sp) tot += csum[sp * ncols + i];
+        atomicAdd(&c_out[i], tot * st.qscale[i]);
+    }
 }
 
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
 template <typename V>
-__global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int j,
-                                                            const V* __restrict__ r, int from_r,
-                                                            LanczosState st, const double* __restrict__ c_in,
-                                                            double* __restrict__ beta2_out) {
+__global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
+                                                            int pass, int last_pass, const V* __restrict__ r,
+                                                            LanczosState st) {
     constexpr int W = VecT<V>::W;
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
     __shared__ double red[32];
-    if (st.flags[0]) return;
+    const int j = *st.jdev;
+    if (st.flags[0] || j >= k - 1) return;
+    const int from_r = pass == 0;
+    const double* __restrict__ c_in = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
+    double* __restrict__ beta2_out = last_pass ? st.beta2_acc + j : nullptr;
     const int ncols = j + 1;
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) cf[i] = c_in[i] * st.qscale[i];
     __syncthreads();
@@ -247,61 +280,133 @@ __global__ void rc_transpose_kernel(const double* __restrict__ Rcc, int m, int k
     }
 }
 
-// rows per dots tile: ~2 CTAs per SM, a multiple of 32 vector chunks
+// rows per dots tile: ~4 CTAs per SM, a multiple of 32 vector chunks
 template <typename V>
 int64_t reorth_tile_rows(int64_t ldq) {
     const int64_t quantum = 32 * VecT<V>::W;
-    return std::max<int64_t>(quantum, round_up(ceil_div(ldq, 148 * 2), quantum));
+    return std::max<int64_t>(quantum, round_up(ceil_div(ldq, 148 * 4), quantum));
+}
+
+__global__ void advance_step_kernel(int* jdev) {
+    if (threadIdx.x == 0) jdev[0] += 1;
+}
+
+template <typename V>
+struct StepPlan {
+    Cache* c;
+    int k, m, P, mean_y, gm, gr, gu;
+    int64_t ldq, tile_rows;
+    size_t smd, smu;
+};
+
+// Enqueue one Lanczos step (the step index lives in device memory).  j_host is only used
+// for the addresses of the multi-GPU all-reduces (eager mode).
+template <typename V>
+void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
+    Cache& c = *pl.c;
+    const LanczosState& st = c.st;
+    V* Q = (V*)c.Q;
+    V* r = (V*)c.r;
+    double* u = (double*)c.u;
+    const StepRef ref{st.jdev, pl.ldq, st.qscale, st.flags};
+    {
+        ProfScope ps(LOVE_PROF_SCALARS, s);
+        LOVE_LAUNCH(step_prologue_kernel, pl.gm, 256, 0, s, st, pl.k, c.tol, pl.m, (const double*)c.z[0],
+                    (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.mean_y);
+    }
+    {
+        ProfScope ps(LOVE_PROF_SCATTER, s);
+        launch_scatter<V>(c, Q, ref, u, s);
+    }
+    if (c.world > 1) {
+        ProfScope ps(LOVE_PROF_COMM, s);
+        allreduce_sum(c, u, pl.m, true, s);
+    }
+    double* zj = (double*)c.z[j_host & 1];
+    {
+        ProfScope ps(LOVE_PROF_KUU, s);
+        launch_kuu(c, u, zj, s);
+    }
+    {
+        ProfScope ps(LOVE_PROF_GATHER, s);
+        launch_gather<V>(c, zj, Q, ref, r, st.alpha_acc, s);
+    }
+    if (c.world > 1) {
+        ProfScope ps(LOVE_PROF_COMM, s);
+        allreduce_sum(c, st.alpha_acc + j_host, 1, true, s);
+    }
+    for (int pass = 0; pass < pl.P; ++pass) {
+        {
+            ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
+            LOVE_LAUNCH(reorth_dots_kernel<V>, pl.gr, 256, pl.smd, s, Q, pl.ldq, pl.tile_rows, pl.k, pass, r, st);
+        }
+        if (c.world > 1 && j_host < pl.k - 1) {
+            ProfScope ps(LOVE_PROF_COMM, s);
+            allreduce_sum(c, st.c_acc + ((int64_t)pass * pl.k + j_host) * (pl.k + 1), j_host + 1, true, s);
+        }
+        {
+            ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
+            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
+                        pass == pl.P - 1 ? 1 : 0, r, st);
+        }
+    }
+    if (c.world > 1 && j_host < pl.k - 1) {
+        ProfScope ps(LOVE_PROF_COMM, s);
+        allreduce_sum(c, st.beta2_acc + j_host, 1, true, s);
+    }
+    LOVE_LAUNCH(advance_step_kernel, 1, 32, 0, s, st.jdev);
 }
 
 template <typename V>
 void lanczos_impl(Cache& c, cudaStream_t s) {
-    const int k = c.k_req;
-    const int m = c.g.m_total;
-    const int64_t ldq = c.ldq;
-    V* Q = (V*)c.Q;
-    V* r = (V*)c.r;
-    V* u = (V*)c.u;
-    double* Rcc = (double*)c.Rc_col;
-    double* a = (double*)c.a;
+    StepPlan<V> pl;
+    pl.c = &c;
+    pl.k = c.k_req;
+    pl.m = c.g.m_total;
+    pl.P = c.reorth_passes;
+    pl.mean_y = c.probe == LOVE_PROBE_Y;
+    pl.ldq = c.ldq;
+    pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
+    pl.tile_rows = reorth_tile_rows<V>(c.ldq);
+    pl.gr = (int)ceil_div(c.ldq, pl.tile_rows);
+    pl.gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.ldq / VecT<V>::W, 256), 148 * 8));
+    pl.smd = sizeof(double) * round_up(std::max(pl.k + 1, 8), 2) + sizeof(V) * pl.tile_rows;
+    pl.smu = sizeof(double) * (pl.k + 1);
+    ensure_smem((const void*)reorth_dots_kernel<V>, pl.smd);
+    ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
     const LanczosState& st = c.st;
-    const int P = c.reorth_passes;
-    const int mean_y = c.probe == LOVE_PROBE_Y;
-    const int gm = (int)std::min<int64_t>(ceil_div(m, 256), 148 * 8);
-    const int64_t tile_rows = reorth_tile_rows<V>(ldq);
-    const int gr = (int)ceil_div(ldq, tile_rows);
-    const int gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ldq / VecT<V>::W, 256), 148 * 8));
-
-    LOVE_LAUNCH(norm2_kernel<V>, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.n, 256), 148 * 4)), 256,
-                0, s, Q, c.n, st.bnorm2);
-    if (c.world > 1) allreduce_sum(c, st.bnorm2, 1, true, s);
-    for (int j = 0; j < k; ++j) {
-        LOVE_LAUNCH(lanczos_scalars_kernel, 1, 32, 0, s, st, j, k, c.tol);
-        if (j > 0)
-            LOVE_LAUNCH(rc_update_kernel<V>, gm, 256, 0, s, st, j - 1, m, (const V*)c.z[(j - 1) & 1], Rcc, a,
-                        mean_y);
-        const V* qj = Q + (int64_t)j * ldq;
-        V* zj = (V*)c.z[j & 1];
-        launch_scatter<V>(c, qj, st.qscale + j, u, s);
-        if (c.world > 1) allreduce_sum(c, u, m, sizeof(V) == 8, s);
-        launch_kuu<V>(c, u, zj, s);
-        launch_gather<V>(c, zj, qj, st.qscale + j, r, st.alpha_acc + j, s);
-        if (c.world > 1) allreduce_sum(c, st.alpha_acc + j, 1, true, s);
-        if (j == k - 1) break;
-        for (int pass = 0; pass < P; ++pass) {
-            double* cacc = st.c_acc + ((int64_t)(pass & 1) * k + j) * (k + 1);
-            if (pass >= 2) cuda_check(cudaMemsetAsync(cacc, 0, sizeof(double) * (k + 1), s), "c zero");
-            const int from_r = pass == 0;
-            const size_t smd = sizeof(double) * round_up(j + 1, 2) + sizeof(V) * tile_rows;
-            LOVE_LAUNCH(reorth_dots_kernel<V>, gr, 256, smd, s, Q, ldq, tile_rows, j, r, from_r, st, cacc);
-            if (c.world > 1) allreduce_sum(c, cacc, j + 1, true, s);
-            LOVE_LAUNCH(reorth_update_kernel<V>, gu, 256, sizeof(double) * (j + 1), s, Q, ldq, c.n, j, r, from_r,
-                        st, cacc, pass == P - 1 ? st.beta2_acc + j : nullptr);
-        }
-        if (c.world > 1) allreduce_sum(c, st.beta2_acc + j, 1, true, s);
+    {
+        ProfScope ps(LOVE_PROF_SETUP, s);
+        LOVE_LAUNCH(norm2_kernel<V>, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.n, 256), 148 * 4)),
+                    256, 0, s, (const V*)c.Q, c.n, st.bnorm2);
     }
-    LOVE_LAUNCH(lanczos_scalars_kernel, 1, 32, 0, s, st, k, k, c.tol);
-    LOVE_LAUNCH(rc_update_kernel<V>, gm, 256, 0, s, st, k - 1, m, (const V*)c.z[(k - 1) & 1], Rcc, a, mean_y);
+    if (c.world > 1) {
+        ProfScope ps(LOVE_PROF_COMM, s);
+        allreduce_sum(c, st.bnorm2, 1, true, s);
+    }
+    const bool graph = c.world == 1 && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    if (graph) {
+        // one step as a CUDA graph, replayed k times (z buffer parity alternates: capture
+        // two steps so both parities are covered and replay the pair)
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+        enqueue_step<V>(pl, 0, s);
+        enqueue_step<V>(pl, 1, s);
+        cuda_check(cudaStreamEndCapture(s, &g), "end capture");
+        cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+        for (int j = 0; j + 1 < pl.k; j += 2) cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+        if (pl.k & 1) enqueue_step<V>(pl, pl.k - 1, s);
+        cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
+        cuda_check(cudaGraphDestroy(g), "graph destroy");
+    } else {
+        for (int j = 0; j < pl.k; ++j) enqueue_step<V>(pl, j, s);
+    }
+    {   // finalise index k-1: alpha_{k-1}, L_{k-1,k-1}, Rc[:, k-1], a
+        ProfScope ps(LOVE_PROF_SCALARS, s);
+        LOVE_LAUNCH(step_prologue_kernel, pl.gm, 256, 0, s, st, pl.k, c.tol, pl.m, (const double*)c.z[0],
+                    (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.mean_y);
+    }
 }
 
 }  // namespace
@@ -312,6 +417,7 @@ void run_lanczos(Cache& c, cudaStream_t s) {
 }
 
 void finish_cache(Cache& c, cudaStream_t s) {
+    ProfScope ps(LOVE_PROF_FINISH, s);
     const int m = c.g.m_total;
     c.k_pad = (int)round_up(std::max(c.k_eff, 1), 4);
     c.Rc = dalloc(c, c.vsize * (size_t)m * c.k_pad, s);

@@ -6,7 +6,9 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "love_internal.h"
 
@@ -25,6 +27,17 @@ void cuda_check(cudaError_t e, const char* what) {
     (void)cudaGetLastError();
     throw LoveError{e == cudaErrorMemoryAllocation ? LOVE_ERR_OOM : LOVE_ERR_CUDA,
                     std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+void ensure_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    if (bytes <= 48 * 1024) return;
+    std::lock_guard<std::mutex> g(mu);
+    size_t& cur = done[fn];
+    if (cur >= bytes) return;
+    cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem attr");
+    cur = bytes;
 }
 
 void* dalloc(Cache& c, size_t bytes, cudaStream_t s) {
@@ -82,6 +95,24 @@ __global__ void init_state_kernel(int* flags, int k, double* one) {
     }
 }
 
+// The build runs on a private non-blocking stream (the caller's stream may be the legacy
+// default stream, which cannot be captured into a CUDA graph); it is ordered after the
+// caller's stream by an event and the build synchronises it before returning.
+cudaStream_t work_stream(int dev) {
+    thread_local cudaStream_t streams[64] = {nullptr};
+    if (dev < 0 || dev >= 64) throw LoveError{LOVE_ERR_CUDA, "device index out of range"};
+    if (!streams[dev]) cuda_check(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking), "stream create");
+    return streams[dev];
+}
+
+void order_after(cudaStream_t waiter, cudaStream_t producer) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+    cuda_check(cudaEventRecord(e, producer), "event record");
+    cuda_check(cudaStreamWaitEvent(waiter, e, 0), "stream wait");
+    cuda_check(cudaEventDestroy(e), "event destroy");
+}
+
 love_status fail(const LoveError& e) {
     set_error(e.msg);
     return e.status;
@@ -131,8 +162,12 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
                              const double* y, int64_t n_local, int32_t k, const love_opts* opts,
                              const love_dist* dist, void* stream, love_cache** out) {
     Cache* c = nullptr;
-    cudaStream_t s = (cudaStream_t)stream;
+    cudaStream_t s = nullptr;
     try {
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        s = work_stream(dev);
+        order_after(s, (cudaStream_t)stream);
         if (out) *out = nullptr;
         validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
         love_opts o{};
@@ -166,6 +201,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->vsize = o.precision == LOVE_FP64 ? 8 : 4;
         c->probe = o.probe;
         c->prior = o.prior;
+        if (o.reorth_passes > 2) throw LoveError{LOVE_ERR_ARG, "reorth_passes must be 0, 1 or 2"};
         c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (o.precision == LOVE_FP64 ? 2 : 1);
         c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
         c->k_sample_req = o.k_sample;
@@ -186,7 +222,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             cuda_check(cudaMemcpyAsync(&c->n_global, dn, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "n d2h");
             cuda_check(cudaStreamSynchronize(s), "sync");
         }
-        if (k > c->n_global) throw LoveError{LOVE_ERR_ARG, "k exceeds the number of training points"};
+        if (c->n_global < 1) throw LoveError{LOVE_ERR_ARG, "no training points"};
+        if (k > c->n_global) k = (int32_t)c->n_global;     // a Krylov space has at most n dimensions
         c->k_req = k;
         const int M = g.m_total;
         const size_t vs = c->vsize;
@@ -202,6 +239,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->cell_item_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
         for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * std::max<int64_t>(c->n, 1), s);
         c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        prof_begin(LOVE_PROF_SETUP, s);
         launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);
         {   // the range check is global: every rank must agree before continuing
             float fl = 0.f;
@@ -224,16 +262,17 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->item_cell = (int*)dalloc(*c, sizeof(int) * std::max<int64_t>(c->n_items, 1), s);
         c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 1), s);
         launch_build_items(*c, s);
-        c->M = dalloc(*c, vs * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
+        c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
 
         // ---- K_UU
         setup_kuu(*c, s);
+        prof_end(LOVE_PROF_SETUP, s);
 
         // ---- Lanczos state
         c->r = dalloc(*c, vs * c->ldq, s);
-        c->u = dalloc(*c, vs * M, s);
-        c->z[0] = dalloc(*c, vs * M, s);
-        c->z[1] = dalloc(*c, vs * M, s);
+        c->u = dalloc(*c, sizeof(double) * M, s);
+        c->z[0] = dalloc(*c, sizeof(double) * M, s);
+        c->z[1] = dalloc(*c, sizeof(double) * M, s);
         c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
         c->a = dalloc(*c, sizeof(double) * M, s);
         c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
@@ -256,7 +295,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             st.amax_bmax = p; p += 2;
             c->one = p; p += 1;
             st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
-            st.rc_done = st.flags + 4;
+            st.jdev = st.flags + 4;
             LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
         }
 
@@ -287,7 +326,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         return LOVE_OK;
     } catch (const LoveError& e) {
         if (c) {
-            cudaStreamSynchronize(s);
+            if (s) cudaStreamSynchronize(s);
             release(c);
         }
         return fail(e);
@@ -387,25 +426,27 @@ love_status love_ski_mvm(const love_cache* cache, const void* v, void* out, void
         const size_t vs = c->vsize;
         void* vsrt = tmp.get(vs * c->ldq);
         void* rs = tmp.get(vs * c->ldq);
-        void* u = tmp.get(vs * c->g.m_total);
-        void* z = tmp.get(vs * c->g.m_total);
-        w.M = tmp.get(vs * (size_t)(1 << (2 * c->g.d)) * std::max<int64_t>(c->n_items, 1));
-        if (c->fft_buf) w.fft_buf = tmp.get(2 * vs * c->fft_N);
+        double* u = (double*)tmp.get(sizeof(double) * c->g.m_total);
+        double* z = (double*)tmp.get(sizeof(double) * c->g.m_total);
+        w.M = tmp.get(sizeof(double) * (size_t)(1 << (2 * c->g.d)) * std::max<int64_t>(c->n_items, 1));
+        if (c->fft_buf) w.fft_buf = tmp.get(sizeof(double2) * c->fft_N);
         if (c->ktmp[0]) {
-            w.ktmp[0] = tmp.get(vs * c->g.m_total);
-            w.ktmp[1] = tmp.get(vs * c->g.m_total);
+            w.ktmp[0] = tmp.get(sizeof(double) * c->g.m_total);
+            w.ktmp[1] = tmp.get(sizeof(double) * c->g.m_total);
         }
         if (c->precision == LOVE_FP64) {
             launch_permute<double>(w, (const double*)v, (double*)vsrt, true, s);
-            launch_scatter<double>(w, (const double*)vsrt, c->one, (double*)u, s);
-            launch_kuu<double>(w, (const double*)u, (double*)z, s);
-            launch_gather<double>(w, (const double*)z, (const double*)vsrt, c->one, (double*)rs, nullptr, s);
+            const StepRef ref{nullptr, 0, c->one, nullptr};
+            launch_scatter<double>(w, (const double*)vsrt, ref, u, s);
+            launch_kuu(w, u, z, s);
+            launch_gather<double>(w, z, (const double*)vsrt, ref, (double*)rs, nullptr, s);
             launch_permute<double>(w, (const double*)rs, (double*)out, false, s);
         } else {
             launch_permute<float>(w, (const float*)v, (float*)vsrt, true, s);
-            launch_scatter<float>(w, (const float*)vsrt, c->one, (float*)u, s);
-            launch_kuu<float>(w, (const float*)u, (float*)z, s);
-            launch_gather<float>(w, (const float*)z, (const float*)vsrt, c->one, (float*)rs, nullptr, s);
+            const StepRef ref{nullptr, 0, c->one, nullptr};
+            launch_scatter<float>(w, (const float*)vsrt, ref, u, s);
+            launch_kuu(w, u, z, s);
+            launch_gather<float>(w, z, (const float*)vsrt, ref, (float*)rs, nullptr, s);
             launch_permute<float>(w, (const float*)rs, (float*)out, false, s);
         }
         cuda_check(cudaGetLastError(), "ski_mvm launch");
@@ -423,14 +464,20 @@ love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void
         TempPool tmp(s);
         Cache w = *c;
         w.allocs.clear();
-        const size_t vs = c->vsize;
-        if (c->fft_buf) w.fft_buf = tmp.get(2 * vs * c->fft_N);
+        if (c->fft_buf) w.fft_buf = tmp.get(sizeof(double2) * c->fft_N);
         if (c->ktmp[0]) {
-            w.ktmp[0] = tmp.get(vs * c->g.m_total);
-            w.ktmp[1] = tmp.get(vs * c->g.m_total);
+            w.ktmp[0] = tmp.get(sizeof(double) * c->g.m_total);
+            w.ktmp[1] = tmp.get(sizeof(double) * c->g.m_total);
         }
-        if (c->precision == LOVE_FP64) launch_kuu<double>(w, (const double*)u, (double*)out, s);
-        else launch_kuu<float>(w, (const float*)u, (float*)out, s);
+        if (c->precision == LOVE_FP64) {
+            launch_kuu(w, (const double*)u, (double*)out, s);
+        } else {
+            double* ud = (double*)tmp.get(sizeof(double) * c->g.m_total);
+            double* zd = (double*)tmp.get(sizeof(double) * c->g.m_total);
+            launch_convert<float, double>((const float*)u, ud, c->g.m_total, s);
+            launch_kuu(w, ud, zd, s);
+            launch_convert<double, float>(zd, (float*)out, c->g.m_total, s);
+        }
         cuda_check(cudaGetLastError(), "kuu_mvm launch");
         return LOVE_OK;
     } catch (const LoveError& e) {

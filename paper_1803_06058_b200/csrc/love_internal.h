@@ -22,6 +22,18 @@ struct GridDev {
     int m_total;
 };
 
+// Which Lanczos column a step kernel works on.  Step kernels read the step index j from
+// device memory (so one captured step graph can be replayed k times); the vector they use
+// is base + j * ld, scaled by scale[j]; they do nothing once flags[0] (done) is set.
+struct StepRef {
+    const int* jdev;        // nullptr -> j = 0
+    int64_t ld;             // column stride (0 for a single vector)
+    const double* scale;    // scale[j] multiplies the stored column
+    const int* flags;       // nullptr -> never skip
+};
+__device__ __forceinline__ int step_j(const StepRef& r) { return r.jdev ? *r.jdev : 0; }
+__device__ __forceinline__ bool step_done(const StepRef& r) { return r.flags != nullptr && r.flags[0] != 0; }
+
 // Device-resident Lanczos state (fp64).  Written only by lanczos_scalars_kernel / the
 // finalize kernel; the accumulators are summed into with atomics by the step kernels and
 // (multi-GPU) all-reduced between kernels.
@@ -38,7 +50,7 @@ struct LanczosState {
     double* g;             // [k]        L^{-1} e_1
     double* amax_bmax;     // [2]
     int* flags;            // [4]        done, k_eff, notpd, zero_probe
-    int* rc_done;          // [1]        Rc columns written
+    int* jdev;             // [1]        current step index j
 };
 
 struct Cache {
@@ -67,19 +79,22 @@ struct Cache {
 
     // ---------------- K_UU
     double* cols64 = nullptr;            // [sum m_d] Toeplitz first columns (fp64)
-    void* cols = nullptr;                // same in V
+    double h_cols64[3][4] = {};          // host copy of c_d[0..3] (variance-query prior)
     int fft_N = 0, fft_N1 = 0, fft_N2 = 0;
-    void* lam = nullptr;                 // V[N] eigenvalues * s^2/N in pass-B layout
-    void* fft_buf = nullptr;             // complex V[N]
-    void* ktmp[2] = {nullptr, nullptr};  // V[m] scratch for axis passes
+    void* lam = nullptr;                 // double[N] eigenvalues * s^2/N in pass-B layout
+    void* fft_buf = nullptr;             // double2[N]
+    void* tw1 = nullptr;                 // double2 twiddle tables (line FFTs of N1 / small N)
+    void* tw2 = nullptr;                 // (line FFTs of N2)
+    void* twF = nullptr;                 // exp(-2 pi i k / N), k < N1
+    void* ktmp[2] = {nullptr, nullptr};  // double[m] scratch for axis passes
 
     // ---------------- Lanczos
     int k_alloc = 0;
     void* Q = nullptr;                   // V[ldq * (k+1)] column-major, unnormalised columns
     void* r = nullptr;                   // V[ldq]
-    void* u = nullptr;                   // V[m]
-    void* z[2] = {nullptr, nullptr};     // V[m]
-    void* M = nullptr;                   // V[4^d * n_items] per-item stencil moments
+    void* u = nullptr;                   // double[m]
+    void* z[2] = {nullptr, nullptr};     // double[m]
+    void* M = nullptr;                   // double[4^d * n_items] per-item stencil moments
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)
     void* Rc = nullptr;                  // V[m * k_pad] row-major
     void* a = nullptr;                   // double[m] mean cache
@@ -107,6 +122,8 @@ struct LoveError {
     std::string msg;
 };
 void cuda_check(cudaError_t e, const char* what);
+// raises a kernel's dynamic shared-memory limit once (cudaFuncSetAttribute is a host call)
+void ensure_smem(const void* fn, size_t bytes);
 void* dalloc(Cache& c, size_t bytes, cudaStream_t s);   // zero-filled, owned by the cache
 
 // ---------------------------------------------------------------------------------------
@@ -120,16 +137,16 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
 void launch_build_items(Cache& c, cudaStream_t s);                 // after n_items known
 int64_t count_items_host(Cache& c, cudaStream_t s);                 // syncs
 // ski.cu
-template <typename V> void launch_scatter(const Cache& c, const V* q, const double* scale,
-                                          V* u, cudaStream_t s);
-template <typename V> void launch_gather(const Cache& c, const V* z, const V* q,
-                                         const double* qscale, V* r, double* alpha_acc,
-                                         cudaStream_t s);
+template <typename V> void launch_scatter(const Cache& c, const V* qbase, StepRef ref, double* u,
+                                          cudaStream_t s);
+template <typename V> void launch_gather(const Cache& c, const double* z, const V* qbase, StepRef ref, V* r,
+                                         double* alpha_base, cudaStream_t s);
+template <typename A, typename B> void launch_convert(const A* in, B* out, int64_t n, cudaStream_t s);
 template <typename V> void launch_permute(const Cache& c, const V* in, V* out, bool to_sorted,
                                           cudaStream_t s);
 // kuu.cu
 void setup_kuu(Cache& c, cudaStream_t s);
-template <typename V> void launch_kuu(const Cache& c, const V* u, V* z, cudaStream_t s);
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
@@ -141,6 +158,16 @@ void build_sampling_cache(Cache& c, cudaStream_t s);
 template <typename V> void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns,
                                          uint64_t seed, const double* zeta, V* out,
                                          cudaStream_t s);
+// profile.cpp (phase timing, love_profile_*)
+bool profiling();
+void prof_begin(int cat, cudaStream_t s);
+void prof_end(int cat, cudaStream_t s);
+struct ProfScope {
+    int cat;
+    cudaStream_t s;
+    ProfScope(int c, cudaStream_t st) : cat(c), s(st) { prof_begin(cat, s); }
+    ~ProfScope() { prof_end(cat, s); }
+};
 // nccl_shim.cpp
 bool nccl_available(std::string* why);
 love_status nccl_get_unique_id(void* out128);
