@@ -76,11 +76,15 @@ typedef struct {
     int32_t precision;      /* LOVE_FP32 (V = float, reductions in fp64) | LOVE_FP64 (V = double) */
     int32_t probe;          /* LOVE_PROBE_Y (default: b = y, reading A1) | LOVE_PROBE_AVGCOL (reserved) */
     int32_t prior;          /* LOVE_PRIOR_SKI (w*^T K_UU w*, default) | LOVE_PRIOR_EXACT (k(x*,x*)) */
-    int32_t reorth_passes;  /* full reorthogonalisation passes per step: 0 => 1 (fp32) / 2 (fp64) */
+    int32_t reorth_passes;  /* classical Gram-Schmidt passes of the full reorthogonalisation:
+                               0 => 1 (fp32) / 2 (fp64, CGS2) */
     double breakdown_tol;   /* tau of the breakdown rule (reading A12); 0 => 1e-6 (fp32) / 1e-10 (fp64) */
     int32_t k_sample;       /* k' of the sampling cache; 0 => no sampling cache */
-    int32_t reserved;
+    int32_t lanczos_mode;   /* LOVE_LANCZOS_AUTO (0) | LOVE_LANCZOS_TWO_PASS (1): classical Gram-Schmidt,
+                               Q read twice per step | LOVE_LANCZOS_ONE_READ (2, fp32 only): the
+                               lagged one-read fused pass (lanczos_fused.cu) */
 } love_opts;
+enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ = 2 };
 
 /* Data-parallel sharding of the training points.  Every rank calls
  * love_build_cache with its own X/y shard and identical grid/kernel/sigma^2/k/opts; the
@@ -209,7 +213,8 @@ enum {
     LOVE_PROF_SAMPLE_CACHE = 9,  /* sampling root */
     LOVE_PROF_SAMPLE = 10,       /* sample draws */
     LOVE_PROF_COMM = 11,         /* NCCL all-reduces */
-    LOVE_PROF_N = 12
+    LOVE_PROF_FUSED_PASS = 12,   /* one-read pass: lagged update + gather + moments + Gram dots */
+    LOVE_PROF_N = 13
 };
 void love_profile_enable(int32_t on);
 /* ms_out, calls_out: HOST arrays of LOVE_PROF_N entries (either may be NULL); reset != 0

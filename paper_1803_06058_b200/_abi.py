@@ -16,7 +16,7 @@ LOVE_PROBE_Y, LOVE_PROBE_AVGCOL = 0, 1
 LOVE_PRIOR_SKI, LOVE_PRIOR_EXACT = 0, 1
 LOVE_EXPORT_RC, LOVE_EXPORT_MEAN, LOVE_EXPORT_S, LOVE_EXPORT_PERM = 0, 1, 2, 3
 PROF_NAMES = ["setup", "scatter", "kuu", "gather", "reorth_dots", "reorth_update", "scalars_rc",
-              "finish", "query", "sample_cache", "sample", "comm"]
+              "finish", "query", "sample_cache", "sample", "comm", "fused_pass"]
 
 
 class love_grid(ctypes.Structure):
@@ -31,7 +31,7 @@ class love_rbf(ctypes.Structure):
 class love_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("probe", ctypes.c_int32), ("prior", ctypes.c_int32),
                 ("reorth_passes", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
-                ("k_sample", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32)]
 
 
 class love_dist(ctypes.Structure):

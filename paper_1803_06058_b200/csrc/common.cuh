@@ -38,6 +38,17 @@ __device__ __forceinline__ void keys4(T f, T w[4]) {
     w[3] = T(0.5) * f3 - T(0.5) * f2;
 }
 
+// single Keys weight: slot 0..3 of keys4 (nodes j-1, j, j+1, j+2), branch-free
+template <typename T>
+__device__ __forceinline__ T keys1(T f, int slot) {
+    // coefficients (f^3, f^2, f^1, f^0) of the four cubics of keys4, packed per slot
+    const T c3 = slot == 0 ? T(-0.5) : slot == 1 ? T(1.5) : slot == 2 ? T(-1.5) : T(0.5);
+    const T c2 = slot == 0 ? T(1) : slot == 1 ? T(-2.5) : slot == 2 ? T(2) : T(-0.5);
+    const T c1 = slot == 0 ? T(-0.5) : slot == 2 ? T(0.5) : T(0);
+    const T c0 = slot == 1 ? T(1) : T(0);
+    return ((c3 * f + c2) * f + c1) * f + c0;
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

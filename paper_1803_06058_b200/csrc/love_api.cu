@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -164,12 +165,12 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
     Cache* c = nullptr;
     cudaStream_t s = nullptr;
     try {
+        if (out) *out = nullptr;
+        validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
         int dev = 0;
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
         s = work_stream(dev);
         order_after(s, (cudaStream_t)stream);
-        if (out) *out = nullptr;
-        validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
         love_opts o{};
         o.precision = LOVE_FP32;
         if (opts) o = *opts;
@@ -203,6 +204,12 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->prior = o.prior;
         if (o.reorth_passes > 2) throw LoveError{LOVE_ERR_ARG, "reorth_passes must be 0, 1 or 2"};
         c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (o.precision == LOVE_FP64 ? 2 : 1);
+        int mode = o.lanczos_mode;
+        if (const char* e = std::getenv("LOVE_LANCZOS_MODE")) mode = std::atoi(e);
+        if (mode < 0 || mode > 2) throw LoveError{LOVE_ERR_ARG, "bad lanczos_mode"};
+        if (mode == LOVE_LANCZOS_ONE_READ && o.precision != LOVE_FP32)
+            throw LoveError{LOVE_ERR_ARG, "the one-read Lanczos pass is fp32 only"};
+        c->fused = mode == LOVE_LANCZOS_ONE_READ;
         c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
         c->k_sample_req = o.k_sample;
         c->n = n_local;
@@ -237,7 +244,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->perm = (int*)dalloc(*c, sizeof(int) * std::max<int64_t>(c->n, 1), s);
         c->cell_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
         c->cell_item_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
-        for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * std::max<int64_t>(c->n, 1), s);
+        for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * (c->ldq + 4), s);   // padded to 16 B units
         c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
         prof_begin(LOVE_PROF_SETUP, s);
         launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);
@@ -259,8 +266,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         }
         launch_counting_sort(*c, cell, frac64, y, c->n, c->Q, s);
         c->n_items = count_items_host(*c, s);
-        c->item_cell = (int*)dalloc(*c, sizeof(int) * std::max<int64_t>(c->n_items, 1), s);
-        c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 1), s);
+        c->item_cell = (int*)dalloc(*c, sizeof(int) * (c->n_items + 8), s);     // padded: staged in 16 B units
+        c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
         launch_build_items(*c, s);
         c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
 
@@ -271,8 +278,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         // ---- Lanczos state
         c->r = dalloc(*c, vs * c->ldq, s);
         c->u = dalloc(*c, sizeof(double) * M, s);
-        c->z[0] = dalloc(*c, sizeof(double) * M, s);
-        c->z[1] = dalloc(*c, sizeof(double) * M, s);
+        c->z[0] = dalloc(*c, sizeof(double) * (M + 4), s);      // padded: tiles stage z in 16-byte units
+        c->z[1] = dalloc(*c, sizeof(double) * (M + 4), s);
         c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
         c->a = dalloc(*c, sizeof(double) * M, s);
         c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
@@ -300,7 +307,9 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         }
 
         // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
-        run_lanczos(*c, s);
+        if (c->fused) setup_fused(*c, s);
+        if (c->fused) run_lanczos_fused(*c, s);
+        else run_lanczos(*c, s);
         int hfl[4];
         double bn2 = 0;
         cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");

@@ -51,6 +51,10 @@ struct LanczosState {
     double* amax_bmax;     // [2]
     int* flags;            // [4]        done, k_eff, notpd, zero_probe
     int* jdev;             // [1]        current step index j
+    // fused (one-read) mode
+    double* AB;            // [k][2][k+1] Gram sums A_i = Q~_i^T r~_j, B_i = Q~_i^T Q~_j of pass j
+    double* cvec;          // [k+1]      reorthogonalisation coefficients on Q~_i for the next pass
+    double* gam;           // [k+1]      coefficients of u~_i in u~_{j+1}
 };
 
 struct Cache {
@@ -95,7 +99,18 @@ struct Cache {
     void* u = nullptr;                   // double[m]
     void* z[2] = {nullptr, nullptr};     // double[m]
     void* M = nullptr;                   // double[4^d * n_items] per-item stencil moments
+    void* M2 = nullptr;                  // second moments buffer (fused mode: moments of Q~_j)
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)
+    // fused (one-read) Lanczos mode
+    bool fused = false;
+    int tile_cap = 0;                    // max points per fused-pass tile
+    int64_t n_tiles = 0;
+    int* tile_first = nullptr;           // [n_tiles+1] first item of each tile
+    void* tile_meta = nullptr;           // [n_tiles] per-tile descriptors (lanczos_fused.cu)
+    alignas(64) unsigned char qmap[128] = {};   // CUtensorMap of Q~ (lanczos_fused.cu)
+    int fused_threads = 256;
+    double* U64 = nullptr;               // [3][m] u~_{j-1}, u~_j, u~_{j+1} (rolling, fp64)
+    float* U32 = nullptr;                // [k+1][m] every u~_i in fp32 (reorth correction)
     void* Rc = nullptr;                  // V[m * k_pad] row-major
     void* a = nullptr;                   // double[m] mean cache
     double* one = nullptr;               // device 1.0 (scale of un-normalised MVMs)
@@ -142,6 +157,7 @@ template <typename V> void launch_scatter(const Cache& c, const V* qbase, StepRe
 template <typename V> void launch_gather(const Cache& c, const double* z, const V* qbase, StepRef ref, V* r,
                                          double* alpha_base, cudaStream_t s);
 template <typename A, typename B> void launch_convert(const A* in, B* out, int64_t n, cudaStream_t s);
+void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s);   // from c.M
 template <typename V> void launch_permute(const Cache& c, const V* in, V* out, bool to_sorted,
                                           cudaStream_t s);
 // kuu.cu
@@ -149,6 +165,8 @@ void setup_kuu(Cache& c, cudaStream_t s);
 void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
+void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu
+void setup_fused(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
 // query.cu
 template <typename V> void launch_predict(const Cache& c, const double* Xa, const double* Xb,

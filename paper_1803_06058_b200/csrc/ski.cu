@@ -12,20 +12,14 @@
 //    reuses them for every point of the item.
 #include <cuda_runtime.h>
 
-#include <type_traits>
-
 #include "love_internal.h"
+#include "ski_device.cuh"
 
 namespace love {
 
 namespace {
 
-template <int D> struct Slots { static constexpr int value = 1 << (2 * D); };
-
-// arithmetic type of the per-point stencil sums: fp64 for d <= 2 (m-side precision plan),
-// V for the 64-slot 3-D stencil (registers; 3-D configs are far from the cancellation regime)
-template <typename V, int D> struct AccT { using type = double; };
-template <int D> struct AccT<float, D> { using type = typename std::conditional<D == 3, float, double>::type; };
+constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
 
 template <typename V, int D>
 __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
@@ -41,11 +35,10 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
     A acc[S];
 #pragma unroll
     for (int l = 0; l < S; ++l) acc[l] = A(0);
-    constexpr int B = 8;                    // points loaded per batch (memory-level parallelism)
-    for (int pb = p0; pb < p1; pb += B) {
-        A qv[B], fa[B], fb[B], fc[B];
+    for (int pb = p0; pb < p1; pb += kBatch) {
+        A qv[kBatch], fa[kBatch], fb[kBatch], fc[kBatch];
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
+        for (int u = 0; u < kBatch; ++u) {
             const int p = pb + u;
             const bool in = p < p1;
             qv[u] = in ? (A)q[p] : A(0);    // q = 0 makes padded lanes contribute nothing
@@ -54,29 +47,12 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
             fc[u] = (D > 2 && in) ? (A)f2[p] : A(0);
         }
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
+        for (int u = 0; u < kBatch; ++u) {
             A w0[4], w1[4], w2[4];
             keys4<A>(fa[u], w0);
             if (D > 1) keys4<A>(fb[u], w1);
             if (D > 2) keys4<A>(fc[u], w2);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const A ta = qv[u] * w0[a];
-                if (D == 1) {
-                    acc[a] += ta;
-                } else {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const A tb = ta * w1[b];
-                        if (D == 2) {
-                            acc[a * 4 + b] += tb;
-                        } else {
-#pragma unroll
-                            for (int cc = 0; cc < 4; ++cc) acc[(a * 4 + b) * 4 + cc] += tb * w2[cc];
-                        }
-                    }
-                }
-            }
+            stencil_accum<A, D>(acc, qv[u], w0, w1, w2);
         }
     }
 #pragma unroll
@@ -91,47 +67,7 @@ __global__ void __launch_bounds__(256) nodepass_kernel(GridDev g, int64_t n_item
                                                        double* __restrict__ u) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.m_total || step_done(ref)) return;
-    int ic[3] = {0, 0, 0};
-    {
-        int rem = i;
-        for (int d = 0; d < D; ++d) {
-            ic[d] = rem / g.stride[d];
-            rem -= ic[d] * g.stride[d];
-        }
-    }
-    double sum = 0.0;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int c0 = ic[0] - a + 1;
-        if (c0 < 0 || c0 >= g.m[0]) continue;
-        if (D == 1) {
-            const int cf = c0;
-            const int e = cis[cf + 1];
-            for (int it = cis[cf]; it < e; ++it) sum += M[(int64_t)a * n_items + it];
-            continue;
-        }
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int c1 = ic[1] - b + 1;
-            if (c1 < 0 || c1 >= g.m[1]) continue;
-            if (D == 2) {
-                const int cf = c0 * g.stride[0] + c1;
-                const int e = cis[cf + 1];
-                for (int it = cis[cf]; it < e; ++it) sum += M[(int64_t)(a * 4 + b) * n_items + it];
-                continue;
-            }
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                const int c2 = ic[2] - cc + 1;
-                if (c2 < 0 || c2 >= g.m[2]) continue;
-                const int cf = c0 * g.stride[0] + c1 * g.stride[1] + c2;
-                const int e = cis[cf + 1];
-                for (int it = cis[cf]; it < e; ++it)
-                    sum += M[(int64_t)((a * 4 + b) * 4 + cc) * n_items + it];
-            }
-        }
-    }
-    u[i] = sum * ref.scale[step_j(ref)];
+    u[i] = node_pull<D>(g, n_items, cis, M, i) * ref.scale[step_j(ref)];
 }
 
 template <typename V, int D>
@@ -153,40 +89,13 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
     const A vsc = (A)sc, vsig = (A)(sigma2 * sc);
     double alpha = 0.0;
     if (it < n_items) {
-        const int c = item_cell[it];
-        int base = 0;
-        {
-            int rem = c;
-            for (int d = 0; d < D; ++d) {
-                const int cd = rem / g.stride[d];
-                rem -= cd * g.stride[d];
-                base += (cd - 1) * g.stride[d];
-            }
-        }
         A zl[S];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            if (D == 1) {
-                zl[a] = (A)z[base + a];
-            } else {
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    if (D == 2) {
-                        zl[a * 4 + b] = (A)z[base + a * g.stride[0] + b];
-                    } else {
-#pragma unroll
-                        for (int cc = 0; cc < 4; ++cc)
-                            zl[(a * 4 + b) * 4 + cc] = (A)z[base + a * g.stride[0] + b * g.stride[1] + cc];
-                    }
-                }
-            }
-        }
+        load_stencil<A, D>(g, z, stencil_base<D>(g, item_cell[it]), zl);
         const int p0 = item_start[it], p1 = item_start[it + 1];
-        constexpr int B = 8;                // points loaded per batch
-        for (int pb = p0; pb < p1; pb += B) {
-            A qv[B], fa[B], fb[B], fc[B];
+        for (int pb = p0; pb < p1; pb += kBatch) {
+            A qv[kBatch], fa[kBatch], fb[kBatch], fc[kBatch];
 #pragma unroll
-            for (int u = 0; u < B; ++u) {
+            for (int u = 0; u < kBatch; ++u) {
                 const int p = pb + u;
                 const bool in = p < p1;
                 qv[u] = in ? (A)q[p] : A(0);
@@ -195,33 +104,12 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                 fc[u] = (D > 2 && in) ? (A)f2[p] : A(0);
             }
 #pragma unroll
-            for (int u = 0; u < B; ++u) {
+            for (int u = 0; u < kBatch; ++u) {
                 A w0[4], w1[4], w2[4];
                 keys4<A>(fa[u], w0);
                 if (D > 1) keys4<A>(fb[u], w1);
                 if (D > 2) keys4<A>(fc[u], w2);
-                A acc = A(0);
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    if (D == 1) {
-                        acc += w0[a] * zl[a];
-                    } else {
-                        A ta = A(0);
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) {
-                            if (D == 2) {
-                                ta += w1[b] * zl[a * 4 + b];
-                            } else {
-                                A tb = A(0);
-#pragma unroll
-                                for (int cc = 0; cc < 4; ++cc) tb += w2[cc] * zl[(a * 4 + b) * 4 + cc];
-                                ta += w1[b] * tb;
-                            }
-                        }
-                        acc += w0[a] * ta;
-                    }
-                }
-                const V rv = (V)(acc + vsig * qv[u]);
+                const V rv = (V)(stencil_dot<A, D>(w0, w1, w2, zl) + vsig * qv[u]);
                 if (pb + u < p1) {
                     r[pb + u] = rv;
                     alpha += (double)(vsc * qv[u]) * (double)rv;
@@ -245,32 +133,40 @@ __global__ void permute_kernel(const int* __restrict__ perm, int64_t n, const V*
     }
 }
 
+template <typename A, typename B>
+__global__ void convert_kernel(const A* __restrict__ in, B* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (B)in[i];
+}
+
 }  // namespace
+
+void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s) {
+    const int gm = (int)ceil_div(c.g.m_total, 256);
+    const double* M = (const double*)c.M;
+    switch (c.g.d) {
+        case 1: LOVE_LAUNCH((nodepass_kernel<1>), gm, 256, 0, s, c.g, c.n_items, c.cell_item_start, M, ref, u); break;
+        case 2: LOVE_LAUNCH((nodepass_kernel<2>), gm, 256, 0, s, c.g, c.n_items, c.cell_item_start, M, ref, u); break;
+        default: LOVE_LAUNCH((nodepass_kernel<3>), gm, 256, 0, s, c.g, c.n_items, c.cell_item_start, M, ref, u); break;
+    }
+}
 
 template <typename V>
 void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStream_t s) {
     const int64_t ni = c.n_items;
-    const int mt = c.g.m_total;
     const int gi = (int)std::max<int64_t>(1, ceil_div(ni, 256));
-    const int gm = (int)ceil_div(mt, 256);
     const V* f0 = (const V*)c.frac[0];
     const V* f1 = (const V*)c.frac[1];
     const V* f2 = (const V*)c.frac[2];
     double* M = (double*)c.M;
-    switch (c.g.d) {
-        case 1:
-            if (ni) LOVE_LAUNCH((moments_kernel<V, 1>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M);
-            LOVE_LAUNCH((nodepass_kernel<1>), gm, 256, 0, s, c.g, ni, c.cell_item_start, M, ref, u);
-            break;
-        case 2:
-            if (ni) LOVE_LAUNCH((moments_kernel<V, 2>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M);
-            LOVE_LAUNCH((nodepass_kernel<2>), gm, 256, 0, s, c.g, ni, c.cell_item_start, M, ref, u);
-            break;
-        default:
-            if (ni) LOVE_LAUNCH((moments_kernel<V, 3>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M);
-            LOVE_LAUNCH((nodepass_kernel<3>), gm, 256, 0, s, c.g, ni, c.cell_item_start, M, ref, u);
-            break;
+    if (ni) {
+        switch (c.g.d) {
+            case 1: LOVE_LAUNCH((moments_kernel<V, 1>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+            case 2: LOVE_LAUNCH((moments_kernel<V, 2>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+            default: LOVE_LAUNCH((moments_kernel<V, 3>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+        }
     }
+    launch_nodepass(c, ref, u, s);
 }
 
 template <typename V>
@@ -282,20 +178,15 @@ void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* 
     const V* f0 = (const V*)c.frac[0];
     const V* f1 = (const V*)c.frac[1];
     const V* f2 = (const V*)c.frac[2];
+#define LOVE_GATHER(DD)                                                                                       \
+    LOVE_LAUNCH((gather_kernel<V, DD>), gi, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1, f2, z, q,  \
+                ref, c.sigma2, r, alpha_base)
     switch (c.g.d) {
-        case 1:
-            LOVE_LAUNCH((gather_kernel<V, 1>), gi, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1,
-                        f2, z, q, ref, c.sigma2, r, alpha_base);
-            break;
-        case 2:
-            LOVE_LAUNCH((gather_kernel<V, 2>), gi, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1,
-                        f2, z, q, ref, c.sigma2, r, alpha_base);
-            break;
-        default:
-            LOVE_LAUNCH((gather_kernel<V, 3>), gi, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1,
-                        f2, z, q, ref, c.sigma2, r, alpha_base);
-            break;
+        case 1: LOVE_GATHER(1); break;
+        case 2: LOVE_GATHER(2); break;
+        default: LOVE_GATHER(3); break;
     }
+#undef LOVE_GATHER
 }
 
 template <typename V>
@@ -303,12 +194,6 @@ void launch_permute(const Cache& c, const V* in, V* out, bool to_sorted, cudaStr
     if (c.n == 0) return;
     const int gb = (int)std::min<int64_t>(ceil_div(c.n, 256), 148 * 32);
     LOVE_LAUNCH(permute_kernel<V>, gb, 256, 0, s, c.perm, c.n, in, out, to_sorted ? 1 : 0);
-}
-
-template <typename A, typename B>
-__global__ void convert_kernel(const A* __restrict__ in, B* __restrict__ out, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = (B)in[i];
 }
 
 template <typename A, typename B>

@@ -76,7 +76,7 @@ class LoveCache:
     def build(cls, X, y, m: Sequence[int], lo: Sequence[float], h: Sequence[float],
               lengthscale: Sequence[float], outputscale: float, sigma2: float, k: int,
               precision: str = "fp32", prior: str = "ski", k_sample: int = 0,
-              reorth_passes: int = 0, breakdown_tol: float = 0.0,
+              reorth_passes: int = 0, breakdown_tol: float = 0.0, lanczos_mode: str = "auto",
               rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
               stream=None) -> "LoveCache":
         d = len(m)
@@ -97,6 +97,7 @@ class LoveCache:
         o.reorth_passes = int(reorth_passes)
         o.breakdown_tol = float(breakdown_tol)
         o.k_sample = int(k_sample)
+        o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2}[lanczos_mode]
         dist = None
         idbuf = None
         if world > 1:
