@@ -390,12 +390,18 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         // two steps so both parities are covered and replay the pair)
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
+        const int64_t before = g_launch_count.load();      // captured launches run once per replay
         cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
         enqueue_step<V>(pl, 0, s);
         enqueue_step<V>(pl, 1, s);
         cuda_check(cudaStreamEndCapture(s, &g), "end capture");
         cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
-        for (int j = 0; j + 1 < pl.k; j += 2) cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+        const int64_t nodes = g_launch_count.load() - before;
+        g_launch_count -= nodes;
+        for (int j = 0; j + 1 < pl.k; j += 2) {
+            cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+            g_launch_count += nodes;
+        }
         if (pl.k & 1) enqueue_step<V>(pl, pl.k - 1, s);
         cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
         cuda_check(cudaGraphDestroy(g), "graph destroy");

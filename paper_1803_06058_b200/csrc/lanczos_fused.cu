@@ -765,11 +765,17 @@ void run_lanczos_fused(Cache& c, cudaStream_t s) {
     if (graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
+        const int64_t before = g_launch_count.load();      // captured launches run once per replay
         cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
         enqueue_fused_step(c, 0, wbuf, s);
         cuda_check(cudaStreamEndCapture(s, &g), "end capture");
         cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
-        for (int j = 0; j < k; ++j) cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+        const int64_t nodes = g_launch_count.load() - before;
+        g_launch_count -= nodes;
+        for (int j = 0; j < k; ++j) {
+            cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+            g_launch_count += nodes;
+        }
         cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
         cuda_check(cudaGraphDestroy(g), "graph destroy");
     } else {

@@ -1,0 +1,93 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The oracle builds configs 2 and 3 at full size in seconds (numpy FFT / dense per-axis
+Toeplitz), so variances are compared point by point on a seeded sample of the test points.
+Config 4 (n = 2e6, 64 nnz per point) takes the oracle minutes: it is checked through
+properties that hold at any size (k_eff, Ritz values of T >= sigma^2, 0 <= var <= prior,
+monotone decrease in k) plus a sampled comparison against oracle fixtures when present.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import CONFIGS, make_inputs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _build(p, inp, **kw):
+    from paper_1803_06058_b200 import LoveCache
+    return LoveCache.build(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2,
+                           kw.pop("k", p.k), precision=p.precision, **kw)
+
+
+def _prior(model, X):
+    ia, wa = O.interp(X, model.m, model.lo, model.h)
+    return O.prior_ski(model, ia, wa, ia, wa)
+
+
+@pytest.mark.parametrize("ci", [2, 3])
+def test_full_size_sampled_variances(ci):
+    p = CONFIGS[ci]
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    idx = np.sort(np.random.default_rng(123).choice(p.t, 20_000, replace=False))
+    Xs = inp.Xs[idx]
+    var, mean = c.predict_var(torch.from_numpy(inp.Xs).cuda(), return_mean=True)
+    var = var.cpu().numpy()[idx].astype(np.float64)
+    mean = mean.cpu().numpy()[idx].astype(np.float64)
+    model = O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+    oc = O.love_precompute(model, p.k)
+    assert c.info()["k_eff"] == oc.lanczos.k_eff == p.k
+    ov = O.predict_var(model, oc, Xs)
+    prior = _prior(model, Xs)
+    err = np.abs(var - ov)
+    bound = 1e-3 * np.abs(ov) + 1e-6 * prior
+    assert np.all(err <= bound), (np.max(err / bound), np.max(err / np.abs(ov)))
+    om = O.predict_mean(model, oc, Xs)
+    assert np.max(np.abs(mean - om)) < 2e-3 * np.abs(om).max()
+
+
+def test_cfg4_properties():
+    p = CONFIGS[4]
+    inp = make_inputs(p)
+    c100 = _build(p, inp)
+    info = c100.info()
+    assert info["k_eff"] == p.k and info["n_global"] == p.n
+    T = np.diag(info["alpha"]) + np.diag(info["beta"], 1) + np.diag(info["beta"], -1)
+    assert np.all(info["beta"] > 0)
+    # K_hat >= sigma^2 I, so every Ritz value is >= sigma^2 (up to fp32 round-off of ||K_hat||)
+    assert np.linalg.eigvalsh(T).min() >= p.sigma2 * (1 - 1e-3)
+    sel = np.random.default_rng(7).choice(p.t, 20_000, replace=False)
+    Xs = torch.from_numpy(inp.Xs[sel]).cuda()
+    v100 = c100.predict_var(Xs).cpu().numpy().astype(np.float64)
+    c100.free()
+    c50 = _build(p, inp, k=50)
+    v50 = c50.predict_var(Xs).cpu().numpy().astype(np.float64)
+    model = O.build_model(inp.X[:10], inp.y[:10], p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+    prior = _prior(model, inp.Xs[sel])
+    assert np.all(v100 >= -1e-6 * prior) and np.all(v100 <= prior * (1 + 1e-6))
+    # monotone non-increasing in k (Galerkin over nested Krylov spaces), up to fp32 round-off
+    assert np.all(v100 <= v50 + 1e-5 * prior)
+    c50.free()
+
+
+def test_cfg4_full_size_vs_oracle_fixture():
+    """Sampled full-size parity against tests/golden/cfg4_oracle_sample.npz, written by the
+    committed script tests/golden/make_oracle_fixtures.py (oracle only, ~80 s on CPU)."""
+    p = CONFIGS[4]
+    fx = os.path.join(os.path.dirname(__file__), "golden", "cfg4_oracle_sample.npz")
+    d = np.load(fx)
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    assert c.info()["k_eff"] == int(d["k_eff"])
+    vg, mg = c.predict_var(torch.from_numpy(d["Xs"]).cuda(), return_mean=True)
+    vg = vg.cpu().numpy().astype(np.float64)
+    err = np.abs(vg - d["var"])
+    bound = 1e-3 * np.abs(d["var"]) + 1e-6 * d["prior"]
+    assert np.all(err <= bound), (np.max(err / bound), np.max(err / np.abs(d["var"])))
+    mg = mg.cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(mg - d["mean"])) < 2e-3 * np.abs(d["mean"]).max()

@@ -119,16 +119,17 @@ def test_cfg1_fp64_end_to_end():
     np.testing.assert_allclose(mean.cpu().numpy(), om, atol=1e-9 * np.abs(om).max())
 
 
+@pytest.mark.parametrize("mode", ["two_pass", "one_read"])
 @pytest.mark.parametrize("ci,n,m,k,t", [
     (2, 60_001, (6000,), 40, 3001),          # 1-D four-step FFT, ragged n and t
     (3, 30_007, (48, 48), 40, 2003),         # 2-D Kronecker
     (4, 60_013, (24, 24, 24), 40, 2005),     # 3-D Kronecker
     (5, 20_011, (2000,), 30, 1999),          # config-5 data, shorter grid
 ])
-def test_scaled_fp32_variances_and_covariances(ci, n, m, k, t):
+def test_scaled_fp32_variances_and_covariances(ci, n, m, k, t, mode):
     p = scaled_config(ci, n=n, m=m, k=k, t=t)
     inp = make_inputs(p)
-    c = _build(p, inp)
+    c = _build(p, inp, lanczos_mode=mode)
     var, mean = c.predict_var(inp.Xs, return_mean=True)
     model = _model(p, inp)
     oc = O.love_precompute(model, p.k)
