@@ -124,6 +124,7 @@ struct Cache {
     void* S = nullptr;                   // V[m * ks_pad] row-major sampling root
     double b_norm = 0;
     std::vector<double> h_alpha, h_beta;
+    std::vector<double> h_evals;         // eigenvalues of T' (sampling cache)
 
     std::vector<void*> allocs;           // everything to release
 };
