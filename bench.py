@@ -16,7 +16,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -65,57 +64,60 @@ def reorth_bytes(n_local: int, k: int, vsize: int, passes: int = 1) -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle-reason sampling DURING the timed region (the recipe's clocks
+    line).  NVML is polled from a thread every ~2 ms (nvidia-smi -lms cannot resolve a
+    timed region of tens of ms); `nvidia-smi` is the fallback when NVML is unavailable."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.002):
         self.idx = gpu_index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.sm, self.reasons, self.smax = [], set(), None
+        self.stop_ev = threading.Event()
         self.thread = None
+        self.err = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.smax = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        except Exception as e:                       # no NVML: no clocks record
+            self.err = f"nvml unavailable: {e}"
             return
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.N, self.h = N, h
+        self.thread = threading.Thread(target=self._run, daemon=True)
         self.thread.start()
+        t0 = time.time()
+        while not self.sm and time.time() - t0 < 2.0:   # first sample before the region starts
+            time.sleep(0.001)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        N, h = self.N, self.h
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                mask = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for nm, attr in self.REASONS:
+                    if mask & getattr(N, attr, 0):
+                        self.reasons.add(nm)
+            except Exception as e:
+                self.err = str(e)
+                break
+            time.sleep(self.period)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
+        if self.thread is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "no samples"], "samples": 0}
+        self.stop_ev.set()
         self.thread.join(timeout=2)
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                smax = float(parts[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.smax,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms polling"}
 
 
 # ----------------------------------------------------------------------------- oracle arm
@@ -198,6 +200,7 @@ def main():
     import torch.distributed as dist
     from paper_1803_06058_b200 import LoveCache, launch_count, nccl_unique_id
     from paper_1803_06058_b200 import _abi
+    from paper_1803_06058_b200 import dist as D
     from synth import make_inputs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -210,9 +213,7 @@ def main():
     nccl_id = None
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        obj = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id = D.nccl_id_for_group(make_id=nccl_unique_id)
 
     inp = make_inputs(p, seed=p.seed + rank)           # this rank's shard (weak scaling)
     X = torch.from_numpy(inp.X).to(dev)
@@ -265,10 +266,7 @@ def main():
     barrier()
     launches = launch_count() - launches0
     clk = clocks.stop()
-    t_step = torch.tensor([total_ms / args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t_step, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t_step.item())
+    ms_per_step = D.max_over_ranks(total_ms / args.steps, dev)
     value = world * p.t / (ms_per_step / 1e3)
 
     # ---------------- phase timing: the same steps with CUDA events around every phase's
@@ -340,12 +338,10 @@ def main():
             b.record(stream)
             b.synchronize()
             tot += a.elapsed_time(b)
-        te = torch.tensor([tot / args.steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * p.t / (float(te.item()) / 1e3), "unit": "variances/s",
+        te = D.max_over_ranks(tot / args.steps, dev)
+        e2e = {"value": world * p.t / (te / 1e3), "unit": "variances/s",
                "h2d_bytes_per_step": int(inp.X.nbytes + inp.y.nbytes + inp.Xs.nbytes),
-               "d2h_bytes_per_step": int(p.t * vs), "ms_per_step": float(te.item())}
+               "d2h_bytes_per_step": int(p.t * vs), "ms_per_step": te}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -74,7 +74,8 @@ typedef struct {
 
 typedef struct {
     int32_t precision;      /* LOVE_FP32 (V = float, reductions in fp64) | LOVE_FP64 (V = double) */
-    int32_t probe;          /* LOVE_PROBE_Y (default: b = y, reading A1) | LOVE_PROBE_AVGCOL (reserved) */
+    int32_t probe;          /* LOVE_PROBE_Y (default: b = y, reading A1) | LOVE_PROBE_AVGCOL (b = (1/m) W_X^T K_UU 1, P:286;
+                               mean cache by Eq. 4) */
     int32_t prior;          /* LOVE_PRIOR_SKI (w*^T K_UU w*, default) | LOVE_PRIOR_EXACT (k(x*,x*)) */
     int32_t reorth_passes;  /* classical Gram-Schmidt passes of the full reorthogonalisation:
                                0 => 1 (fp32) / 2 (fp64, CGS2) */
@@ -89,7 +90,10 @@ enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ =
 /* Data-parallel sharding of the training points.  Every rank calls
  * love_build_cache with its own X/y shard and identical grid/kernel/sigma^2/k/opts; the
  * returned caches are identical replicas.  nccl_unique_id: 128 bytes (HOST memory) from
- * love_nccl_unique_id on rank 0, broadcast by the caller.  NULL love_dist => one GPU. */
+ * love_nccl_unique_id on rank 0, broadcast by the caller.  NULL love_dist => one GPU, no
+ * collectives.  world == 1 with an id runs the sharded code path with a one-rank
+ * communicator (every all-reduce an identity).  Errors: LOVE_ERR_ARG (rank/world/id
+ * inconsistent), LOVE_ERR_NCCL (NCCL missing or failing). */
 typedef struct {
     int32_t rank;
     int32_t world;

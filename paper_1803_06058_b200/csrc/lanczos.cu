@@ -318,7 +318,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_SCATTER, s);
         launch_scatter<V>(c, Q, ref, u, s);
     }
-    if (c.world > 1) {
+    if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, u, pl.m, true, s);
     }
@@ -331,7 +331,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_GATHER, s);
         launch_gather<V>(c, zj, Q, ref, r, st.alpha_acc, s);
     }
-    if (c.world > 1) {
+    if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.alpha_acc + j_host, 1, true, s);
     }
@@ -340,7 +340,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
             LOVE_LAUNCH(reorth_dots_kernel<V>, pl.gr, 256, pl.smd, s, Q, pl.ldq, pl.tile_rows, pl.k, pass, r, st);
         }
-        if (c.world > 1 && j_host < pl.k - 1) {
+        if (c.comm != nullptr && j_host < pl.k - 1) {
             ProfScope ps(LOVE_PROF_COMM, s);
             allreduce_sum(c, st.c_acc + ((int64_t)pass * pl.k + j_host) * (pl.k + 1), j_host + 1, true, s);
         }
@@ -350,7 +350,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
                         pass == pl.P - 1 ? 1 : 0, r, st);
         }
     }
-    if (c.world > 1 && j_host < pl.k - 1) {
+    if (c.comm != nullptr && j_host < pl.k - 1) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.beta2_acc + j_host, 1, true, s);
     }
@@ -380,11 +380,11 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         LOVE_LAUNCH(norm2_kernel<V>, (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.n, 256), 148 * 4)),
                     256, 0, s, (const V*)c.Q, c.n, st.bnorm2);
     }
-    if (c.world > 1) {
+    if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.bnorm2, 1, true, s);
     }
-    const bool graph = c.world == 1 && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    const bool graph = c.comm == nullptr && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
     if (graph) {
         // one step as a CUDA graph, replayed k times (z buffer parity alternates: capture
         // two steps so both parities are covered and replay the pair)
@@ -415,11 +415,93 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     }
 }
 
+__global__ void fill_kernel(double* __restrict__ u, int m, double v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) u[i] = v;
+}
+
+// d[i] += sum_p Q~[p, i] y[p] over this CTA's row tile, i < ncols (fp64 accumulation)
+template <typename V>
+__global__ void __launch_bounds__(256) qty_kernel(const V* __restrict__ Q, int64_t ldq, int64_t n, int ncols,
+                                                  const V* __restrict__ y, int64_t tile_rows,
+                                                  double* __restrict__ d) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * tile_rows;
+    const int64_t r1 = min(n, r0 + tile_rows);
+    for (int i = wid; i < ncols; i += nw) {
+        const V* __restrict__ q = Q + (int64_t)i * ldq;
+        double acc = 0.0;
+        for (int64_t p = r0 + lane; p < r1; p += 32) acc += (double)q[p] * (double)y[p];
+        acc = warp_sum(acc);
+        if (lane == 0) atomicAdd(&d[i], acc);
+    }
+}
+
+// g = L^{-1} (S d), S = diag(qscale): forward substitution with the bidiagonal factor of T
+// (P:295-298), one thread
+__global__ void eq4_solve_kernel(LanczosState st, int k_eff, double* __restrict__ d) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double prev = 0.0;
+    for (int i = 0; i < k_eff; ++i) {
+        const double rhs = d[i] * st.qscale[i] - (i > 0 ? st.Ls[i - 1] * prev : 0.0);
+        prev = rhs / st.Ld[i];
+        d[i] = prev;
+    }
+}
+
+// a[p] = sum_i Rc[p, i] g[i]   (Rc column-major fp64, m x k_eff)
+__global__ void rc_gemv_kernel(const double* __restrict__ Rc, int m, int k_eff, const double* __restrict__ g,
+                               double* __restrict__ a) {
+    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < k_eff; ++i) acc += Rc[(int64_t)i * m + p] * g[i];
+        a[p] = acc;
+    }
+}
+
+template <typename V>
+void avgcol_impl(Cache& c, cudaStream_t s) {
+    const int m = c.g.m_total;
+    double* u = (double*)c.u;
+    double* z = (double*)c.z[1];
+    double* zero = (double*)dalloc(c, sizeof(double), s);
+    LOVE_LAUNCH(fill_kernel, (int)std::min<int64_t>(ceil_div(m, 256), 148 * 8), 256, 0, s, u, m, 1.0 / m);
+    launch_kuu(c, u, z, s);
+    // r = W^T z + sigma^2 * 0 * r : the gather with a zero scale on its q term
+    const StepRef ref{nullptr, 0, zero, nullptr};
+    launch_gather<V>(c, z, (const V*)c.r, ref, (V*)c.Q, nullptr, s);
+}
+
+template <typename V>
+void eq4_impl(Cache& c, cudaStream_t s) {
+    const int m = c.g.m_total, ke = c.k_eff;
+    double* d = (double*)dalloc(c, sizeof(double) * std::max(ke, 1), s);
+    const int64_t tile = std::max<int64_t>(1024, round_up(ceil_div(c.n, 148 * 4), 32));
+    if (c.n > 0)
+        LOVE_LAUNCH(qty_kernel<V>, (int)ceil_div(c.n, tile), 256, 0, s, (const V*)c.Q, c.ldq, c.n, ke,
+                    (const V*)c.ysort, tile, d);
+    if (c.comm != nullptr) allreduce_sum(c, d, ke, true, s);
+    LOVE_LAUNCH(eq4_solve_kernel, 1, 32, 0, s, c.st, ke, d);
+    LOVE_LAUNCH(rc_gemv_kernel, (int)std::min<int64_t>(ceil_div(m, 256), 148 * 8), 256, 0, s,
+                (const double*)c.Rc_col, m, ke, d, (double*)c.a);
+}
+
 }  // namespace
 
 void run_lanczos(Cache& c, cudaStream_t s) {
     if (c.precision == LOVE_FP64) lanczos_impl<double>(c, s);
     else lanczos_impl<float>(c, s);
+}
+
+void avgcol_probe(Cache& c, cudaStream_t s) {
+    ProfScope ps(LOVE_PROF_SETUP, s);
+    if (c.precision == LOVE_FP64) avgcol_impl<double>(c, s);
+    else avgcol_impl<float>(c, s);
+}
+
+void mean_cache_eq4(Cache& c, cudaStream_t s) {
+    ProfScope ps(LOVE_PROF_FINISH, s);
+    if (c.precision == LOVE_FP64) eq4_impl<double>(c, s);
+    else eq4_impl<float>(c, s);
 }
 
 void finish_cache(Cache& c, cudaStream_t s) {

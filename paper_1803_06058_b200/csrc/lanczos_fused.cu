@@ -650,7 +650,7 @@ void enqueue_fused_step(Cache& c, int j_host, double* wbuf, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_FUSED_PASS, s);
         launch_fused_pass(c, s);
     }
-    if (c.world > 1) {
+    if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, c.st.AB + (int64_t)j_host * 2 * (k + 1), 2 * (k + 1), true, s);
     }
@@ -660,7 +660,7 @@ void enqueue_fused_step(Cache& c, int j_host, double* wbuf, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_SCATTER, s);
-        if (c.world > 1) {
+        if (c.comm != nullptr) {
             launch_mside(c, 1, wbuf, s);
             {
                 ProfScope pc(LOVE_PROF_COMM, s);
@@ -745,12 +745,12 @@ void run_lanczos_fused(Cache& c, cudaStream_t s) {
     const int k = c.k_req;
     const int m = c.g.m_total;
     double* wbuf = nullptr;
-    if (c.world > 1) cuda_check(cudaMallocAsync((void**)&wbuf, sizeof(double) * 2 * (size_t)m, s), "wbuf alloc");
+    if (c.comm != nullptr) cuda_check(cudaMallocAsync((void**)&wbuf, sizeof(double) * 2 * (size_t)m, s), "wbuf alloc");
     {   // u~_0 = W Q~_0 (the probe b) and z~_0 = K_UU u~_0
         ProfScope ps(LOVE_PROF_SCATTER, s);
         const StepRef ref{nullptr, 0, c.one, nullptr};
         launch_scatter<float>(c, (const float*)c.Q, ref, (double*)c.u, s);
-        if (c.world > 1) {
+        if (c.comm != nullptr) {
             ProfScope pc(LOVE_PROF_COMM, s);
             allreduce_sum(c, c.u, m, true, s);
         }
@@ -761,7 +761,7 @@ void run_lanczos_fused(Cache& c, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_KUU, s);
         launch_kuu(c, (const double*)c.u, (double*)c.z[0], s);
     }
-    const bool graph = c.world == 1 && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    const bool graph = c.comm == nullptr && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
     if (graph) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;

@@ -175,7 +175,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         o.precision = LOVE_FP32;
         if (opts) o = *opts;
         if (o.precision != LOVE_FP32 && o.precision != LOVE_FP64) throw LoveError{LOVE_ERR_ARG, "bad precision"};
-        if (o.probe != LOVE_PROBE_Y) throw LoveError{LOVE_ERR_ARG, "only LOVE_PROBE_Y is implemented"};
+        if (o.probe != LOVE_PROBE_Y && o.probe != LOVE_PROBE_AVGCOL) throw LoveError{LOVE_ERR_ARG, "bad probe"};
         if (o.prior != LOVE_PRIOR_SKI && o.prior != LOVE_PRIOR_EXACT) throw LoveError{LOVE_ERR_ARG, "bad prior"};
         if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
 
@@ -213,8 +213,10 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
         c->k_sample_req = o.k_sample;
         c->n = n_local;
-        if (dist && dist->world > 1) {
-            if (dist->rank < 0 || dist->rank >= dist->world || !dist->nccl_unique_id)
+        // a communicator is set up whenever a NCCL id is given (world == 1 runs every
+        // collective of the sharded path as an identity; used by the single-GPU tests)
+        if (dist && (dist->world > 1 || dist->nccl_unique_id)) {
+            if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world || !dist->nccl_unique_id)
                 throw LoveError{LOVE_ERR_ARG, "bad love_dist"};
             c->world = dist->world;
             c->rank = dist->rank;
@@ -253,7 +255,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             int hflag = 0;
             cuda_check(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
             cuda_check(cudaStreamSynchronize(s), "sync");
-            if (c->world > 1) {
+            if (c->comm != nullptr) {
                 float* df = (float*)tmp.get(sizeof(float));
                 fl = (float)hflag;
                 cuda_check(cudaMemcpyAsync(df, &fl, sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
@@ -264,7 +266,10 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             }
             if (hflag) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
         }
-        launch_counting_sort(*c, cell, frac64, y, c->n, c->Q, s);
+        // probe y: the sorted targets are the first Lanczos column; probe avg: they are kept
+        // for the mean cache (Eq. 4) and column 0 is filled below
+        if (c->probe == LOVE_PROBE_AVGCOL) c->ysort = dalloc(*c, vs * c->ldq, s);
+        launch_counting_sort(*c, cell, frac64, y, c->n, c->probe == LOVE_PROBE_Y ? c->Q : c->ysort, s);
         c->n_items = count_items_host(*c, s);
         c->item_cell = (int*)dalloc(*c, sizeof(int) * (c->n_items + 8), s);     // padded: staged in 16 B units
         c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
@@ -306,6 +311,9 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
         }
 
+        // ---- probe b = (1/m) W_X^T K_UU 1 (average column of K_XU K_UU..., Alg. 1)
+        if (c->probe == LOVE_PROBE_AVGCOL) avgcol_probe(*c, s);
+
         // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
         if (c->fused) setup_fused(*c, s);
         if (c->fused) run_lanczos_fused(*c, s);
@@ -327,6 +335,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         if (c->k_eff > 1)
             cuda_check(cudaMemcpy(c->h_beta.data(), c->st.beta, sizeof(double) * (c->k_eff - 1),
                                   cudaMemcpyDeviceToHost), "beta d2h");
+        if (c->probe == LOVE_PROBE_AVGCOL) mean_cache_eq4(*c, s);   // a = R^T T^{-1} Q^T y
         finish_cache(*c, s);
         if (c->k_sample_req > 0) build_sampling_cache(*c, s);
         cuda_check(cudaStreamSynchronize(s), "build sync");

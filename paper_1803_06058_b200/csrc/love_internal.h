@@ -113,6 +113,7 @@ struct Cache {
     float* U32 = nullptr;                // [k+1][m] every u~_i in fp32 (reorth correction)
     void* Rc = nullptr;                  // V[m * k_pad] row-major
     void* a = nullptr;                   // double[m] mean cache
+    void* ysort = nullptr;               // V[ldq] targets in sorted order (probe avg only)
     double* one = nullptr;               // device 1.0 (scale of un-normalised MVMs)
     double* scal = nullptr;              // backing store of LanczosState
     LanczosState st;
@@ -169,6 +170,8 @@ void run_lanczos(Cache& c, cudaStream_t s);
 void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu
 void setup_fused(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
+void avgcol_probe(Cache& c, cudaStream_t s);    // Q~[:, 0] = (1/m) W^T K_UU 1   (probe avg)
+void mean_cache_eq4(Cache& c, cudaStream_t s);  // a = Rc L^{-1} Q^T y after the Lanczos loop
 // query.cu
 template <typename V> void launch_predict(const Cache& c, const double* Xa, const double* Xb,
                                           int64_t t, V* out, V* mean_out, cudaStream_t s);

@@ -103,14 +103,14 @@ void nccl_comm_destroy(Cache& c) {
 }
 
 void allreduce_sum(const Cache& c, void* buf, int64_t count, bool is_double, cudaStream_t s) {
-    if (c.world <= 1 || count <= 0) return;
+    if (c.comm == nullptr || count <= 0) return;
     nccl_check(api().AllReduce(buf, buf, (size_t)count, is_double ? kNcclFloat64 : kNcclFloat32, kNcclSum,
                                (NcclComm)c.comm, s),
                "ncclAllReduce");
 }
 
 void allreduce_sum_i64(const Cache& c, int64_t* buf, int64_t count, cudaStream_t s) {
-    if (c.world <= 1 || count <= 0) return;
+    if (c.comm == nullptr || count <= 0) return;
     nccl_check(api().AllReduce(buf, buf, (size_t)count, kNcclInt64, kNcclSum, (NcclComm)c.comm, s),
                "ncclAllReduce");
 }

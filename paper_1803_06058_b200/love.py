@@ -75,7 +75,7 @@ class LoveCache:
     @classmethod
     def build(cls, X, y, m: Sequence[int], lo: Sequence[float], h: Sequence[float],
               lengthscale: Sequence[float], outputscale: float, sigma2: float, k: int,
-              precision: str = "fp32", prior: str = "ski", k_sample: int = 0,
+              precision: str = "fp32", prior: str = "ski", k_sample: int = 0, probe: str = "y",
               reorth_passes: int = 0, breakdown_tol: float = 0.0, lanczos_mode: str = "auto",
               rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
               stream=None) -> "LoveCache":
@@ -92,7 +92,7 @@ class LoveCache:
             r.lengthscale[i] = float(lengthscale[i])
         o = _abi.love_opts()
         o.precision = _abi.LOVE_FP64 if precision == "fp64" else _abi.LOVE_FP32
-        o.probe = _abi.LOVE_PROBE_Y
+        o.probe = {"y": _abi.LOVE_PROBE_Y, "avg": _abi.LOVE_PROBE_AVGCOL}[probe]
         o.prior = _abi.LOVE_PRIOR_EXACT if prior == "exact" else _abi.LOVE_PRIOR_SKI
         o.reorth_passes = int(reorth_passes)
         o.breakdown_tol = float(breakdown_tol)
@@ -100,7 +100,7 @@ class LoveCache:
         o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2}[lanczos_mode]
         dist = None
         idbuf = None
-        if world > 1:
+        if world > 1 or nccl_id is not None:
             idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
             dist = _abi.love_dist(rank, world, ctypes.cast(idbuf, ctypes.c_void_p))
         out = ctypes.c_void_p()

@@ -1,0 +1,24 @@
+"""World-size-2 gloo tests of the N > 1 path on CPU: the host-side plumbing
+(shard bounds, NCCL-id broadcast, max over ranks) and the per-step exchange schedule of the
+sharded Lanczos loop, which must reproduce the unsharded oracle."""
+import socket
+
+import pytest
+import torch.multiprocessing as mp
+
+import _dist_workers as W
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_host_plumbing_world2():
+    mp.spawn(W.host_plumbing, args=(2, _port()), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("kind,passes", [("cfg1", 2), ("1d_n200", 1), ("2d", 2), ("3d", 2)])
+def test_sharded_lanczos_matches_oracle_world2(kind, passes):
+    mp.spawn(W.sharded_lanczos, args=(2, _port(), kind, passes), nprocs=2, join=True)

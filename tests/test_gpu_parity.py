@@ -119,6 +119,41 @@ def test_cfg1_fp64_end_to_end():
     np.testing.assert_allclose(mean.cpu().numpy(), om, atol=1e-9 * np.abs(om).max())
 
 
+@pytest.mark.parametrize("prec", ["fp64"])
+def test_cfg1_probe_avgcol(prec):
+    """Reading A1: the paper's own probe b = (1/m) W_X^T K_UU 1 (Alg. 1); the
+    mean cache then follows Eq. 4, a = R^T T^{-1} Q^T y."""
+    p = scaled_config(1, precision=prec)
+    inp = make_inputs(p)
+    c = _build(p, inp, probe="avg")
+    var, mean = c.predict_var(inp.Xs, return_mean=True)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k, probe="avg")
+    info = c.info()
+    assert info["k_eff"] == oc.lanczos.k_eff
+    np.testing.assert_allclose(info["b_norm"], oc.lanczos.b_norm, rtol=1e-12 if prec == "fp64" else 1e-6)
+    ov = O.predict_var(model, oc, inp.Xs)
+    _assert_var(var.cpu().numpy().astype(np.float64), ov, _prior(model, inp.Xs), fp64=prec == "fp64")
+    om = O.predict_mean(model, oc, inp.Xs)
+    tol = 1e-9 if prec == "fp64" else 1e-3
+    assert np.max(np.abs(mean.cpu().numpy() - om)) <= tol * np.abs(om).max()
+
+
+@pytest.mark.parametrize("mode", ["two_pass", "one_read"])
+def test_scaled_cfg2_probe_avgcol(mode):
+    p = scaled_config(2, n=60_001, m=(6000,), k=40, t=3001)
+    inp = make_inputs(p)
+    c = _build(p, inp, probe="avg", lanczos_mode=mode)
+    var, mean = c.predict_var(inp.Xs, return_mean=True)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k, probe="avg")
+    assert c.info()["k_eff"] == oc.lanczos.k_eff
+    ov = O.predict_var(model, oc, inp.Xs)
+    _assert_var(var.cpu().numpy().astype(np.float64), ov, _prior(model, inp.Xs), fp64=False)
+    om = O.predict_mean(model, oc, inp.Xs)
+    assert np.max(np.abs(mean.cpu().numpy() - om)) < 1e-3 * np.abs(om).max()
+
+
 @pytest.mark.parametrize("mode", ["two_pass", "one_read"])
 @pytest.mark.parametrize("ci,n,m,k,t", [
     (2, 60_001, (6000,), 40, 3001),          # 1-D four-step FFT, ragged n and t
@@ -221,3 +256,21 @@ def test_prior_exact_mode():
     oc = O.love_precompute(model, p.k)
     ov = O.predict_var(model, oc, inp.Xs, prior="exact")
     _assert_var(var, ov, np.full(len(ov), p.outputscale), fp64=True)
+
+
+@pytest.mark.parametrize("ci,n,m,k", [(2, 50_003, (5000,), 30), (4, 40_009, (24, 24, 24), 25)])
+def test_sharded_code_path_one_rank_nccl(ci, n, m, k):
+    """The multi-GPU code path (every all-reduce issued through NCCL, eager step launches)
+    with a one-rank communicator must give the single-GPU result: the collectives are
+    identities, so any addressing or ordering bug in the sharded path shows up here."""
+    from paper_1803_06058_b200 import nccl_unique_id
+    p = scaled_config(ci, n=n, m=m, k=k, t=2001)
+    inp = make_inputs(p)
+    c1 = _build(p, inp)
+    cN = _build(p, inp, rank=0, world=1, nccl_id=nccl_unique_id())
+    v1, m1 = c1.predict_var(inp.Xs, return_mean=True)
+    vN, mN = cN.predict_var(inp.Xs, return_mean=True)
+    assert cN.info()["k_eff"] == c1.info()["k_eff"]
+    np.testing.assert_allclose(cN.info()["alpha"], c1.info()["alpha"], rtol=1e-6)
+    np.testing.assert_allclose(vN.cpu().numpy(), v1.cpu().numpy(), rtol=1e-4, atol=1e-7)
+    np.testing.assert_allclose(mN.cpu().numpy(), m1.cpu().numpy(), rtol=1e-4, atol=1e-6)
