@@ -79,10 +79,12 @@ _lib = None
 
 
 def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load liblove.so (in-tree).  Raises if it has not been built: there is no fallback."""
+    """Load liblove.so (in-tree; LOVE_LIB overrides the path for A/B builds of the same
+    sources).  Raises if it has not been built: there is no fallback."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("LOVE_LIB", path)
     if not os.path.exists(path):
         raise RuntimeError(f"{path} is missing: run `make -C paper_1803_06058_b200` "
                            "(or __graft_entry__.build()); there is no CPU fallback")

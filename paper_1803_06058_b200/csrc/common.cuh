@@ -4,15 +4,50 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
 #include <string>
 
 namespace love {
 
 extern std::atomic<int64_t> g_launch_count;
 
+// Programmatic dependent launch (PDL).  Inside a PdlScope every LOVE_LAUNCH carries the
+// programmatic-stream-serialization attribute: the next kernel's CTAs may be scheduled while
+// the previous grid drains, and they block in pdl_wait() (griddepcontrol.wait: the previous
+// grid has completed and its writes are visible) before touching anything it produced.
+// Every kernel launched inside a PdlScope must therefore call pdl_wait() first.
+extern thread_local bool t_pdl;
+struct PdlScope {
+    bool prev;
+    explicit PdlScope(bool on) : prev(t_pdl) { t_pdl = on; }
+    ~PdlScope() { t_pdl = prev; }
+};
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                      Args&&... args) {
+    if (!t_pdl) {
+        kernel<<<grid, block, smem, stream>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 #define LOVE_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
     do {                                                                            \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                 \
+        ::love::launch_ex(kernel, dim3(grid), dim3(block), (size_t)(smem), (stream), __VA_ARGS__); \
         ::love::g_launch_count.fetch_add(1, std::memory_order_relaxed);              \
     } while (0)
 

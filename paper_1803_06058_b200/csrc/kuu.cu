@@ -139,6 +139,7 @@ __device__ __forceinline__ C twiddleN(int a, int N1, const C* __restrict__ twN2,
 __global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, const C* __restrict__ tw,
                                  const double* __restrict__ lam, double* __restrict__ z, C* __restrict__ outc,
                                  int mode) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N;
@@ -172,6 +173,7 @@ __global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, con
 template <int G>
 __global__ void fft_passA_kernel(const double* __restrict__ u, int m, int N1, int N2, const C* __restrict__ tw2,
                                  const C* __restrict__ twF, C* __restrict__ Y) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -203,6 +205,7 @@ template <int G>
 __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
                                  const C* __restrict__ tw2, const C* __restrict__ twF,
                                  const double* __restrict__ lamB, C* __restrict__ outc, int mode) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N1;
@@ -249,6 +252,7 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
 template <int G>
 __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
                                  double* __restrict__ z) {
+    pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -278,6 +282,7 @@ __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2,
 constexpr int kAxRows = 16, kAxInner = 32, kAxK = 32;
 __global__ void __launch_bounds__(128) axis_inner_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                          const double* __restrict__ c, int L, int I, double scale) {
+    pdl_wait();
     __shared__ double cs[1024];
     __shared__ double tile[kAxK][kAxInner + 1];
     const int i0 = blockIdx.x * kAxInner;
@@ -317,6 +322,7 @@ __global__ void __launch_bounds__(128) axis_inner_kernel(const double* __restric
 __global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                         const double* __restrict__ c, int64_t O, int L,
                                                         double scale) {
+    pdl_wait();
     __shared__ double cs[1024];
     __shared__ double lines[2 * 1024 + 256];
     const int64_t first = (int64_t)blockIdx.x * 256;           // first output of this CTA

@@ -17,6 +17,14 @@
 
 #include "love_internal.h"
 
+#ifndef LOVE_DOTS_U
+#define LOVE_DOTS_U 8
+#endif
+#ifndef LOVE_UPD_U
+#define LOVE_UPD_U 7
+#endif
+namespace love { constexpr int kUpdU = LOVE_UPD_U; }
+
 namespace love {
 
 namespace {
@@ -52,6 +60,7 @@ __device__ __forceinline__ void vstore(V* p, const V in[VecT<V>::W]) {
 __global__ void step_prologue_kernel(LanczosState st, int k, double tol, int m,
                                      const double* __restrict__ z0, const double* __restrict__ z1,
                                      double* __restrict__ Rc, double* __restrict__ a, int mean_y) {
+    pdl_wait();
     int* fl = st.flags;
     const int j = *st.jdev;
     const double* __restrict__ z = ((j - 1) & 1) ? z1 : z0;     // z_{j-1}
@@ -151,18 +160,18 @@ template <typename V>
 __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ Q, int64_t ldq,
                                                           int64_t tile_rows, int k, int pass,
                                                           const V* __restrict__ r, LanczosState st) {
+    pdl_wait();
     constexpr int W = VecT<V>::W;
-    constexpr int U = 8;
+    constexpr int U = LOVE_DOTS_U;
     extern __shared__ __align__(16) double smd[];
     const int j = *st.jdev;
     if (st.flags[0] || j >= k - 1) return;
     const int from_r = pass == 0;
-    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
     const int ncols = j + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int S = ncols < nw ? nw / ncols : 1;            // row splits per column
     double* csum = smd;                                   // [S][ncols]
-    V* src = reinterpret_cast<V*>(smd + round_up(max(k + 1, nw), 2));   // [tile_rows]
+    V* src = reinterpret_cast<V*>(smd + round_up((k + 1) * nw, 2));    // [tile_rows]
     const int64_t row0 = (int64_t)blockIdx.x * tile_rows;
     const int64_t rows = min(tile_rows, ldq - row0);
     if (rows <= 0) return;
@@ -205,6 +214,7 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
         if (lane == 0) csum[sp * ncols + col] = dp;
     }
     __syncthreads();
+    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
         double tot = 0.0;
         for (int sp = 0; sp < S; ++sp) tot += csum[sp * ncols + i];
@@ -217,6 +227,7 @@ template <typename V>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
                                                             int pass, int last_pass, const V* __restrict__ r,
                                                             LanczosState st) {
+    pdl_wait();
     constexpr int W = VecT<V>::W;
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
     __shared__ double red[32];
@@ -241,8 +252,11 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         V acc[W];
 #pragma unroll
         for (int e = 0; e < W; ++e) acc[e] = V(0);
-#pragma unroll 4
-        for (int i = 0; i < ncols; ++i) {
+        // columns are swept LAST to first: every CTA is resident at once, so the dots pass
+        // streamed Q~ column by column and its last columns are the ones still in L2; the
+        // next step's dots pass starts at column 0, the one this pass reads last.
+#pragma unroll kUpdU
+        for (int i = ncols - 1; i >= 0; --i) {
             V a[W];
             vload<V>(Q + (int64_t)i * ldq + p, a);
             const V ci = (V)cf[i];
@@ -288,6 +302,7 @@ int64_t reorth_tile_rows(int64_t ldq) {
 }
 
 __global__ void advance_step_kernel(int* jdev) {
+    pdl_wait();
     if (threadIdx.x == 0) jdev[0] += 1;
 }
 
@@ -370,7 +385,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.tile_rows = reorth_tile_rows<V>(c.ldq);
     pl.gr = (int)ceil_div(c.ldq, pl.tile_rows);
     pl.gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.ldq / VecT<V>::W, 256), 148 * 8));
-    pl.smd = sizeof(double) * round_up(std::max(pl.k + 1, 8), 2) + sizeof(V) * pl.tile_rows;
+    pl.smd = sizeof(double) * round_up((pl.k + 1) * 8, 2) + sizeof(V) * pl.tile_rows;
     pl.smu = sizeof(double) * (pl.k + 1);
     ensure_smem((const void*)reorth_dots_kernel<V>, pl.smd);
     ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
@@ -385,6 +400,9 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         allreduce_sum(c, st.bnorm2, 1, true, s);
     }
     const bool graph = c.comm == nullptr && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    // every kernel of a step starts with pdl_wait(): its launch can overlap the previous
+    // kernel's drain (programmatic dependent launch)
+    PdlScope pdl(std::getenv("LOVE_NO_PDL") == nullptr);
     if (graph) {
         // one step as a CUDA graph, replayed k times (z buffer parity alternates: capture
         // two steps so both parities are covered and replay the pair)

@@ -26,38 +26,13 @@
 
 #include "love_internal.h"
 #include "ski_device.cuh"
+#include "tma.cuh"
 
 namespace love {
 
 namespace {
 
 constexpr int kZMax = 1280;           // staged z~ nodes per tile (d <= 2)
-
-// ---- TMA 1-D bulk copies (cp.async.bulk) completing on an mbarrier
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(a), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-    const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                 ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
-}
 
 // 2-D tensor TMA: box {rows, 8 columns} of the column-major Q~ at coordinates (row, col)
 __device__ __forceinline__ void tma_q_box(void* dst, const CUtensorMap* map, int row, int col, uint64_t* bar) {

@@ -16,6 +16,7 @@
 namespace love {
 
 std::atomic<int64_t> g_launch_count{0};
+thread_local bool t_pdl = false;
 
 namespace {
 thread_local std::string t_err;
@@ -237,6 +238,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         const int M = g.m_total;
         const size_t vs = c->vsize;
         c->ldq = round_up(std::max<int64_t>(c->n, 1), 4);
+        if (const char* e = std::getenv("LOVE_LDQ_PAD")) c->ldq = round_up(c->ldq, 64) + std::atoll(e);
 
         // ---- interpolation records + cell sort
         int* cell = (int*)tmp.get(sizeof(int) * std::max<int64_t>(c->n, 1));

@@ -26,6 +26,7 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
                                                       const V* __restrict__ f0, const V* __restrict__ f1,
                                                       const V* __restrict__ f2, const V* __restrict__ qbase,
                                                       StepRef ref, double* __restrict__ M) {
+    pdl_wait();
     using A = typename AccT<V, D>::type;
     constexpr int S = Slots<D>::value;
     const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(256) nodepass_kernel(GridDev g, int64_t n_item
                                                        const int* __restrict__ cis,
                                                        const double* __restrict__ M, StepRef ref,
                                                        double* __restrict__ u) {
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= g.m_total || step_done(ref)) return;
     u[i] = node_pull<D>(g, n_items, cis, M, i) * ref.scale[step_j(ref)];
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                                                      const V* __restrict__ f2, const double* __restrict__ z,
                                                      const V* __restrict__ qbase, StepRef ref, double sigma2,
                                                      V* __restrict__ r, double* __restrict__ alpha_base) {
+    pdl_wait();
     using A = typename AccT<V, D>::type;
     constexpr int S = Slots<D>::value;
     __shared__ double red[32];
