@@ -135,10 +135,18 @@ __device__ __forceinline__ C twiddleN(int a, int N1, const C* __restrict__ twN2,
     return SIGN > 0 ? cconj(w) : w;
 }
 
+// u[idx] for idx < m: read directly, or summed from the per-cell scatter moments
+// Mc[l][c + 2] (d = 1, rows of length m + 4): u[i] = Mc[0][i+3] + Mc[1][i+2] + Mc[2][i+1] + Mc[3][i]
+__device__ __forceinline__ double u_at(const double* __restrict__ u, const double* __restrict__ Mc, int m, int idx) {
+    if (Mc == nullptr) return u[idx];
+    const int ld = m + 4;
+    return Mc[idx + 3] + Mc[ld + idx + 2] + Mc[2 * ld + idx + 1] + Mc[3 * ld + idx];
+}
+
 // ---- single-CTA convolution (mode 0) / forward transform (mode 1), N <= 4096
-__global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, const C* __restrict__ tw,
-                                 const double* __restrict__ lam, double* __restrict__ z, C* __restrict__ outc,
-                                 int mode) {
+__global__ void fft_small_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N,
+                                 const C* __restrict__ tw, const double* __restrict__ lam, double* __restrict__ z,
+                                 C* __restrict__ outc, int mode) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -147,7 +155,7 @@ __global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, con
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int i = threadIdx.x + e * blockDim.x;
-        buf[pad(i)] = make_double2(i < m ? u[i] : 0.0, 0.0);
+        buf[pad(i)] = make_double2(i < m ? u_at(u, Mc, m, i) : 0.0, 0.0);
     }
     __syncthreads();
     line_fft<-1>(buf, N, tws);
@@ -171,8 +179,8 @@ __global__ void fft_small_kernel(const double* __restrict__ u, int m, int N, con
 
 // ---- four-step pass A: for each n1, FFT over n2 of x[n1 + N1 n2], times w_N^{n1 k2}
 template <int G>
-__global__ void fft_passA_kernel(const double* __restrict__ u, int m, int N1, int N2, const C* __restrict__ tw2,
-                                 const C* __restrict__ twF, C* __restrict__ Y) {
+__global__ void fft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
+                                 const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y) {
     pdl_wait();
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -185,7 +193,7 @@ __global__ void fft_passA_kernel(const double* __restrict__ u, int m, int N1, in
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n2 = t / G;
         const int idx = n1_0 + g + N1 * n2;
-        buf[pad(g * N2 + n2)] = make_double2(idx < m ? u[idx] : 0.0, 0.0);
+        buf[pad(g * N2 + n2)] = make_double2(idx < m ? u_at(u, Mc, m, idx) : 0.0, 0.0);
     }
     __syncthreads();
     line_fft<-1>(buf, N2, tws);
@@ -405,7 +413,8 @@ constexpr int kSmallFFT = 4096;
 constexpr int kLinesPerCta = 2;
 
 // convolution (mode 0) of u (m entries) or forward FFT (mode 1) of u (N entries)
-void fft_run(const Cache& c, const double* u, int m, double* z, C* work, C* outc, int mode, cudaStream_t s) {
+void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc, int mode,
+             cudaStream_t s) {
     const int N = c.fft_N, N1 = c.fft_N1, N2 = c.fft_N2;
     const C* tw1 = (const C*)c.tw1;
     const C* tw2 = (const C*)c.tw2;
@@ -414,7 +423,7 @@ void fft_run(const Cache& c, const double* u, int m, double* z, C* work, C* outc
     if (N1 == 0) {
         const size_t sm = sizeof(C) * (padded(N) + N);
         ensure_smem((const void*)fft_small_kernel, sm);
-        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, m, N, tw1, lam, z, outc, mode);
+        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, Mc, m, N, tw1, lam, z, outc, mode);
         return;
     }
     constexpr int G = kLinesPerCta;
@@ -422,7 +431,7 @@ void fft_run(const Cache& c, const double* u, int m, double* z, C* work, C* outc
     ensure_smem((const void*)fft_passA_kernel<G>, smA);
     ensure_smem((const void*)fft_passB_kernel<G>, smB);
     ensure_smem((const void*)fft_passC_kernel<G>, smA);
-    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, m, N1, N2, tw2, twF, work);
+    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work);
     LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode);
     if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z);
 }
@@ -500,16 +509,16 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     cuda_check(cudaMallocAsync((void**)&col, sizeof(double) * N, s), "lam alloc");
     cuda_check(cudaMallocAsync((void**)&X, sizeof(C) * N, s), "lam alloc");
     LOVE_LAUNCH(embed_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, c.cols64, m, N, col);
-    fft_run(c, col, N, nullptr, (C*)c.fft_buf, X, 1, s);
+    fft_run(c, col, nullptr, N, nullptr, (C*)c.fft_buf, X, 1, s);
     LOVE_LAUNCH(lambda_store_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N, c.fft_N1,
                 c.fft_N2, c.fft_N1 != 0, c.rbf.outputscale / (double)N, (double*)c.lam);
     cuda_check(cudaFreeAsync(col, s), "lam free");
     cuda_check(cudaFreeAsync(X, s), "lam free");
 }
 
-void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s) {
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc) {
     if (c.g.d > 1) kuu_axes(c, u, z, s);
-    else fft_run(c, u, c.g.m[0], z, (C*)c.fft_buf, nullptr, 0, s);
+    else fft_run(c, u, Mc, c.g.m[0], z, (C*)c.fft_buf, nullptr, 0, s);
 }
 
 }  // namespace love

@@ -222,6 +222,21 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
     }
 }
 
+// Last-CTA-done step advance: every CTA of the grid calls this once at its end (uniformly
+// per CTA); the last one to arrive resets the counter and writes j + 1 to the step index.
+__device__ __forceinline__ void advance_step(const LanczosState& st, int j) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(st.step_ctr), 1u);
+        if (prev == gridDim.x - 1) {
+            st.step_ctr[0] = 0;
+            st.jdev[0] = j + 1;
+            __threadfence();
+        }
+    }
+}
+
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
 template <typename V>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
@@ -232,7 +247,12 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
     __shared__ double red[32];
     const int j = *st.jdev;
-    if (st.flags[0] || j >= k - 1) return;
+    // the last pass's update is the last kernel of step j: its last CTA to finish advances
+    // the device step index (every CTA has read j by then), also on the early-exit path
+    if (st.flags[0] || j >= k - 1) {
+        if (last_pass) advance_step(st, j);
+        return;
+    }
     const int from_r = pass == 0;
     const double* __restrict__ c_in = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
     double* __restrict__ beta2_out = last_pass ? st.beta2_acc + j : nullptr;
@@ -274,6 +294,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     if (beta2_out != nullptr) {
         b2 = block_sum(b2, red);
         if (threadIdx.x == 0) atomicAdd(beta2_out, b2);
+        advance_step(st, j);
     }
 }
 
@@ -301,15 +322,13 @@ int64_t reorth_tile_rows(int64_t ldq) {
     return std::max<int64_t>(quantum, round_up(ceil_div(ldq, 148 * 4), quantum));
 }
 
-__global__ void advance_step_kernel(int* jdev) {
-    pdl_wait();
-    if (threadIdx.x == 0) jdev[0] += 1;
-}
+
 
 template <typename V>
 struct StepPlan {
     Cache* c;
     int k, m, P, mean_y, gm, gr, gu;
+    bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
     int64_t ldq, tile_rows;
     size_t smd, smu;
 };
@@ -331,7 +350,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_SCATTER, s);
-        launch_scatter<V>(c, Q, ref, u, s);
+        launch_scatter<V>(c, Q, ref, u, s, pl.mfuse);
     }
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
@@ -340,7 +359,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     double* zj = (double*)c.z[j_host & 1];
     {
         ProfScope ps(LOVE_PROF_KUU, s);
-        launch_kuu(c, u, zj, s);
+        launch_kuu(c, u, zj, s, pl.mfuse ? (const double*)c.Mc : nullptr);
     }
     {
         ProfScope ps(LOVE_PROF_GATHER, s);
@@ -369,7 +388,6 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.beta2_acc + j_host, 1, true, s);
     }
-    LOVE_LAUNCH(advance_step_kernel, 1, 32, 0, s, st.jdev);
 }
 
 template <typename V>
@@ -380,6 +398,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.m = c.g.m_total;
     pl.P = c.reorth_passes;
     pl.mean_y = c.probe == LOVE_PROBE_Y;
+    pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
     pl.tile_rows = reorth_tile_rows<V>(c.ldq);

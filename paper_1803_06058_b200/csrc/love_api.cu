@@ -277,6 +277,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
         launch_build_items(*c, s);
         c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
+        if (g.d == 1 && !c->fused) c->Mc = dalloc(*c, sizeof(double) * 4 * (size_t)(M + 4), s);
 
         // ---- K_UU
         setup_kuu(*c, s);
@@ -310,6 +311,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
             c->one = p; p += 1;
             st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
             st.jdev = st.flags + 4;
+            st.step_ctr = st.flags + 5;
             LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
         }
 

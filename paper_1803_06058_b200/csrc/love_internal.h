@@ -51,6 +51,7 @@ struct LanczosState {
     double* amax_bmax;     // [2]
     int* flags;            // [4]        done, k_eff, notpd, zero_probe
     int* jdev;             // [1]        current step index j
+    int* step_ctr;         // [1]        CTAs done in the step's last kernel (advance_step)
     // fused (one-read) mode
     double* AB;            // [k][2][k+1] Gram sums A_i = Q~_i^T r~_j, B_i = Q~_i^T Q~_j of pass j
     double* cvec;          // [k+1]      reorthogonalisation coefficients on Q~_i for the next pass
@@ -100,6 +101,7 @@ struct Cache {
     void* z[2] = {nullptr, nullptr};     // double[m]
     void* M = nullptr;                   // double[4^d * n_items] per-item stencil moments
     void* M2 = nullptr;                  // second moments buffer (fused mode: moments of Q~_j)
+    void* Mc = nullptr;                  // d = 1: double[4][m+4] per-cell stencil moments of the scatter
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)
     // fused (one-read) Lanczos mode
     bool fused = false;
@@ -154,8 +156,10 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
 void launch_build_items(Cache& c, cudaStream_t s);                 // after n_items known
 int64_t count_items_host(Cache& c, cudaStream_t s);                 // syncs
 // ski.cu
+// d = 1 (non-fused caches): per-cell moments into c.Mc, then u unless moments_only (the
+// K_UU MVM then reads the moments itself, launch_kuu(..., Mc))
 template <typename V> void launch_scatter(const Cache& c, const V* qbase, StepRef ref, double* u,
-                                          cudaStream_t s);
+                                          cudaStream_t s, bool moments_only = false);
 template <typename V> void launch_gather(const Cache& c, const double* z, const V* qbase, StepRef ref, V* r,
                                          double* alpha_base, cudaStream_t s);
 template <typename A, typename B> void launch_convert(const A* in, B* out, int64_t n, cudaStream_t s);
@@ -164,7 +168,8 @@ template <typename V> void launch_permute(const Cache& c, const V* in, V* out, b
                                           cudaStream_t s);
 // kuu.cu
 void setup_kuu(Cache& c, cudaStream_t s);
-void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s);
+// z = K_UU u; for d = 1, u may instead be given as the per-cell moments Mc of launch_scatter
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
 void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu

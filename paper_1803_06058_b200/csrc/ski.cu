@@ -126,6 +126,52 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
     }
 }
 
+// d = 1: per-cell stencil moments, one thread per cell, already scaled by q_j's column scale:
+//   Mc[l][c + 2] = s_j * sum_{p in cell c} w_l(p) Q~_j[p]      (l = 0..3, rows of length m + 4)
+// so that (W q_j)[i] = Mc[0][i+3] + Mc[1][i+2] + Mc[2][i+1] + Mc[3][i]  (no atomics, fixed order)
+template <typename V>
+__global__ void __launch_bounds__(256) moments_cell1_kernel(int m, const int* __restrict__ cell_start,
+                                                            const V* __restrict__ f0, const V* __restrict__ qbase,
+                                                            StepRef ref, double* __restrict__ Mc) {
+    pdl_wait();
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= m || step_done(ref)) return;
+    const int j = step_j(ref);
+    const V* __restrict__ q = qbase + j * ref.ld;
+    const int p0 = cell_start[c], p1 = cell_start[c + 1];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int pb = p0; pb < p1; pb += kBatch) {
+        double qv[kBatch], fa[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            const int p = pb + u;
+            const bool in = p < p1;
+            qv[u] = in ? (double)q[p] : 0.0;
+            fa[u] = in ? (double)f0[p] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            double w[4];
+            keys4<double>(fa[u], w);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) acc[l] += w[l] * qv[u];
+        }
+    }
+    const double sc = ref.scale[j];
+    const int ld = m + 4;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) Mc[l * ld + c + 2] = acc[l] * sc;
+}
+
+__global__ void __launch_bounds__(256) nodepass_cell1_kernel(int m, const double* __restrict__ Mc, StepRef ref,
+                                                             double* __restrict__ u) {
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m || step_done(ref)) return;
+    const int ld = m + 4;
+    u[i] = Mc[i + 3] + Mc[ld + i + 2] + Mc[2 * ld + i + 1] + Mc[3 * ld + i];
+}
+
 template <typename V>
 __global__ void permute_kernel(const int* __restrict__ perm, int64_t n, const V* __restrict__ in,
                                V* __restrict__ out, int to_sorted) {
@@ -155,7 +201,15 @@ void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s) {
 }
 
 template <typename V>
-void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStream_t s) {
+void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStream_t s, bool moments_only) {
+    if (c.g.d == 1 && c.Mc != nullptr) {
+        const int m = c.g.m_total;
+        LOVE_LAUNCH(moments_cell1_kernel<V>, (int)ceil_div(m, 256), 256, 0, s, m, c.cell_start, (const V*)c.frac[0],
+                    q, ref, (double*)c.Mc);
+        if (!moments_only)
+            LOVE_LAUNCH(nodepass_cell1_kernel, (int)ceil_div(m, 256), 256, 0, s, m, (const double*)c.Mc, ref, u);
+        return;
+    }
     const int64_t ni = c.n_items;
     const int gi = (int)std::max<int64_t>(1, ceil_div(ni, 256));
     const V* f0 = (const V*)c.frac[0];
@@ -207,8 +261,8 @@ void launch_convert(const A* in, B* out, int64_t n, cudaStream_t s) {
 
 template void launch_convert<float, double>(const float*, double*, int64_t, cudaStream_t);
 template void launch_convert<double, float>(const double*, float*, int64_t, cudaStream_t);
-template void launch_scatter<float>(const Cache&, const float*, StepRef, double*, cudaStream_t);
-template void launch_scatter<double>(const Cache&, const double*, StepRef, double*, cudaStream_t);
+template void launch_scatter<float>(const Cache&, const float*, StepRef, double*, cudaStream_t, bool);
+template void launch_scatter<double>(const Cache&, const double*, StepRef, double*, cudaStream_t, bool);
 template void launch_gather<float>(const Cache&, const double*, const float*, StepRef, float*, double*,
                                    cudaStream_t);
 template void launch_gather<double>(const Cache&, const double*, const double*, StepRef, double*, double*,

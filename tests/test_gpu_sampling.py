@@ -44,9 +44,11 @@ def test_sampling_root_covariance_vs_oracle(kind, ks):
     model = _model(p, inp)
     oc = O.love_precompute(model, p.k)
     sc = O.sampling_cache(model, oc, ks)
-    # run past the numerical rank of M: both stop at breakdown, possibly one step apart (the
-    # last beta sits at the tolerance); the extra direction carries a ~0 eigenvalue of T'
-    assert abs(info["k_sample_eff"] - sc.lanczos.k_eff) <= 1
+    # run past the numerical rank of M: both stop at breakdown (reading A12), which falls in
+    # the tail of M's spectrum (52 eigenvalues above 1e-8 max|M|, 63 above 1e-12),
+    # so k'_eff is set by round-off and may differ by a few steps; the extra directions carry
+    # ~0 eigenvalues of T' and the contract is on S S^T below (reading A15)
+    assert abs(info["k_sample_eff"] - sc.lanczos.k_eff) <= 5
     Xs = inp.Xs[:20]
     S = c.export("S").cpu().numpy()
     Cg = _root_cov(p, S, S.size // p.m_total, info["k_sample_eff"], Xs)
