@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "love_internal.h"
 
@@ -283,6 +284,142 @@ __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2,
     }
 }
 
+// ---- real-input convolution at half length (d = 1, N > kSmallFFT).  u is real and so is z,
+// so the length-N circulant product runs on N' = N/2 complex points:
+//   zeta[n] = u[2n] + i u[2n+1]            (pass A', four-step N' = N1' N2')
+//   Z = FFT_N'(zeta);  E[K] = (Z[K] + conj Z[N'-K]) / 2,  O[K] = (Z[K] - conj Z[N'-K]) / 2i
+//   X[K] = E[K] + w^K O[K],  X[K+N'] = E[K] - w^K O[K]            (w = exp(-2 pi i / N))
+//   Y = lambda X (lambda real, symmetric, * s^2/N);  W[K] = (Y[K] + Y[K+N']) + i w^-K (Y[K] - Y[K+N'])
+//   IFFT_N'(W)[n] = z[2n] + i z[2n+1]                                 (passes B' and C')
+// Pass B' holds the line pair {k2, N2'-k2} (k2 = 0 pairs with N2'/2), so every partner
+// index N' - K of its elements is in the CTA.
+
+// pass A': for each n1, FFT over n2 of zeta[n1 + N1 n2], times w_N'^{n1 k2}
+template <int G>
+__global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
+                                  const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* tws = (C*)smraw;
+    C* buf = tws + N2;
+    load_tw(tws, tw2, N2);
+    const int n1_0 = blockIdx.x * G;
+    const int Np = N1 * N2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t % G, n2 = t / G;
+        const int n = n1_0 + g + N1 * n2;
+        const double re = 2 * n < m ? u_at(u, Mc, m, 2 * n) : 0.0;
+        const double im = 2 * n + 1 < m ? u_at(u, Mc, m, 2 * n + 1) : 0.0;
+        buf[pad(g * N2 + n2)] = make_double2(re, im);
+    }
+    __syncthreads();
+    line_fft<-1>(buf, N2, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N2, k2 = t % N2;
+        const int n1 = n1_0 + g;
+        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(t)], twiddleN<-1>((n1 * k2) & (Np - 1), N1, tw2, twF));
+    }
+}
+
+// pass B': lines {ka, kb} of length N1 (64 threads, 8 elements each): FFT over n1, untangle
+// and multiply by lambda, re-tangle, inverse FFT over k1, times w_N'^{-n1 k2}.
+//   twU1[k1] = w_N^{N2 k1}, twU2[k2] = w_N^{k2}  (so w_N^K = twU1[k1] twU2[k2] for K = N2 k1 + k2)
+//   lamN[K] = lambda[K] * s^2 / N for K = 0..N'
+__global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
+                                  const C* __restrict__ tw2, const C* __restrict__ twF, const C* __restrict__ twU1,
+                                  const C* __restrict__ twU2, const double* __restrict__ lamN) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* tws = (C*)smraw;
+    C* buf = tws + N1;
+    load_tw(tws, tw1, N1);
+    const int b = blockIdx.x;
+    const int kl[2] = {b == 0 ? 0 : b, b == 0 ? N2 / 2 : N2 - b};
+    const int Np = N1 * N2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N1, n1 = t % N1;
+        buf[pad(t)] = Y[(int64_t)n1 * N2 + kl[g]];
+    }
+    __syncthreads();
+    line_fft<-1>(buf, N1, tws);
+    C wv[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N1, k1 = t % N1;
+        const int k2 = kl[g];
+        int gp, k1p;                                   // partner of K = N2 k1 + k2: N' - K (mod N')
+        if (k2 == 0) { gp = g; k1p = (N1 - k1) & (N1 - 1); }
+        else if (2 * k2 == N2) { gp = g; k1p = N1 - 1 - k1; }
+        else { gp = 1 - g; k1p = N1 - 1 - k1; }
+        const C zk = buf[pad(t)];
+        const C zq = cconj(buf[pad(gp * N1 + k1p)]);
+        const C E = make_double2(0.5 * (zk.x + zq.x), 0.5 * (zk.y + zq.y));
+        const C D = make_double2(0.5 * (zk.x - zq.x), 0.5 * (zk.y - zq.y));   // O = -i D
+        const C O = make_double2(D.y, -D.x);
+        const C w = cmul(__ldg(&twU1[k1]), __ldg(&twU2[k2]));
+        const C wO = cmul(w, O);
+        const int K = N2 * k1 + k2;
+        const double l1 = lamN[K], l2 = lamN[Np - K];   // lambda[K + N'] = lambda[N' - K]
+        const C Y1 = make_double2(l1 * (E.x + wO.x), l1 * (E.y + wO.y));
+        const C Y2 = make_double2(l2 * (E.x - wO.x), l2 * (E.y - wO.y));
+        const C S = cadd(Y1, Y2);
+        const C Dm = cmul(cconj(w), csub(Y1, Y2));
+        wv[e] = make_double2(S.x - Dm.y, S.y + Dm.x);   // S + i Dm
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) buf[pad(threadIdx.x + e * blockDim.x)] = wv[e];
+    __syncthreads();
+    line_fft<+1>(buf, N1, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N1, n1 = t % N1;
+        const int k2 = kl[g];
+        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(t)], twiddleN<+1>((n1 * k2) & (Np - 1), N1, tw2, twF));
+    }
+}
+
+// pass C': for each n1, inverse FFT over k2; z[2n] = Re, z[2n+1] = Im at n = n1 + N1 n2
+template <int G>
+__global__ void rfft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
+                                  double* __restrict__ z) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* tws = (C*)smraw;
+    C* buf = tws + N2;
+    load_tw(tws, tw2, N2);
+    const int n1_0 = blockIdx.x * G;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N2, k2 = t % N2;
+        buf[pad(t)] = Y[(int64_t)(n1_0 + g) * N2 + k2];
+    }
+    __syncthreads();
+    line_fft<+1>(buf, N2, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t % G, n2 = t / G;
+        const int n = n1_0 + g + N1 * n2;
+        const C w = buf[pad(g * N2 + n2)];
+        if (2 * n < m) z[2 * n] = w.x;
+        if (2 * n + 1 < m) z[2 * n + 1] = w.y;
+    }
+}
+
+__global__ void lambda_natural_kernel(const C* __restrict__ X, int count, double scale, double* __restrict__ lamN) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) lamN[k] = X[k].x * scale;
+}
+
 // ---- dense per-axis Toeplitz products (d > 1), fp64
 // layout (outer O, length L, inner I): out(o,l,i) = scale * sum_l' c[|l-l'|] in(o,l',i).
 // Strided axes (I > 1): a CTA computes a 16 (rows) x 32 (inner) output tile, looping over
@@ -427,6 +564,21 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
         return;
     }
     constexpr int G = kLinesPerCta;
+    if (mode == 0 && c.rfft_N1 != 0) {          // real-input half-length convolution
+        const int R1 = c.rfft_N1, R2 = c.rfft_N2;
+        const C* r1 = (const C*)c.rtw1;
+        const C* r2 = (const C*)c.rtw2;
+        const C* rF = (const C*)c.rtwF;
+        const size_t sA = sizeof(C) * (padded((size_t)G * R2) + R2), sB = sizeof(C) * (padded((size_t)2 * R1) + R1);
+        ensure_smem((const void*)rfft_passA_kernel<G>, sA);
+        ensure_smem((const void*)rfft_passB_kernel, sB);
+        ensure_smem((const void*)rfft_passC_kernel<G>, sA);
+        LOVE_LAUNCH(rfft_passA_kernel<G>, R1 / G, G * R2 / 8, sA, s, u, Mc, m, R1, R2, r2, rF, work);
+        LOVE_LAUNCH(rfft_passB_kernel, R2 / 2, 2 * R1 / 8, sB, s, work, R1, R2, r1, r2, rF, (const C*)c.rtwU1,
+                    (const C*)c.rtwU2, (const double*)c.rlam);
+        LOVE_LAUNCH(rfft_passC_kernel<G>, R1 / G, G * R2 / 8, sA, s, (const C*)work, m, R1, R2, r2, z);
+        return;
+    }
     const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
     ensure_smem((const void*)fft_passA_kernel<G>, smA);
     ensure_smem((const void*)fft_passB_kernel<G>, smB);
@@ -512,6 +664,28 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     fft_run(c, col, nullptr, N, nullptr, (C*)c.fft_buf, X, 1, s);
     LOVE_LAUNCH(lambda_store_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N, c.fft_N1,
                 c.fft_N2, c.fft_N1 != 0, c.rbf.outputscale / (double)N, (double*)c.lam);
+    // measured: the half-length real path wins from N = 2^18 (cfg2) but not at 2^15 (cfg5),
+    // where the passes are latency-bound and half as many CTAs hide less of it
+    if (c.fft_N1 != 0 && N >= (1 << 17) && std::getenv("LOVE_NO_RFFT") == nullptr) {
+        // real-input path: N' = N/2 = R1 * R2 (R1 = 2^floor(lg N'/2)), tables and lambda[0..N']
+        const int Np = N / 2, lgp = ilog2(Np);
+        c.rfft_N1 = 1 << (lgp / 2);
+        c.rfft_N2 = Np / c.rfft_N1;
+        const int R1 = c.rfft_N1, R2 = c.rfft_N2;
+        c.rtw1 = dalloc(c, sizeof(C) * R1, s);
+        c.rtw2 = dalloc(c, sizeof(C) * R2, s);
+        c.rtwF = dalloc(c, sizeof(C) * R1, s);
+        c.rtwU1 = dalloc(c, sizeof(C) * R1, s);
+        c.rtwU2 = dalloc(c, sizeof(C) * R2, s);
+        c.rlam = dalloc(c, sizeof(double) * (Np + 1), s);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(R1, 256), 256, 0, s, (C*)c.rtw1, R1, R1);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(R2, 256), 256, 0, s, (C*)c.rtw2, R2, R2);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(R1, 256), 256, 0, s, (C*)c.rtwF, R1, Np);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(R1, 256), 256, 0, s, (C*)c.rtwU1, R1, 2 * R1);
+        LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(R2, 256), 256, 0, s, (C*)c.rtwU2, R2, N);
+        LOVE_LAUNCH(lambda_natural_kernel, (int)std::min<int64_t>(ceil_div(Np + 1, 256), 4096), 256, 0, s, X, Np + 1,
+                    c.rbf.outputscale / (double)N, (double*)c.rlam);
+    }
     cuda_check(cudaFreeAsync(col, s), "lam free");
     cuda_check(cudaFreeAsync(X, s), "lam free");
 }

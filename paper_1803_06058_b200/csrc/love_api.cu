@@ -278,6 +278,10 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         launch_build_items(*c, s);
         c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
         if (g.d == 1 && !c->fused) c->Mc = dalloc(*c, sizeof(double) * 4 * (size_t)(M + 4), s);
+        if (g.d >= 2) {
+            c->pullT = dalloc(*c, sizeof(double) * (size_t)(g.d == 2 ? 4 : 16) * M, s);
+            if (g.d == 3) c->pullV = dalloc(*c, sizeof(double) * 4 * (size_t)M, s);
+        }
 
         // ---- K_UU
         setup_kuu(*c, s);

@@ -91,6 +91,9 @@ struct Cache {
     void* tw1 = nullptr;                 // double2 twiddle tables (line FFTs of N1 / small N)
     void* tw2 = nullptr;                 // (line FFTs of N2)
     void* twF = nullptr;                 // exp(-2 pi i k / N), k < N1
+    int rfft_N1 = 0, rfft_N2 = 0;        // real-input convolution at N' = N/2 = rfft_N1 * rfft_N2
+    void *rtw1 = nullptr, *rtw2 = nullptr, *rtwF = nullptr, *rtwU1 = nullptr, *rtwU2 = nullptr;
+    void* rlam = nullptr;                // double[N'+1] lambda * s^2 / N, natural order
     void* ktmp[2] = {nullptr, nullptr};  // double[m] scratch for axis passes
 
     // ---------------- Lanczos
@@ -102,6 +105,8 @@ struct Cache {
     void* M = nullptr;                   // double[4^d * n_items] per-item stencil moments
     void* M2 = nullptr;                  // second moments buffer (fused mode: moments of Q~_j)
     void* Mc = nullptr;                  // d = 1: double[4][m+4] per-cell stencil moments of the scatter
+    void* pullT = nullptr;               // d >= 2: double[4^(d-1)][m] last-axis pull of the scatter
+    void* pullV = nullptr;               // d = 3: double[4][m] middle-axis pull
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)
     // fused (one-read) Lanczos mode
     bool fused = false;

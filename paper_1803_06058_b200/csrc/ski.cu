@@ -21,11 +21,11 @@ namespace {
 
 constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
 
-template <typename V, int D>
+template <typename V, int D, typename MT>
 __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
                                                       const V* __restrict__ f0, const V* __restrict__ f1,
                                                       const V* __restrict__ f2, const V* __restrict__ qbase,
-                                                      StepRef ref, double* __restrict__ M) {
+                                                      StepRef ref, MT* __restrict__ M) {
     pdl_wait();
     using A = typename AccT<V, D>::type;
     constexpr int S = Slots<D>::value;
@@ -57,7 +57,78 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
         }
     }
 #pragma unroll
-    for (int l = 0; l < S; ++l) M[(int64_t)l * n_items + it] = (double)acc[l];
+    for (int l = 0; l < S; ++l) M[(int64_t)l * n_items + it] = (MT)acc[l];
+}
+
+// ---- separable node pull of the scatter (d >= 2), u = W q from the per-item moments
+// M[l][item], slot l = ((a*4 + b)*4 + c) (d = 3) or a*4 + b (d = 2), last index along the
+// last grid axis.  Node (i_0, .., i_{d-1}) receives slot component s_e from cell i_e - s_e + 1
+// along axis e, so the pull factorises axis by axis:
+//   pull_last : T[so][lead cells, i_last] = sum_c sum_{items of cell (lead, i_last - c + 1)} M[so*4 + c][item]
+//   pull_mid  : V[a][c0, i1, i2]          = sum_b T[a*4 + b][c0, i1 - b + 1, i2]          (d = 3)
+//   pull_first: u[i0, ...]                = s_j * sum_a X[a][i0 - a + 1, ...]            (X = V or T)
+// Every pull reads 4 neighbours per output, coalesced along the last axis.
+template <int D, typename MT>
+__global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_items, const int* __restrict__ cis,
+                                                        const MT* __restrict__ M, StepRef ref,
+                                                        double* __restrict__ T) {
+    pdl_wait();
+    constexpr int SO = D == 2 ? 4 : 16;
+    const int m = g.m_total;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= m || step_done(ref)) return;
+    const int ml = g.m[D - 1];
+    const int il = x % ml;
+    double sum[SO];
+#pragma unroll
+    for (int so = 0; so < SO; ++so) sum[so] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int cl = il - c + 1;
+        if (cl < 0 || cl >= ml) continue;
+        const int cell = x + 1 - c;
+        const int e = cis[cell + 1];
+        for (int it = cis[cell]; it < e; ++it)
+#pragma unroll
+            for (int so = 0; so < SO; ++so) sum[so] += (double)M[(int64_t)(so * 4 + c) * n_items + it];
+    }
+#pragma unroll
+    for (int so = 0; so < SO; ++so) T[(int64_t)so * m + x] = sum[so];
+}
+
+__global__ void __launch_bounds__(256) pull_mid_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
+                                                       double* __restrict__ Vout) {
+    pdl_wait();
+    const int m = g.m_total;
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= 4 * (int64_t)m || step_done(ref)) return;
+    const int a = (int)(idx / m), x = (int)(idx - (int64_t)a * m);
+    const int i1 = (x / g.stride[1]) % g.m[1];
+    double sum = 0.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int c1 = i1 - b + 1;
+        if (c1 < 0 || c1 >= g.m[1]) continue;
+        sum += T[(int64_t)(a * 4 + b) * m + x + (1 - b) * g.stride[1]];
+    }
+    Vout[idx] = sum;
+}
+
+__global__ void __launch_bounds__(256) pull_first_kernel(GridDev g, const double* __restrict__ X, StepRef ref,
+                                                         double* __restrict__ u) {
+    pdl_wait();
+    const int m = g.m_total;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= m || step_done(ref)) return;
+    const int i0 = x / g.stride[0];
+    double sum = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int c0 = i0 - a + 1;
+        if (c0 < 0 || c0 >= g.m[0]) continue;
+        sum += X[(int64_t)a * m + x + (1 - a) * g.stride[0]];
+    }
+    u[x] = sum * ref.scale[step_j(ref)];
 }
 
 // u[i] = scale * sum over slots l of sum over items of cell (i - l + 1) of M[l][item]
@@ -216,11 +287,31 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
     const V* f1 = (const V*)c.frac[1];
     const V* f2 = (const V*)c.frac[2];
     double* M = (double*)c.M;
+    const int m = c.g.m_total;
+    if (c.g.d >= 2 && c.pullT != nullptr) {
+        if (c.g.d == 2) {
+            if (ni) LOVE_LAUNCH((moments_kernel<V, 2, double>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M);
+            LOVE_LAUNCH((pull_last_kernel<2, double>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
+                        c.cell_item_start, (const double*)M, ref, (double*)c.pullT);
+            LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
+        } else {
+            // the 3-D moments are stored in their accumulation type (fp32 in LOVE_FP32 mode)
+            using MT = typename AccT<V, 3>::type;
+            MT* Mf = (MT*)c.M;
+            if (ni) LOVE_LAUNCH((moments_kernel<V, 3, MT>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, Mf);
+            LOVE_LAUNCH((pull_last_kernel<3, MT>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
+                        c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
+            LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g, (const double*)c.pullT,
+                        ref, (double*)c.pullV);
+            LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);
+        }
+        return;
+    }
     if (ni) {
         switch (c.g.d) {
-            case 1: LOVE_LAUNCH((moments_kernel<V, 1>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
-            case 2: LOVE_LAUNCH((moments_kernel<V, 2>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
-            default: LOVE_LAUNCH((moments_kernel<V, 3>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+            case 1: LOVE_LAUNCH((moments_kernel<V, 1, double>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+            case 2: LOVE_LAUNCH((moments_kernel<V, 2, double>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
+            default: LOVE_LAUNCH((moments_kernel<V, 3, double>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M); break;
         }
     }
     launch_nodepass(c, ref, u, s);

@@ -54,6 +54,7 @@ def _rel2(a, b):
     ("cfg1", 1, None, "fp64"), ("cfg1_fp32", 1, None, "fp32"), ("cfg5m", 5, None, "fp32"),
     ("cfg2m", 2, None, "fp32"), ("cfg3m", 3, None, "fp32"), ("cfg4m", 4, None, "fp32"),
     ("1d_4096", 1, (4096,), "fp32"), ("1d_2049_fp64", 1, (2049,), "fp64"), ("3d_odd", 4, (9, 10, 11), "fp64"),
+    ("1d_65537_fp64", 1, (65537,), "fp64"), ("1d_70001", 1, (70001,), "fp32"),   # real-input half-length FFT
 ])
 def test_kuu_mvm(case):
     name, ci, m, prec = case
