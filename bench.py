@@ -63,6 +63,26 @@ def reorth_bytes(n_local: int, k: int, vsize: int, passes: int = 1) -> dict:
     return {"dots": dots, "update": upd}
 
 
+def build_bytes(p, n_local: int) -> int:
+    """Algorithmic bytes of one cache build, SURVEY.md §8(d):
+    B_step(j) = n (2 r_d + 5 s_v) + P * 2 n j s_v + 4 m s_v  (j = 1..k; P = reorthogonalisation
+    passes: 1 in fp32, 2 = CGS2 in fp64), B_build = sum_j B_step(j) + 2 m k s_v,
+    with s_v the vector element size and r_d = 8d (fp32) / 12d (fp64) bytes of a point's record."""
+    fp64 = p.precision == "fp64"
+    sv, rd, P = (8, 12 * p.d, 2) if fp64 else (4, 8 * p.d, 1)
+    tot = 0
+    for j in range(1, p.k + 1):
+        tot += n_local * (2 * rd + 5 * sv) + P * 2 * n_local * j * sv + 4 * p.m_total * sv
+    return tot + 2 * p.m_total * p.k * sv
+
+
+def query_bytes(p, k_pad: int) -> int:
+    """Algorithmic bytes of one variance query: the 4^d gathered rows of Rc
+    (k_pad values each), the fp64 query point and the result."""
+    sv = 8 if p.precision == "fp64" else 4
+    return 4 ** p.d * k_pad * sv + 8 * p.d + sv
+
+
 class ClockSampler:
     """SM clock and throttle-reason sampling DURING the timed region (the recipe's clocks
     line).  NVML is polled from a thread every ~2 ms (nvidia-smi -lms cannot resolve a
@@ -220,7 +240,7 @@ def main():
     y = torch.from_numpy(inp.y).to(dev)
     Xs = torch.from_numpy(inp.Xs).to(dev)
     kw = dict(m=p.m, lo=p.lo, h=p.h, lengthscale=p.lengthscale, outputscale=p.outputscale, sigma2=p.sigma2,
-              k=p.k, precision=p.precision, rank=rank, world=world, nccl_id=nccl_id)
+              k=p.k, precision=p.precision, rank=rank, world=world, nccl_id=nccl_id, k_sample=p.k_sample)
     lib = _abi.load()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     lib.love_profile_enable(0)
@@ -228,8 +248,12 @@ def main():
     def step(Xd, yd, Xsd, e2e=False):
         c = LoveCache.build(Xd, yd, **kw)
         var = c.predict_var(Xsd)
+        if p.k_sample:
+            F = c.sample(Xsd, p.s, seed=0)
         if e2e:
             var = var.cpu()
+            if p.k_sample:
+                F = F.cpu()
         c.free()
         return var
 
@@ -249,19 +273,26 @@ def main():
     clocks.start()
     launches0 = launch_count()
     total_ms = 0.0
-    build_ms = []
+    build_ms, query_ms, sample_ms = [], [], []
+    k_pad = 0
     barrier()
     for _ in range(args.steps):
         flush.zero_()
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
         e0.record(stream)
         c = LoveCache.build(X, y, **kw)
         e1.record(stream)
         c.predict_var(Xs)
         e2.record(stream)
-        e2.synchronize()
-        total_ms += e0.elapsed_time(e2)
+        if p.k_sample:
+            c.sample(Xs, p.s, seed=0)
+        e3.record(stream)
+        e3.synchronize()
+        total_ms += e0.elapsed_time(e3)
         build_ms.append(e0.elapsed_time(e1))
+        query_ms.append(e1.elapsed_time(e2))
+        sample_ms.append(e2.elapsed_time(e3))
+        k_pad = c.info()["k_pad"]
         c.free()
     barrier()
     launches = launch_count() - launches0
@@ -343,6 +374,24 @@ def main():
                "h2d_bytes_per_step": int(inp.X.nbytes + inp.y.nbytes + inp.Xs.nbytes),
                "d2h_bytes_per_step": int(p.t * vs), "ms_per_step": te}
 
+    # whole-build and query roofline fractions under SURVEY §8(d)'s byte model
+    bb = build_bytes(p, p.n)
+    b_ach = bb / (float(np.mean(build_ms)) / 1e3) / 1e9
+    build_rf = {"bound": "hbm", "algorithmic_bytes": bb, "achieved": b_ach, "peak": peak, "unit": "GB/s",
+                "frac": b_ach / peak, "model": "SURVEY 8(d) B_build (one CGS pass = 2 reads of Q_j per step)"}
+    qb = query_bytes(p, k_pad) * p.t
+    q_ach = qb / (float(np.mean(query_ms)) / 1e3) / 1e9
+    query_rf = {"bound": "hbm (gathered-row model; Rc is L2-resident at these sizes)", "algorithmic_bytes": qb,
+                "achieved": q_ach, "peak": peak, "unit": "GB/s", "frac": q_ach / peak,
+                "bytes_per_query": query_bytes(p, k_pad)}
+    sampling = None
+    if p.k_sample:
+        smean = float(np.mean(sample_ms))
+        sampling = {"s": p.s, "t": p.t, "k_sample": p.k_sample, "sample_ms": smean,
+                    "joint_samples_per_s": world * p.s / (smean / 1e3),
+                    "sample_values_per_s": world * p.s * p.t / (smean / 1e3),
+                    "note": "draws only (Philox zeta + W*^T S zeta + mean); the sampling cache is in build_ms"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(p, inp)
@@ -356,7 +405,10 @@ def main():
                        "d": p.d, "l2": "flushed (256 MB write) between timed steps",
                        "parallelism": f"dp{world} (training + test points sharded, NCCL all-reduce per step)"},
             "build_ms": float(np.mean(build_ms)),
-            "query_variances_per_s": p.t / ((ms_per_step - float(np.mean(build_ms))) / 1e3),
+            "query_ms": float(np.mean(query_ms)),
+            "query_variances_per_s": p.t / (float(np.mean(query_ms)) / 1e3),
+            "build_roofline": build_rf, "query_roofline": query_rf,
+            "sampling": sampling,
             "phase_ms_per_step": {k: round(v, 4) for k, v in prof_ms.items() if v > 0},
             "profiled_step_ms": prof_step_ms,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
