@@ -497,6 +497,77 @@ __global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict
     out[o] = ((a0 + a1) + (a2 + a3)) * scale;
 }
 
+// ---- d > 1: T(c_d) applied along axis d by circulant-embedding FFTs of length N_d (P:187-188,
+// reading A25), batched over the lines of the axis.  lambda_d is real and symmetric, so the
+// circulant maps real lines to real lines and two lines travel as one complex line
+// (x1 + i x2 -> T x1 + i T x2).  Data viewed as [O][L][I]; line (o, i) = in[(o L + l) I + i].
+// P complex lines per CTA, P*N/8 threads (radix-8 Stockham, 8 elements per thread).
+// LFAST (I == 1): a pair is two consecutive lines (o, o+1) and threads walk along l;
+// otherwise a pair is (i, i+1) of one o and threads walk across pairs (coalesced in i).
+template <bool LFAST>
+__global__ void axis_conv_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ lam,
+                                 const C* __restrict__ tw, int L, int I, int64_t O, int N, int P, int64_t npairs,
+                                 double scale) {
+    pdl_wait();
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* tws = (C*)smraw;
+    C* buf = tws + N;
+    load_tw(tws, tw, N);
+    const int64_t q0 = (int64_t)blockIdx.x * P;
+    const int halfI = (I + 1) / 2;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int p = LFAST ? t / N : t % P, n = LFAST ? t % N : t / P;
+        const int64_t q = q0 + p;
+        double x1 = 0.0, x2 = 0.0;
+        if (q < npairs && n < L) {
+            if (LFAST) {
+                const int64_t o = 2 * q;
+                x1 = in[o * L + n];
+                if (o + 1 < O) x2 = in[(o + 1) * L + n];
+            } else {
+                const int64_t o = q / halfI;
+                const int i = 2 * (int)(q - o * halfI);
+                const int64_t base = (o * L + n) * I + i;
+                x1 = in[base];
+                if (i + 1 < I) x2 = in[base + 1];
+            }
+        }
+        buf[pad(p * N + n)] = make_double2(x1, x2);
+    }
+    __syncthreads();
+    line_fft<-1>(buf, N, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const double l = lam[t % N];
+        buf[pad(t)].x *= l;
+        buf[pad(t)].y *= l;
+    }
+    __syncthreads();
+    line_fft<+1>(buf, N, tws);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int p = LFAST ? t / N : t % P, n = LFAST ? t % N : t / P;
+        const int64_t q = q0 + p;
+        if (q >= npairs || n >= L) continue;
+        const C v = buf[pad(p * N + n)];
+        if (LFAST) {
+            const int64_t o = 2 * q;
+            out[o * L + n] = v.x * scale;
+            if (o + 1 < O) out[(o + 1) * L + n] = v.y * scale;
+        } else {
+            const int64_t o = q / halfI;
+            const int i = 2 * (int)(q - o * halfI);
+            const int64_t base = (o * L + n) * I + i;
+            out[base] = v.x * scale;
+            if (i + 1 < I) out[base + 1] = v.y * scale;
+        }
+    }
+}
+
 __global__ void rbf_columns_kernel(GridDev g, double l0, double l1, double l2, double* __restrict__ cols) {
     const double ls[3] = {l0, l1, l2};
     int off = 0;
@@ -600,7 +671,22 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         double* out = (d == g.d - 1) ? z : (double*)c.ktmp[d & 1];
         const double scale = (d == g.d - 1) ? c.rbf.outputscale : 1.0;
         const double* col = c.cols64 + off;
-        if (I == 1) {
+        if (c.ax_N[d] > 0) {                    // batched line FFTs (two real lines per complex line)
+            const int N = c.ax_N[d];
+            const int P = std::max(1, std::min(8, 1024 / N));
+            const int64_t npairs = I == 1 ? (O + 1) / 2 : (int64_t)O * ((I + 1) / 2);
+            const size_t sm = sizeof(C) * (N + padded((size_t)P * N));
+            const int grid = (int)ceil_div(npairs, P);
+            if (I == 1) {
+                ensure_smem((const void*)axis_conv_kernel<true>, sm);
+                LOVE_LAUNCH(axis_conv_kernel<true>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
+                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale);
+            } else {
+                ensure_smem((const void*)axis_conv_kernel<false>, sm);
+                LOVE_LAUNCH(axis_conv_kernel<false>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
+                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale);
+            }
+        } else if (I == 1) {
             const int64_t total = (int64_t)O * L;
             LOVE_LAUNCH(axis_line_kernel, (int)ceil_div(total, 256), 256, 0, s, in, out, col, (int64_t)O, L, scale);
         } else {
@@ -631,6 +717,35 @@ void setup_kuu(Cache& c, cudaStream_t s) {
             if (g.m[d] > 1024) throw LoveError{LOVE_ERR_ARG, "Kronecker grids need m_d <= 1024 per axis"};
         c.ktmp[0] = dalloc(c, sizeof(double) * g.m_total, s);
         c.ktmp[1] = dalloc(c, sizeof(double) * g.m_total, s);
+        // per-axis circulant eigenvalues lambda_d / N_d (FFT of the embedded column, mode 1)
+        const bool use_fft = std::getenv("LOVE_AXIS_DENSE") == nullptr;
+        int off = 0;
+        for (int d = 0; d < g.d; ++d) {
+            const int md = g.m[d];
+            int Nd = 8;
+            while (Nd < 2 * md - 1) Nd *= 2;
+            c.ax_N[d] = 0;
+            if (use_fft && Nd <= kSmallFFT) {
+                c.ax_N[d] = Nd;
+                c.ax_tw[d] = dalloc(c, sizeof(C) * Nd, s);
+                c.ax_lam[d] = dalloc(c, sizeof(double) * Nd, s);
+                LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(Nd, 256), 256, 0, s, (C*)c.ax_tw[d], Nd, Nd);
+                double* colN = nullptr;
+                C* X = nullptr;
+                cuda_check(cudaMallocAsync((void**)&colN, sizeof(double) * Nd, s), "axis lam alloc");
+                cuda_check(cudaMallocAsync((void**)&X, sizeof(C) * Nd, s), "axis lam alloc");
+                LOVE_LAUNCH(embed_kernel, (int)ceil_div(Nd, 256), 256, 0, s, c.cols64 + off, md, Nd, colN);
+                const size_t sm = sizeof(C) * (padded(Nd) + Nd);
+                ensure_smem((const void*)fft_small_kernel, sm);
+                LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, Nd / 8), sm, s, colN, (const double*)nullptr, Nd, Nd,
+                            (const C*)c.ax_tw[d], (const double*)nullptr, (double*)nullptr, X, 1);
+                LOVE_LAUNCH(lambda_store_kernel, (int)ceil_div(Nd, 256), 256, 0, s, X, Nd, 0, 0, 0, 1.0 / (double)Nd,
+                            (double*)c.ax_lam[d]);
+                cuda_check(cudaFreeAsync(colN, s), "axis lam free");
+                cuda_check(cudaFreeAsync(X, s), "axis lam free");
+            }
+            off += md;
+        }
         return;
     }
     // d = 1: circulant embedding and its eigenvalues, stored * s^2 / N

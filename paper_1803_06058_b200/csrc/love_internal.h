@@ -95,6 +95,9 @@ struct Cache {
     void *rtw1 = nullptr, *rtw2 = nullptr, *rtwF = nullptr, *rtwU1 = nullptr, *rtwU2 = nullptr;
     void* rlam = nullptr;                // double[N'+1] lambda * s^2 / N, natural order
     void* ktmp[2] = {nullptr, nullptr};  // double[m] scratch for axis passes
+    int ax_N[3] = {0, 0, 0};             // d > 1: per-axis circulant length (0: dense axis product)
+    void* ax_tw[3] = {nullptr, nullptr, nullptr};   // exp(-2 pi i k / N_d), k < N_d
+    void* ax_lam[3] = {nullptr, nullptr, nullptr};  // double[N_d]: lambda_d / N_d
 
     // ---------------- Lanczos
     int k_alloc = 0;
