@@ -22,13 +22,14 @@ namespace {
 constexpr int kMaxKs = 112;          // k' limit of the single-CTA Jacobi eigensolver (smem)
 
 // out[c] += sum_r A[r + c*lda] * x[r], c < ncol   (fp64, CTA row tiles, warps own columns)
+constexpr int kDotRows = 128;       // rows per CTA tile of dots_kernel (~m/128 CTAs)
 __global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ A, int64_t lda, int nrow, int ncol,
                                                    const double* __restrict__ x, double* __restrict__ out,
                                                    const int* __restrict__ stop) {
     if (stop && *stop) return;
-    __shared__ double xs[1024];
-    const int r0 = blockIdx.x * 1024;
-    const int nr = min(1024, nrow - r0);
+    __shared__ double xs[kDotRows];
+    const int r0 = blockIdx.x * kDotRows;
+    const int nr = min(kDotRows, nrow - r0);
     for (int i = threadIdx.x; i < nr; i += blockDim.x) xs[i] = x[r0 + i];
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -174,7 +175,9 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
         __syncthreads();
         if ((threadIdx.x & 31) == 0) atomicAdd(&diag_norm, dia);
         __syncthreads();
-        if (offn <= 1e-30 * (diag_norm + 1e-300)) break;
+        // converged: off-diagonal Frobenius norm <= 1e-13 of the diagonal's (fp64 round-off of
+        // the rotations is ~1e-15 per sweep; the root only needs T'^{1/2} to ~1e-12)
+        if (offn <= 1e-26 * (diag_norm + 1e-300)) break;
         for (int round = 0; round < N - 1; ++round) {
             // round-robin pairs: position 0 fixed, the others rotate
             for (int pi = threadIdx.x; pi < N / 2; pi += blockDim.x) {
@@ -452,7 +455,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         const int kk = ks;
         cuda_check(cudaMemcpyAsync(st.flags + 1, &kk, sizeof(int), cudaMemcpyHostToDevice, s), "flags");
     }
-    const int gm = (int)ceil_div(m, 256), gd = (int)ceil_div(m, 1024);
+    const int gm = (int)ceil_div(m, 256), gd = (int)ceil_div(m, kDotRows);
     double* n2 = st.acc + (int64_t)ks * slot;          // spare slot: ||M 1||^2
     // M v for a vector x: z = K_UU x ; t = Rc^T x ; out = z - Rc t
     auto apply_M = [&](const double* x, double* out, double* tacc) {
@@ -465,7 +468,14 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     apply_M(v, v, n2 + 4);
     LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, v, (int64_t)ldq, m, 1, v, n2, (const int*)nullptr);
     LOVE_LAUNCH(probe_normalize_kernel, gm, 256, 0, s, v, Qp, m, n2, st);
+    int* hflag = nullptr;                               // pinned: breakdown polled every 8 steps
+    cuda_check(cudaMallocHost((void**)&hflag, sizeof(int)), "pinned flag");
     for (int j = 0; j < ks; ++j) {
+        if (j > 0 && (j & 7) == 0) {   // stop issuing steps once the M-Lanczos has broken down (A12)
+            cuda_check(cudaMemcpyAsync(hflag, st.flags, sizeof(int), cudaMemcpyDeviceToHost, s), "flag poll");
+            cuda_check(cudaStreamSynchronize(s), "flag poll");
+            if (*hflag) break;
+        }
         double* acc = st.acc + (int64_t)j * slot;      // [0] alpha, [1] beta^2, [4..] CGS dots, then Rc^T q
         const double* qj = Qp + (int64_t)j * ldq;
         apply_M(qj, v, acc + 4 + 2 * (ks + 1));
@@ -486,6 +496,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     int hfl[4];
     cuda_check(cudaMemcpyAsync(hfl, st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
     cuda_check(cudaStreamSynchronize(s), "sampling sync");
+    cudaFreeHost(hflag);
     if (hfl[2]) throw LoveError{LOVE_ERR_ZERO_PROBE, "sampling probe M 1 is zero"};
     const int ke = hfl[0] ? hfl[1] : ks;
     c.k_sample_eff = ke;
