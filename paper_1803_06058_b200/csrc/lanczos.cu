@@ -20,6 +20,9 @@
 #ifndef LOVE_DOTS_U
 #define LOVE_DOTS_U 8
 #endif
+#ifndef LOVE_SWEEP_NB
+#define LOVE_SWEEP_NB 1
+#endif
 #ifndef LOVE_UPD_U
 #define LOVE_UPD_U 7
 #endif
@@ -222,6 +225,100 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
     }
 }
 
+// ---- reorthogonalisation dots, column-sweep variant (the update kernel's access pattern):
+// every thread holds CPT 16-byte chunks of r' in registers and sweeps the columns in blocks of
+// 8; the 8 per-lane partials of a block are reduced across the warp by a butterfly
+// reduce-scatter (xor 4, 2, 1: 7 shuffles) plus xor 8, 16, after which lane l holds column
+// 8b + (l & 7) summed over the warp; lanes 0..7 park it in shared memory (fp64).
+template <typename V, int CPT>
+__global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restrict__ Q, int64_t ldq, int k, int pass,
+                                                                const V* __restrict__ r, LanczosState st) {
+    pdl_wait();
+    constexpr int W = VecT<V>::W;
+    extern __shared__ __align__(16) double smd[];
+    const int j = *st.jdev;
+    if (st.flags[0] || j >= k - 1) return;
+    const int from_r = pass == 0;
+    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
+    const int ncols = j + 1;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* csum = smd;                                   // [nw][ncols]
+    const double sj = st.qscale[j];
+    const double aj = st.alpha_acc[j] * sj;
+    const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
+    const int64_t nvec = ldq / W;
+    V src[CPT][W];
+    int64_t qv[CPT];
+#pragma unroll
+    for (int u = 0; u < CPT; ++u) {
+        qv[u] = ((int64_t)blockIdx.x * CPT + u) * blockDim.x + threadIdx.x;
+        double v[W];
+        if (qv[u] < nvec) load_src<V>(Q, ldq, r, from_r, j, aj, bj1, qv[u] * W, v);
+        else
+#pragma unroll
+            for (int e = 0; e < W; ++e) v[e] = 0.0;
+#pragma unroll
+        for (int e = 0; e < W; ++e) src[u][e] = (V)v[e];
+    }
+    const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
+    constexpr int NB = LOVE_SWEEP_NB;                    // 8-column blocks whose loads are issued together
+    for (int c00 = 0; c00 < ncols; c00 += 8 * NB) {
+    V pvb[NB][8];
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb)
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+            V& pcell = pvb[bb][cc];
+            const int cidx = c00 + 8 * bb + cc;
+            pcell = V(0);
+            if (cidx < ncols) {
+#pragma unroll
+                for (int u = 0; u < CPT; ++u) {
+                    if (qv[u] < nvec) {
+                        V a[W];
+                        vload<V>(Q + (int64_t)cidx * ldq + qv[u] * W, a);
+#pragma unroll
+                        for (int e = 0; e < W; ++e) pcell += a[e] * src[u][e];
+                    }
+                }
+            }
+        }
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb) {
+        const int c0 = c00 + 8 * bb;
+        if (c0 >= ncols) break;
+        const V* pv = pvb[bb];
+        // reduce-scatter: keep 4 of 8 (xor 4), 2 of 4 (xor 2), 1 of 2 (xor 1)
+        double h4[4], h2[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double keep = (double)(b2 ? pv[i + 4] : pv[i]), send = (double)(b2 ? pv[i] : pv[i + 4]);
+            h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const double keep = b1 ? h4[i + 2] : h4[i], send = b1 ? h4[i] : h4[i + 2];
+            h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        double h1;
+        {
+            const double keep = b0 ? h2[1] : h2[0], send = b0 ? h2[0] : h2[1];
+            h1 = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        }
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 8);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, 16);
+        const int col = c0 + (b2 << 2 | b1 << 1 | b0);
+        if (lane < 8 && col < ncols) csum[wid * ncols + col] = h1;
+    }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+        double tot = 0.0;
+        for (int w = 0; w < nw; ++w) tot += csum[w * ncols + i];
+        atomicAdd(&c_out[i], tot * st.qscale[i]);
+    }
+}
+
 // Last-CTA-done step advance: every CTA of the grid calls this once at its end (uniformly
 // per CTA); the last one to arrive resets the counter and writes j + 1 to the step index.
 __device__ __forceinline__ void advance_step(const LanczosState& st, int j) {
@@ -328,6 +425,7 @@ template <typename V>
 struct StepPlan {
     Cache* c;
     int k, m, P, mean_y, gm, gr, gu;
+    int dots_mode;                // 1 (default): column sweep, 1 chunk per thread; 2: 2 chunks; 0: row tiles
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
     int64_t ldq, tile_rows;
     size_t smd, smu;
@@ -372,7 +470,14 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     for (int pass = 0; pass < pl.P; ++pass) {
         {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
-            LOVE_LAUNCH(reorth_dots_kernel<V>, pl.gr, 256, pl.smd, s, Q, pl.ldq, pl.tile_rows, pl.k, pass, r, st);
+            if (pl.dots_mode == 0)
+                LOVE_LAUNCH(reorth_dots_kernel<V>, pl.gr, 256, pl.smd, s, Q, pl.ldq, pl.tile_rows, pl.k, pass, r, st);
+            else if (pl.dots_mode == 1)
+                LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
+                            sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
+            else
+                LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 2>), (int)ceil_div(pl.ldq / VecT<V>::W, 512), 256,
+                            sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
         }
         if (c.comm != nullptr && j_host < pl.k - 1) {
             ProfScope ps(LOVE_PROF_COMM, s);
@@ -398,6 +503,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.m = c.g.m_total;
     pl.P = c.reorth_passes;
     pl.mean_y = c.probe == LOVE_PROBE_Y;
+    pl.dots_mode = std::getenv("LOVE_DOTS") ? std::atoi(std::getenv("LOVE_DOTS")) : 1;
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
