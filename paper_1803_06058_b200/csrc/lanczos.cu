@@ -319,14 +319,57 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     }
 }
 
-// Last-CTA-done step advance: every CTA of the grid calls this once at its end (uniformly
-// per CTA); the last one to arrive resets the counter and writes j + 1 to the step index.
-__device__ __forceinline__ void advance_step(const LanczosState& st, int j) {
+// Scalars of index i once alpha_i and beta_i^2 are complete (same rules as the prologue):
+// alpha_i, row i of the Cholesky of T, g_i = (L^{-1} e_1)_i, beta_i, the
+// breakdown test (reading A12) and the scale of q_{i+1}.  One thread.
+__device__ __forceinline__ void finalize_index(const LanczosState& st, int i, int k, double tol) {
+    int* fl = st.flags;
+    if (fl[1] <= i || fl[2] || fl[3]) return;
+    const double al = st.alpha_acc[i];
+    const double amax = fmax(st.amax_bmax[0], fabs(al));
+    const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
+    const double piv = al - lsub * lsub;
+    if (!(piv > 0.0)) {
+        fl[2] = 1;
+        fl[0] = 1;
+        fl[1] = i;
+        return;
+    }
+    const double ld = sqrt(piv);
+    st.alpha[i] = al;
+    st.Ld[i] = ld;
+    st.g[i] = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
+    st.amax_bmax[0] = amax;
+    if (i + 1 == k) {
+        fl[0] = 1;
+        fl[1] = k;
+        return;
+    }
+    const double b = sqrt(st.beta2_acc[i]);
+    const double bmax = fmax(st.amax_bmax[1], b);
+    st.amax_bmax[1] = bmax;
+    if (!(b >= tol * (amax + 2.0 * bmax))) {
+        fl[0] = 1;
+        fl[1] = i + 1;
+    } else {
+        st.beta[i] = b;
+        st.Ls[i] = b / ld;
+        st.qscale[i + 1] = 1.0 / b;
+    }
+}
+
+// Last-CTA-done step advance (every CTA calls it once at its end): the last CTA optionally
+// finalises the scalars of index j (single GPU: beta_j^2 is complete once every CTA of the
+// update has added its part) and writes j + 1 to the step index.
+__device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
+                                             double tol = 0.0) {
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(st.step_ctr), 1u);
         if (prev == gridDim.x - 1) {
+            __threadfence();
+            if (fin) finalize_index(st, j, k, tol);
             st.step_ctr[0] = 0;
             st.jdev[0] = j + 1;
             __threadfence();
@@ -338,7 +381,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j) {
 template <typename V>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
                                                             int pass, int last_pass, const V* __restrict__ r,
-                                                            LanczosState st) {
+                                                            LanczosState st, double tol, int fold) {
     pdl_wait();
     constexpr int W = VecT<V>::W;
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
@@ -347,7 +390,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     // the last pass's update is the last kernel of step j: its last CTA to finish advances
     // the device step index (every CTA has read j by then), also on the early-exit path
     if (st.flags[0] || j >= k - 1) {
-        if (last_pass) advance_step(st, j);
+        if (last_pass) advance_step(st, j, fold && j == k - 1, k, tol);
         return;
     }
     const int from_r = pass == 0;
@@ -391,7 +434,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     if (beta2_out != nullptr) {
         b2 = block_sum(b2, red);
         if (threadIdx.x == 0) atomicAdd(beta2_out, b2);
-        advance_step(st, j);
+        advance_step(st, j, fold != 0, k, tol);
     }
 }
 
@@ -421,10 +464,31 @@ int64_t reorth_tile_rows(int64_t ldq) {
 
 
 
+// q_0 = b / ||b|| (scale of column 0) or the zero-probe flag (folded-prologue path)
+__global__ void init_q0_kernel(LanczosState st) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double b2 = st.bnorm2[0];
+    if (!(b2 > 0.0)) {
+        st.flags[3] = 1;
+        st.flags[0] = 1;
+        st.flags[1] = 0;
+    } else {
+        st.qscale[0] = 1.0 / sqrt(b2);
+    }
+}
+
+// the last streamed cache column (index *jdev - 1) after the loop
+__global__ void stream_rc_kernel(RcStream rs) {
+    pdl_wait();
+    stream_rc_column(rs, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 template <typename V>
 struct StepPlan {
     Cache* c;
     int k, m, P, mean_y, gm, gr, gu;
+    bool fold;                    // single GPU: scalars in the update's last CTA, cache column in the gather
+    RcStream rs;
     int dots_mode;                // 1 (default): column sweep, 1 chunk per thread; 2: 2 chunks; 0: row tiles
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
     int64_t ldq, tile_rows;
@@ -441,7 +505,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     V* r = (V*)c.r;
     double* u = (double*)c.u;
     const StepRef ref{st.jdev, pl.ldq, st.qscale, st.flags};
-    {
+    if (!pl.fold) {
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(step_prologue_kernel, pl.gm, 256, 0, s, st, pl.k, c.tol, pl.m, (const double*)c.z[0],
                     (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.mean_y);
@@ -461,7 +525,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_GATHER, s);
-        launch_gather<V>(c, zj, Q, ref, r, st.alpha_acc, s);
+        launch_gather<V>(c, zj, Q, ref, r, st.alpha_acc, s, pl.fold ? &pl.rs : nullptr);
     }
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
@@ -486,7 +550,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
             LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
-                        pass == pl.P - 1 ? 1 : 0, r, st);
+                        pass == pl.P - 1 ? 1 : 0, r, st, c.tol, pl.fold ? 1 : 0);
         }
     }
     if (c.comm != nullptr && j_host < pl.k - 1) {
@@ -505,6 +569,9 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.mean_y = c.probe == LOVE_PROBE_Y;
     pl.dots_mode = std::getenv("LOVE_DOTS") ? std::atoi(std::getenv("LOVE_DOTS")) : 1;
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
+    pl.fold = c.comm == nullptr && std::getenv("LOVE_NO_FOLD") == nullptr;
+    pl.rs = RcStream{c.st, (const double*)c.z[0], (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.m,
+                     pl.mean_y};
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
     pl.tile_rows = reorth_tile_rows<V>(c.ldq);
@@ -523,6 +590,10 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.bnorm2, 1, true, s);
+    }
+    if (pl.fold) {
+        ProfScope ps(LOVE_PROF_SCALARS, s);
+        LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st);
     }
     const bool graph = c.comm == nullptr && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
     // every kernel of a step starts with pdl_wait(): its launch can overlap the previous
@@ -551,7 +622,10 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     } else {
         for (int j = 0; j < pl.k; ++j) enqueue_step<V>(pl, j, s);
     }
-    {   // finalise index k-1: alpha_{k-1}, L_{k-1,k-1}, Rc[:, k-1], a
+    if (pl.fold) {   // the last streamed column (its scalars were finalised by the last update)
+        ProfScope ps(LOVE_PROF_SCALARS, s);
+        LOVE_LAUNCH(stream_rc_kernel, pl.gm, 256, 0, s, pl.rs);
+    } else {         // finalise index k-1: alpha_{k-1}, L_{k-1,k-1}, Rc[:, k-1], a
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(step_prologue_kernel, pl.gm, 256, 0, s, st, pl.k, c.tol, pl.m, (const double*)c.z[0],
                     (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.mean_y);

@@ -58,6 +58,20 @@ struct LanczosState {
     double* gam;           // [k+1]      coefficients of u~_i in u~_{j+1}
 };
 
+// Column i of the streamed cache, Rc[:, i] = (z_i - L_{i,i-1} Rc[:, i-1]) / L_ii and
+// a += ||b|| g_i Rc[:, i] (probe y), computed by extra CTAs of the next step's gather
+// kernel once the update kernel's last CTA has finalised the scalars of index i
+// (single-GPU Lanczos; i = *jdev - 1, z_i in z[i & 1]).
+struct RcStream {
+    LanczosState st;
+    const double* z0;
+    const double* z1;
+    double* Rc;          // fp64 column-major m x k
+    double* a;           // mean cache (probe y)
+    int m;
+    int mean_y;
+};
+
 struct Cache {
     // ---------------- configuration
     GridDev g;
@@ -169,7 +183,23 @@ int64_t count_items_host(Cache& c, cudaStream_t s);                 // syncs
 template <typename V> void launch_scatter(const Cache& c, const V* qbase, StepRef ref, double* u,
                                           cudaStream_t s, bool moments_only = false);
 template <typename V> void launch_gather(const Cache& c, const double* z, const V* qbase, StepRef ref, V* r,
-                                         double* alpha_base, cudaStream_t s);
+                                         double* alpha_base, cudaStream_t s, const RcStream* rs = nullptr);
+// device part of the streamed cache column (RcStream), rows p0, p0+stride, ...
+__device__ __forceinline__ void stream_rc_column(const RcStream& rs, int p0, int stride) {
+    const int i = *rs.st.jdev - 1;
+    const int* fl = rs.st.flags;
+    if (i < 0 || fl[1] <= i || fl[2] || fl[3]) return;
+    const double ld = rs.st.Ld[i];
+    const double lsub = i > 0 ? rs.st.Ls[i - 1] : 0.0;
+    const double ag = sqrt(rs.st.bnorm2[0]) * rs.st.g[i];
+    const double* __restrict__ z = (i & 1) ? rs.z1 : rs.z0;
+    for (int p = p0; p < rs.m; p += stride) {
+        const double prev = i > 0 ? rs.Rc[(int64_t)(i - 1) * rs.m + p] : 0.0;
+        const double v = (z[p] - lsub * prev) / ld;
+        rs.Rc[(int64_t)i * rs.m + p] = v;
+        if (rs.mean_y) rs.a[p] += ag * v;
+    }
+}
 template <typename A, typename B> void launch_convert(const A* in, B* out, int64_t n, cudaStream_t s);
 void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s);   // from c.M
 template <typename V> void launch_permute(const Cache& c, const V* in, V* out, bool to_sorted,

@@ -150,8 +150,13 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                                                      const V* __restrict__ f0, const V* __restrict__ f1,
                                                      const V* __restrict__ f2, const double* __restrict__ z,
                                                      const V* __restrict__ qbase, StepRef ref, double sigma2,
-                                                     V* __restrict__ r, double* __restrict__ alpha_base) {
+                                                     V* __restrict__ r, double* __restrict__ alpha_base,
+                                                     RcStream rs, int ngather) {
     pdl_wait();
+    if ((int)blockIdx.x >= ngather) {          // extra CTAs: the streamed cache column
+        stream_rc_column(rs, (blockIdx.x - ngather) * blockDim.x + threadIdx.x, (gridDim.x - ngather) * blockDim.x);
+        return;
+    }
     using A = typename AccT<V, D>::type;
     constexpr int S = Slots<D>::value;
     __shared__ double red[32];
@@ -319,16 +324,22 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
 
 template <typename V>
 void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* r, double* alpha_base,
-                   cudaStream_t s) {
+                   cudaStream_t s, const RcStream* rsp) {
     const int64_t ni = c.n_items;
-    if (ni == 0) return;
     const int gi = (int)ceil_div(ni, 256);
+    RcStream rs{};
+    int extra = 0;
+    if (rsp != nullptr) {
+        rs = *rsp;
+        extra = (int)std::min<int64_t>(ceil_div(rs.m, 256), 148 * 2);
+    }
+    if (gi + extra == 0) return;
     const V* f0 = (const V*)c.frac[0];
     const V* f1 = (const V*)c.frac[1];
     const V* f2 = (const V*)c.frac[2];
 #define LOVE_GATHER(DD)                                                                                       \
-    LOVE_LAUNCH((gather_kernel<V, DD>), gi, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1, f2, z, q,  \
-                ref, c.sigma2, r, alpha_base)
+    LOVE_LAUNCH((gather_kernel<V, DD>), gi + extra, 256, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1, f2, z, \
+                q, ref, c.sigma2, r, alpha_base, rs, gi)
     switch (c.g.d) {
         case 1: LOVE_GATHER(1); break;
         case 2: LOVE_GATHER(2); break;
@@ -355,9 +366,9 @@ template void launch_convert<double, float>(const double*, float*, int64_t, cuda
 template void launch_scatter<float>(const Cache&, const float*, StepRef, double*, cudaStream_t, bool);
 template void launch_scatter<double>(const Cache&, const double*, StepRef, double*, cudaStream_t, bool);
 template void launch_gather<float>(const Cache&, const double*, const float*, StepRef, float*, double*,
-                                   cudaStream_t);
+                                   cudaStream_t, const RcStream*);
 template void launch_gather<double>(const Cache&, const double*, const double*, StepRef, double*, double*,
-                                    cudaStream_t);
+                                    cudaStream_t, const RcStream*);
 template void launch_permute<float>(const Cache&, const float*, float*, bool, cudaStream_t);
 template void launch_permute<double>(const Cache&, const double*, double*, bool, cudaStream_t);
 
