@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LOVE_ABI_VERSION 1
+#define LOVE_ABI_VERSION 2
 
 typedef struct love_cache love_cache;   /* opaque */
 
@@ -84,7 +84,14 @@ typedef struct {
     int32_t lanczos_mode;   /* LOVE_LANCZOS_AUTO (0) | LOVE_LANCZOS_TWO_PASS (1): classical Gram-Schmidt,
                                Q read twice per step | LOVE_LANCZOS_ONE_READ (2, fp32 only): the
                                lagged one-read fused pass (lanczos_fused.cu) */
+    int32_t var_blocks;     /* LOVE_VAR_BLOCKS_AUTO (0): for d <= 2 the build also stores, per cell c, the
+                               fp64 block B_c = (K_UU - Rc Rc^T) restricted to the 4^d stencil nodes of c
+                               (SURVEY 8(f) NEXT #3b), and love_predict_var returns w*^T B_c w* (the same
+                               Eq. 10 value, reassociated: 4^d(4^d+1)/2 doubles read per query instead of
+                               4^d rows of Rc, and the cancellation happens in fp64) |
+                               LOVE_VAR_BLOCKS_OFF (1): variances from the Rc rows */
 } love_opts;
+enum { LOVE_VAR_BLOCKS_AUTO = 0, LOVE_VAR_BLOCKS_OFF = 1 };
 enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ = 2 };
 
 /* Data-parallel sharding of the training points.  Every rank calls

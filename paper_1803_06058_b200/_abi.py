@@ -31,7 +31,7 @@ class love_rbf(ctypes.Structure):
 class love_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("probe", ctypes.c_int32), ("prior", ctypes.c_int32),
                 ("reorth_passes", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
-                ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32)]
+                ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32), ("var_blocks", ctypes.c_int32)]
 
 
 class love_dist(ctypes.Structure):

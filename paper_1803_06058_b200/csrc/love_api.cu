@@ -179,6 +179,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         if (o.probe != LOVE_PROBE_Y && o.probe != LOVE_PROBE_AVGCOL) throw LoveError{LOVE_ERR_ARG, "bad probe"};
         if (o.prior != LOVE_PRIOR_SKI && o.prior != LOVE_PRIOR_EXACT) throw LoveError{LOVE_ERR_ARG, "bad prior"};
         if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
+        if (o.var_blocks != LOVE_VAR_BLOCKS_AUTO && o.var_blocks != LOVE_VAR_BLOCKS_OFF)
+            throw LoveError{LOVE_ERR_ARG, "bad var_blocks"};
 
         c = new Cache();
         cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
@@ -345,6 +347,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
                                   cudaMemcpyDeviceToHost), "beta d2h");
         if (c->probe == LOVE_PROBE_AVGCOL) mean_cache_eq4(*c, s);   // a = R^T T^{-1} Q^T y
         finish_cache(*c, s);
+        c->var_blocks_off = o.var_blocks == LOVE_VAR_BLOCKS_OFF;
+        build_var_blocks(*c, s);
         if (c->k_sample_req > 0) build_sampling_cache(*c, s);
         cuda_check(cudaStreamSynchronize(s), "build sync");
         cuda_check(cudaGetLastError(), "build kernels");

@@ -137,6 +137,8 @@ struct Cache {
     float* U32 = nullptr;                // [k+1][m] every u~_i in fp32 (reorth correction)
     void* Rc = nullptr;                  // V[m * k_pad] row-major
     void* a = nullptr;                   // double[m] mean cache
+    void* vblk = nullptr;                // d <= 2: double[m][4^d(4^d+1)/2] per-cell variance blocks
+    bool var_blocks_off = false;
     void* ysort = nullptr;               // V[ldq] targets in sorted order (probe avg only)
     double* one = nullptr;               // device 1.0 (scale of un-normalised MVMs)
     double* scal = nullptr;              // backing store of LanczosState
@@ -218,6 +220,7 @@ void mean_cache_eq4(Cache& c, cudaStream_t s);  // a = Rc L^{-1} Q^T y after the
 // query.cu
 template <typename V> void launch_predict(const Cache& c, const double* Xa, const double* Xb,
                                           int64_t t, V* out, V* mean_out, cudaStream_t s);
+void build_var_blocks(Cache& c, cudaStream_t s);   // per-cell fp64 variance blocks (d <= 2)
 // sample.cu
 void build_sampling_cache(Cache& c, cudaStream_t s);
 template <typename V> void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns,

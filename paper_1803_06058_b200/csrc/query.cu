@@ -213,13 +213,179 @@ __global__ void __launch_bounds__(256) predict_kernel(GridDev g, const double* _
     }
 }
 
+// ---- per-cell variance blocks (SURVEY 8(f) NEXT #3b, d <= 2).  For a cell c with stencil
+// nodes S_c (4^d of them), B_c = K_UU|S_c - (Rc Rc^T)|S_c in fp64, stored packed upper
+// triangular (pairs a <= b in row-major order).  Eq. 10 with the SKI prior is then
+//   var(x*) = w*^T K_UU w* - ||Rc^T w*||^2 = w*^T B_c w*   for x* in cell c.
+// Rc is the fp64 column-major streamed cache (m x k_eff).
+__host__ __device__ constexpr int blk_size(int D) { return D == 1 ? 10 : 136; }
+
+__global__ void __launch_bounds__(256) var_blocks1_kernel(int m, int k_eff, const double* __restrict__ Rc,
+                                                          const double* __restrict__ c0, double s2,
+                                                          double* __restrict__ blk) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= m) return;
+    double* out = blk + (int64_t)c * 10;
+    if (c < 1 || c > m - 3) {
+#pragma unroll
+        for (int p = 0; p < 10; ++p) out[p] = 0.0;
+        return;
+    }
+    double acc[10];
+#pragma unroll
+    for (int p = 0; p < 10; ++p) acc[p] = 0.0;
+    for (int i = 0; i < k_eff; ++i) {
+        const double* col = Rc + (int64_t)i * m + (c - 1);
+        const double r0 = col[0], r1 = col[1], r2 = col[2], r3 = col[3];
+        acc[0] += r0 * r0; acc[1] += r0 * r1; acc[2] += r0 * r2; acc[3] += r0 * r3;
+        acc[4] += r1 * r1; acc[5] += r1 * r2; acc[6] += r1 * r3;
+        acc[7] += r2 * r2; acc[8] += r2 * r3;
+        acc[9] += r3 * r3;
+    }
+    int p = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = a; b < 4; ++b, ++p) out[p] = s2 * c0[b - a] - acc[p];
+}
+
+// d = 2: one warp per cell; lanes 0..15 load the 16 node values of Rc column i, every lane
+// owns pairs p = lane, lane + 32, ... of the 136 and pulls the two values by shuffles.
+__global__ void __launch_bounds__(256) var_blocks2_kernel(GridDev g, int k_eff, const double* __restrict__ Rc,
+                                                          const double* __restrict__ cols, double s2,
+                                                          double* __restrict__ blk) {
+    const int lane = threadIdx.x & 31;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int m = g.m_total;
+    if (c >= m) return;
+    const int ci = c / g.m[1], cj = c - ci * g.m[1];
+    double* out = blk + (int64_t)c * 136;
+    const bool ok = ci >= 1 && ci <= g.m[0] - 3 && cj >= 1 && cj <= g.m[1] - 3;
+    int pa[5], pb[5];
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {           // pair index -> (a, b), a <= b, row-major over a
+        int p = lane + 32 * t, a = 0;
+        while (p >= 16 - a && a < 16) { p -= 16 - a; ++a; }
+        pa[t] = a;
+        pb[t] = a + p;
+    }
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const int node = ok ? (ci - 1 + (lane >> 2)) * g.m[1] + (cj - 1 + (lane & 3)) : 0;
+    if (ok) {
+        for (int i = 0; i < k_eff; ++i) {
+            const double v = lane < 16 ? Rc[(int64_t)i * m + node] : 0.0;
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+                const double va = __shfl_sync(0xffffffffu, v, pa[t] & 15);
+                const double vb = __shfl_sync(0xffffffffu, v, pb[t] & 15);
+                acc[t] += va * vb;
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        const int p = lane + 32 * t;
+        if (p >= 136) continue;
+        const int a = pa[t], b = pb[t];
+        const double kuu = s2 * cols[abs((a >> 2) - (b >> 2))] * cols[g.m[0] + abs((a & 3) - (b & 3))];
+        out[p] = ok ? kuu - acc[t] : 0.0;
+    }
+}
+
+// variance (and mean) from the cell blocks: thread per query, fp64
+template <typename V, int D>
+__global__ void __launch_bounds__(256) predict_block_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
+                                                            int prior_mode, const double* __restrict__ blk,
+                                                            const double* __restrict__ amean,
+                                                            const double* __restrict__ Xs, int64_t t,
+                                                            V* __restrict__ out, V* __restrict__ mean_out,
+                                                            unsigned long long* __restrict__ counters) {
+    const int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (qi >= t) return;
+    const Stencil A = make_stencil<D>(g, Xs + qi * D);
+    if (!A.ok) {
+        out[qi] = (V)NAN;
+        if (mean_out) mean_out[qi] = (V)NAN;
+        atomicAdd(&counters[1], 1ull);
+        return;
+    }
+    constexpr int S = D == 1 ? 4 : 16;
+    double w[S];
+#pragma unroll
+    for (int a = 0; a < S; ++a) w[a] = D == 1 ? A.w[0][a] : A.w[0][a >> 2] * A.w[1][a & 3];
+    const int cell = D == 1 ? A.j[0] : A.j[0] * g.m[1] + A.j[1];
+    const double* __restrict__ B = blk + (int64_t)cell * blk_size(D);
+    double v = 0.0;
+    int p = 0;
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+        double row = 0.5 * w[a] * B[p++];
+#pragma unroll
+        for (int b = a + 1; b < S; ++b) row += w[b] * B[p++];
+        v += 2.0 * w[a] * row;
+    }
+    if (prior_mode == LOVE_PRIOR_EXACT) {
+        // k(x*, x*) - w^T K_UU w + w^T B w   (the exact prior of Eq. 10)
+        double pr = s2;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc += A.w[d][a] * A.w[d][b] * c4.c[d][a > b ? a - b : b - a];
+            pr *= acc;
+        }
+        v += s2 - pr;
+    }
+    out[qi] = (V)v;
+    if (v < 0.0) atomicAdd(&counters[0], 1ull);
+    if (mean_out) {
+        double mu = 0.0;
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+            const int node = D == 1 ? A.base + a : A.base + (a >> 2) * g.stride[0] + (a & 3);
+            mu += w[a] * amean[node];
+        }
+        mean_out[qi] = (V)mu;
+    }
+}
+
 }  // namespace
+
+void build_var_blocks(Cache& c, cudaStream_t s) {
+    if (c.g.d > 2 || c.var_blocks_off || c.k_eff < 1) return;
+    ProfScope ps(LOVE_PROF_FINISH, s);
+    const int m = c.g.m_total;
+    c.vblk = dalloc(c, sizeof(double) * (size_t)m * blk_size(c.g.d), s);
+    if (c.g.d == 1)
+        LOVE_LAUNCH(var_blocks1_kernel, (int)ceil_div(m, 256), 256, 0, s, m, c.k_eff, (const double*)c.Rc_col,
+                    (const double*)c.cols64, c.rbf.outputscale, (double*)c.vblk);
+    else
+        LOVE_LAUNCH(var_blocks2_kernel, (int)ceil_div((int64_t)m * 32, 256), 256, 0, s, c.g, c.k_eff,
+                    (const double*)c.Rc_col, (const double*)c.cols64, c.rbf.outputscale, (double*)c.vblk);
+}
 
 template <typename V>
 void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t t, V* out, V* mean_out,
                     cudaStream_t s) {
     if (t <= 0) return;
     ProfScope ps(LOVE_PROF_QUERY, s);
+    if (Xb == nullptr && c.vblk != nullptr) {
+        C4 c4{};
+        for (int d = 0; d < c.g.d; ++d)
+            for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
+        const int blocks = (int)ceil_div(t, 256);
+        if (c.g.d == 1)
+            LOVE_LAUNCH((predict_block_kernel<V, 1>), blocks, 256, 0, s, c.g, c4, c.rbf.outputscale,
+                        c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.prior, (const double*)c.vblk,
+                        (const double*)c.a, Xa, t, out, mean_out, c.counters);
+        else
+            LOVE_LAUNCH((predict_block_kernel<V, 2>), blocks, 256, 0, s, c.g, c4, c.rbf.outputscale,
+                        c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.prior, (const double*)c.vblk,
+                        (const double*)c.a, Xa, t, out, mean_out, c.counters);
+        return;
+    }
     constexpr int G = 8;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(t, 8 * (32 / G)), 148 * 16));
     const double* L = c.rbf.lengthscale;

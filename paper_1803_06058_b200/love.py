@@ -77,6 +77,7 @@ class LoveCache:
               lengthscale: Sequence[float], outputscale: float, sigma2: float, k: int,
               precision: str = "fp32", prior: str = "ski", k_sample: int = 0, probe: str = "y",
               reorth_passes: int = 0, breakdown_tol: float = 0.0, lanczos_mode: str = "auto",
+              var_blocks: str = "auto",
               rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
               stream=None) -> "LoveCache":
         d = len(m)
@@ -98,6 +99,7 @@ class LoveCache:
         o.breakdown_tol = float(breakdown_tol)
         o.k_sample = int(k_sample)
         o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2}[lanczos_mode]
+        o.var_blocks = {"auto": 0, "off": 1}[var_blocks]
         dist = None
         idbuf = None
         if world > 1 or nccl_id is not None:

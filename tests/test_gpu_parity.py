@@ -275,3 +275,30 @@ def test_sharded_code_path_one_rank_nccl(ci, n, m, k):
     np.testing.assert_allclose(cN.info()["alpha"], c1.info()["alpha"], rtol=1e-6)
     np.testing.assert_allclose(vN.cpu().numpy(), v1.cpu().numpy(), rtol=1e-4, atol=1e-7)
     np.testing.assert_allclose(mN.cpu().numpy(), m1.cpu().numpy(), rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("ci,n,m,k,prec", [(1, 1000, (256,), 50, "fp64"), (2, 60_001, (6000,), 40, "fp32"),
+                                           (3, 30_007, (48, 48), 40, "fp32"), (5, 20_011, (2000,), 30, "fp32")])
+@pytest.mark.parametrize("prior", ["ski", "exact"])
+def test_var_blocks_vs_rc_rows_and_oracle(ci, n, m, k, prec, prior):
+    """SURVEY 8(f) NEXT #3b: per-cell fp64 blocks B_c = (K_UU - Rc Rc^T)|stencil give the same
+    Eq. 10 variances as the Rc-row path (reassociated), and both meet the oracle bound."""
+    p = scaled_config(ci, n=n, m=m, k=k, t=4001, precision=prec)
+    inp = make_inputs(p)
+    cb = _build(p, inp, prior=prior)
+    cr = _build(p, inp, prior=prior, var_blocks="off")
+    vb, mb = cb.predict_var(inp.Xs, return_mean=True)
+    vr, mr = cr.predict_var(inp.Xs, return_mean=True)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    ov = O.predict_var(model, oc, inp.Xs, prior=prior)
+    prior_v = _prior(model, inp.Xs)
+    for v in (vb, vr):
+        _assert_var(v.cpu().numpy().astype(np.float64), ov, prior_v, fp64=prec == "fp64")
+    # means: same formula on both paths; the two builds differ only by fp64 atomic order
+    np.testing.assert_allclose(mb.cpu().numpy(), mr.cpu().numpy(), rtol=1e-5, atol=1e-6)
+    # the block path does the cancellation in fp64: in fp32 mode it is at least as close to
+    # the oracle as the row path (median over points)
+    eb = np.abs(vb.cpu().numpy().astype(np.float64) - ov)
+    er = np.abs(vr.cpu().numpy().astype(np.float64) - ov)
+    assert np.median(eb) <= np.median(er) * 1.5 + 1e-15
