@@ -199,6 +199,17 @@ inline int grid_for(int64_t n, int threads) {
 
 }  // namespace
 
+void counting_sort_keys(const int* keys, int64_t n, int nbins, int* start, int* perm, cudaStream_t s) {
+    int* count = nullptr;
+    cuda_check(cudaMallocAsync((void**)&count, sizeof(int) * (nbins + 1), s), "sort alloc");
+    cuda_check(cudaMemsetAsync(count, 0, sizeof(int) * (nbins + 1), s), "sort memset");
+    if (n > 0) LOVE_LAUNCH(histogram_kernel, grid_for(n, 256), 256, 0, s, keys, n, count);
+    exclusive_scan(count, nbins, start, s);
+    cuda_check(cudaMemsetAsync(count, 0, sizeof(int) * (nbins + 1), s), "sort memset");
+    if (n > 0) LOVE_LAUNCH(place_kernel, grid_for(n, 256), 256, 0, s, keys, n, start, count, perm);
+    cuda_check(cudaFreeAsync(count, s), "sort free");
+}
+
 void launch_interp_points(const Cache& c, const double* X, int64_t n, int* cell, double* frac64,
                           int* range_flag, cudaStream_t s) {
     if (n == 0) return;

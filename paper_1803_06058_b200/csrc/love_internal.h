@@ -179,6 +179,9 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
                           int64_t n, void* b_out, cudaStream_t s);   // fills perm, frac, cells
 void launch_build_items(Cache& c, cudaStream_t s);                 // after n_items known
 int64_t count_items_host(Cache& c, cudaStream_t s);                 // syncs
+// keys in [0, nbins): start[nbins+1] = exclusive scan of the histogram, perm[start[k] ..] = the
+// indices with key k (order within a key unspecified)
+void counting_sort_keys(const int* keys, int64_t n, int nbins, int* start, int* perm, cudaStream_t s);
 // ski.cu
 // d = 1 (non-fused caches): per-cell moments into c.Mc, then u unless moments_only (the
 // K_UU MVM then reads the moments itself, launch_kuu(..., Mc))

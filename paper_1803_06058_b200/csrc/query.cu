@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "love_internal.h"
 
@@ -353,6 +354,144 @@ __global__ void __launch_bounds__(256) predict_block_kernel(GridDev g, C4 c4, do
 
 }  // namespace
 
+// ---- d = 3 variance queries grouped by cell (SURVEY 8(f) NEXT #3a): the queries are
+// counting-sorted by cell, a CTA stages the 64 stencil rows of Rc of one cell in shared
+// memory once and every query of that cell reads them from there.
+__global__ void query_cell3_kernel(GridDev g, const double* __restrict__ Xs, int64_t t, int* __restrict__ key) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < t; q += (int64_t)gridDim.x * blockDim.x) {
+        int cell = 0;
+        bool ok = true;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double jf = floor((Xs[q * 3 + d] - g.lo[d]) / g.h[d]);
+            ok = ok && jf >= 1.0 && jf <= (double)(g.m[d] - 3);       // reading A4
+            cell += (ok ? (int)jf : 0) * g.stride[d];
+        }
+        key[q] = ok ? cell : g.m_total;
+    }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
+                                                              double l2, int prior_mode, const V* __restrict__ Rc,
+                                                              int k_pad, const double* __restrict__ amean,
+                                                              const double* __restrict__ Xs,
+                                                              const int* __restrict__ qstart,
+                                                              const int* __restrict__ perm, int cells_per_cta,
+                                                              V* __restrict__ out, V* __restrict__ mean_out,
+                                                              unsigned long long* __restrict__ counters) {
+    constexpr int W = QV<V>::W;
+    using VT = typename QV<V>::T;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    V* rows = reinterpret_cast<V*>(smraw);                       // [64][k_pad]
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nch = k_pad / W;
+    const int m = g.m_total;
+    const int c_begin = blockIdx.x * cells_per_cta;
+    const int c_end = min(m, c_begin + cells_per_cta);
+    for (int c = c_begin; c < c_end; ++c) {
+        const int p0 = qstart[c], p1 = qstart[c + 1];
+        if (p0 == p1) continue;
+        const int base = c - g.stride[0] - g.stride[1] - 1;      // node of stencil offset (0, 0, 0)
+        __syncthreads();                                        // previous cell's rows are free
+        for (int e = threadIdx.x; e < 64 * nch; e += blockDim.x) {
+            const int l = e / nch, ch = e - l * nch;
+            const int node = base + (l >> 4) * g.stride[0] + ((l >> 2) & 3) * g.stride[1] + (l & 3);
+            *reinterpret_cast<VT*>(rows + l * k_pad + ch * W) =
+                __ldg(reinterpret_cast<const VT*>(Rc + (int64_t)node * k_pad + ch * W));
+        }
+        __syncthreads();
+        for (int pos = p0 + wid; pos < p1; pos += nw) {
+            const int q = perm[pos];
+            const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
+            double dot = 0.0;
+            for (int ch = lane; ch < nch; ch += 32) {
+                double acc[W];
+#pragma unroll
+                for (int e = 0; e < W; ++e) acc[e] = 0.0;
+                // separable: r = sum_a w0_a sum_b w1_b sum_c w2_c Rc[row(a,b,c)], innermost first
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    V ra[W];
+#pragma unroll
+                    for (int e = 0; e < W; ++e) ra[e] = V(0);
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        // the 16-term (b, c) sums in the storage type V (fp32 rows in LOVE_FP32:
+                        // a few ulp of fp32 on top of what the fp32 storage of Rc already carries,
+                        // without converting every row element to fp64); the a-sum and the
+                        // norm are fp64
+                        V rb[W];
+#pragma unroll
+                        for (int e = 0; e < W; ++e) rb[e] = V(0);
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) {
+                            const VT v = *reinterpret_cast<const VT*>(rows + (a * 16 + b * 4 + cc) * k_pad + ch * W);
+                            const V w = (V)A.w[2][cc];
+                            if constexpr (W == 4) {
+                                rb[0] += w * v.x; rb[1] += w * v.y; rb[2] += w * v.z; rb[3] += w * v.w;
+                            } else {
+                                rb[0] += w * v.x; rb[1] += w * v.y;
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < W; ++e) ra[e] += (V)A.w[1][b] * rb[e];
+                    }
+#pragma unroll
+                    for (int e = 0; e < W; ++e) acc[e] += A.w[0][a] * (double)ra[e];
+                }
+#pragma unroll
+                for (int e = 0; e < W; ++e) dot += acc[e] * acc[e];
+            }
+            // mean: each lane takes 2 of the 64 nodes
+            double mu = 0.0;
+            if (mean_out) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int l = lane + 32 * h;
+                    const double w = pick4(A.w[0], l >> 4) * pick4(A.w[1], (l >> 2) & 3) * pick4(A.w[2], l & 3);
+                    mu += w * amean[base + (l >> 4) * g.stride[0] + ((l >> 2) & 3) * g.stride[1] + (l & 3)];
+                }
+                mu = warp_sum(mu);
+            }
+            dot = warp_sum(dot);
+            if (lane != 0) continue;
+            double prior;
+            if (prior_mode == LOVE_PRIOR_EXACT) {
+                prior = s2;
+            } else {
+                prior = s2;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc += A.w[d][a] * A.w[d][b] * c4.c[d][a > b ? a - b : b - a];
+                    prior *= acc;
+                }
+            }
+            const double v = prior - dot;
+            out[q] = (V)v;
+            if (v < 0.0) atomicAdd(&counters[0], 1ull);
+            if (mean_out) mean_out[q] = (V)mu;
+        }
+    }
+}
+
+template <typename V>
+__global__ void nan_fill_kernel(const int* __restrict__ qstart, int m, const int* __restrict__ perm,
+                                V* __restrict__ out, V* __restrict__ mean_out,
+                                unsigned long long* __restrict__ counters) {
+    const int p0 = qstart[m], p1 = qstart[m + 1];
+    for (int pos = p0 + blockIdx.x * blockDim.x + threadIdx.x; pos < p1; pos += gridDim.x * blockDim.x) {
+        const int q = perm[pos];
+        out[q] = (V)NAN;
+        if (mean_out) mean_out[q] = (V)NAN;
+        atomicAdd(&counters[1], 1ull);
+    }
+}
+
 void build_var_blocks(Cache& c, cudaStream_t s) {
     if (c.g.d > 2 || c.var_blocks_off || c.k_eff < 1) return;
     ProfScope ps(LOVE_PROF_FINISH, s);
@@ -384,6 +523,30 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
             LOVE_LAUNCH((predict_block_kernel<V, 2>), blocks, 256, 0, s, c.g, c4, c.rbf.outputscale,
                         c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.prior, (const double*)c.vblk,
                         (const double*)c.a, Xa, t, out, mean_out, c.counters);
+        return;
+    }
+    if (Xb == nullptr && c.g.d == 3 && t >= 65536 && std::getenv("LOVE_NO_SORTED_QUERIES") == nullptr) {
+        const int m = c.g.m_total;
+        int *key = nullptr, *perm = nullptr, *qstart = nullptr;
+        cuda_check(cudaMallocAsync((void**)&key, sizeof(int) * t, s), "query sort alloc");
+        cuda_check(cudaMallocAsync((void**)&perm, sizeof(int) * t, s), "query sort alloc");
+        cuda_check(cudaMallocAsync((void**)&qstart, sizeof(int) * (m + 2), s), "query sort alloc");
+        LOVE_LAUNCH(query_cell3_kernel, (int)std::min<int64_t>(ceil_div(t, 256), 148 * 16), 256, 0, s, c.g, Xa, t,
+                    key);
+        counting_sort_keys(key, t, m + 1, qstart, perm, s);
+        C4 c4{};
+        for (int d = 0; d < 3; ++d)
+            for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
+        const int cpc = 8;
+        const size_t sm = sizeof(V) * 64 * (size_t)c.k_pad;
+        ensure_smem((const void*)predict_sorted3_kernel<V>, sm);
+        LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm, s, c.g, c4, c.rbf.outputscale,
+                    c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
+                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters);
+        LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, qstart, m, perm, out, mean_out, c.counters);
+        cuda_check(cudaFreeAsync(key, s), "query sort free");
+        cuda_check(cudaFreeAsync(perm, s), "query sort free");
+        cuda_check(cudaFreeAsync(qstart, s), "query sort free");
         return;
     }
     constexpr int G = 8;

@@ -302,3 +302,28 @@ def test_var_blocks_vs_rc_rows_and_oracle(ci, n, m, k, prec, prior):
     eb = np.abs(vb.cpu().numpy().astype(np.float64) - ov)
     er = np.abs(vr.cpu().numpy().astype(np.float64) - ov)
     assert np.median(eb) <= np.median(er) * 1.5 + 1e-15
+
+
+def test_sorted_queries_d3_match_unsorted_and_oracle(monkeypatch):
+    """SURVEY 8(f) NEXT #3a: d = 3 variance queries counting-sorted by cell (64 Rc rows staged
+    once per cell) equal the per-query path and the oracle; out-of-range points stay NaN."""
+    p = scaled_config(4, n=60_013, m=(24, 24, 24), k=40, t=70_001)
+    inp = make_inputs(p)
+    Xs = inp.Xs.copy()
+    Xs[17] = [9.0, 0.0, 0.0]                  # outside the grid -> NaN + counter
+    Xs[40_000] = [0.0, -9.0, 0.0]
+    c = _build(p, inp)
+    vs, ms = c.predict_var(Xs, return_mean=True)
+    monkeypatch.setenv("LOVE_NO_SORTED_QUERIES", "1")
+    vu, mu = c.predict_var(Xs, return_mean=True)
+    vs, ms, vu, mu = (x.cpu().numpy().astype(np.float64) for x in (vs, ms, vu, mu))
+    bad = np.isnan(vu)
+    assert bad.sum() == 2 and np.array_equal(np.isnan(vs), bad)
+    np.testing.assert_allclose(vs[~bad], vu[~bad], rtol=1e-5, atol=1e-7)
+    np.testing.assert_allclose(ms[~bad], mu[~bad], rtol=1e-5, atol=1e-7)
+    assert c.info()["n_out_of_range"] == 4
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    sel = np.setdiff1d(np.arange(0, p.t, 13), [17, 40_000])
+    ov = O.predict_var(model, oc, Xs[sel])
+    _assert_var(vs[sel], ov, _prior(model, Xs[sel]), fp64=False)
