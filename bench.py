@@ -76,11 +76,18 @@ def build_bytes(p, n_local: int) -> int:
     return tot + 2 * p.m_total * p.k * sv
 
 
-def query_bytes(p, k_pad: int) -> int:
-    """Algorithmic bytes of one variance query: the 4^d gathered rows of Rc
-    (k_pad values each), the fp64 query point and the result."""
+def query_bytes(p, k_pad: int):
+    """Algorithmic bytes of one variance query and the model used.
+    d <= 2 (per-cell variance blocks, SURVEY §8(f) #3b): the fp64 query point, the packed fp64
+    block of its cell (4^d (4^d + 1) / 2 values) and the result.
+    d = 3: SURVEY §8(d)'s gathered-row model, the 4^d rows of Rc (k_pad values each) + point +
+    result (the cell-sorted kernel stages those rows once per cell, so this is an upper bound
+    on what it reads)."""
     sv = 8 if p.precision == "fp64" else 4
-    return 4 ** p.d * k_pad * sv + 8 * p.d + sv
+    if p.d <= 2:
+        nb = 4 ** p.d
+        return 8 * p.d + 8 * nb * (nb + 1) // 2 + sv, "cell-block (x*, fp64 block of its cell, result)"
+    return 4 ** p.d * k_pad * sv + 8 * p.d + sv, "gathered rows (SURVEY 8(d) B_query)"
 
 
 class ClockSampler:
@@ -379,11 +386,12 @@ def main():
     b_ach = bb / (float(np.mean(build_ms)) / 1e3) / 1e9
     build_rf = {"bound": "hbm", "algorithmic_bytes": bb, "achieved": b_ach, "peak": peak, "unit": "GB/s",
                 "frac": b_ach / peak, "model": "SURVEY 8(d) B_build (one CGS pass = 2 reads of Q_j per step)"}
-    qb = query_bytes(p, k_pad) * p.t
+    bq, qmodel = query_bytes(p, k_pad)
+    qb = bq * p.t
     q_ach = qb / (float(np.mean(query_ms)) / 1e3) / 1e9
-    query_rf = {"bound": "hbm (gathered-row model; Rc is L2-resident at these sizes)", "algorithmic_bytes": qb,
+    query_rf = {"bound": "hbm", "model": qmodel, "algorithmic_bytes": qb,
                 "achieved": q_ach, "peak": peak, "unit": "GB/s", "frac": q_ach / peak,
-                "bytes_per_query": query_bytes(p, k_pad)}
+                "bytes_per_query": bq}
     sampling = None
     if p.k_sample:
         smean = float(np.mean(sample_ms))
