@@ -128,7 +128,7 @@ typedef struct {
  *   grid, rbf, opts : HOST structs (opts may be NULL => defaults).
  *   sigma2          : observation noise variance sigma^2 > 0.
  *   X               : n_local x d fp64, row-major.  y : n_local fp64.
- *   k               : Lanczos steps, k >= 1 (k > n_global is clamped to n_global).
+ *   k               : Lanczos steps, 1 <= k <= 2048 (k > n_global is clamped to n_global).
  *   dist            : HOST struct or NULL.
  *   out             : HOST pointer receiving the new cache.
  * Runs: interpolation indices/weights, cell sort, K_UU setup, k steps

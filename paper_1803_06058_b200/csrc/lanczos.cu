@@ -580,6 +580,8 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.smd = sizeof(double) * round_up((pl.k + 1) * 8, 2) + sizeof(V) * pl.tile_rows;
     pl.smu = sizeof(double) * (pl.k + 1);
     ensure_smem((const void*)reorth_dots_kernel<V>, pl.smd);
+    ensure_smem((const void*)reorth_dots_sweep_kernel<V, 1>, sizeof(double) * 8 * (pl.k + 1));
+    ensure_smem((const void*)reorth_dots_sweep_kernel<V, 2>, sizeof(double) * 8 * (pl.k + 1));
     ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
     const LanczosState& st = c.st;
     {

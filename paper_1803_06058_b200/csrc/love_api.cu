@@ -136,6 +136,8 @@ void validate_build(const love_grid* grid, const love_rbf* rbf, double sigma2, c
     if (!(rbf->outputscale > 0.0)) throw LoveError{LOVE_ERR_ARG, "outputscale must be > 0"};
     if (!(sigma2 > 0.0)) throw LoveError{LOVE_ERR_ARG, "sigma^2 must be > 0"};
     if (k < 1) throw LoveError{LOVE_ERR_ARG, "k must be >= 1"};
+    // per-step shared memory holds 8 (k+1) fp64 partial dots (reorthogonalisation)
+    if (k > 2048) throw LoveError{LOVE_ERR_ARG, "k must be <= 2048"};
     if (n_local < 0 || n_local >= (int64_t(1) << 31)) throw LoveError{LOVE_ERR_ARG, "bad n_local"};
     if (n_local > 0 && (!X || !y)) throw LoveError{LOVE_ERR_ARG, "NULL X/y"};
 }

@@ -327,3 +327,11 @@ def test_sorted_queries_d3_match_unsorted_and_oracle(monkeypatch):
     sel = np.setdiff1d(np.arange(0, p.t, 13), [17, 40_000])
     ov = O.predict_var(model, oc, Xs[sel])
     _assert_var(vs[sel], ov, _prior(model, Xs[sel]), fp64=False)
+
+
+def test_k_limit_is_an_argument_error():
+    _, LoveError = _love()
+    p, inp = tiny_problem("1d_n40")
+    with pytest.raises(LoveError) as ei:
+        _build(p, inp, k=4096)
+    assert "k must be" in str(ei.value)
