@@ -23,6 +23,10 @@ Pins (tests/test_oracle_pins.py, all `-m "not gpu"`):
   mean cache ............................... == dense SKI GP mean; == CG solve      -> pinned
   sampling_cache / draw_samples ............ SS^T == K_UU - R^T R' at full rank; Monte-Carlo
                                               moments                                -> pinned
+  additive models (Eq. 16) ....... block-diagonal K_UU == sum of 1-D kernels on
+                                              node pairs; stacked W adjointness; LOVE ==
+                                              dense SKI GP of the additive kernel at full
+                                              Krylov dimension                       -> pinned
 """
 from __future__ import annotations
 
@@ -41,6 +45,7 @@ __all__ = [
     "LoveCache", "love_precompute", "prior_ski", "prior_exact", "predict_mean",
     "predict_var", "predict_covar", "sampling_cache", "draw_samples", "SamplingCache",
     "dense_ski_gp", "cg_solve", "smae",
+    "build_model_additive", "interp_additive", "model_interp", "model_kuu_matvec", "model_kuu_dense",
 ]
 
 
@@ -218,13 +223,20 @@ class SKIModel:
     outputscale: float
     lengthscale: Tuple[float, ...]
     sigma2: float
-    idx: np.ndarray           # (n, 4^d) training stencils
+    idx: np.ndarray           # (n, 4^d) training stencils  (additive: (n, 4d))
     w: np.ndarray             # (n, 4^d) training weights
     y: np.ndarray             # (n,)
+    kind: str = "product"     # "product" (Kronecker grid) | "additive" (Eq. 16)
+    outputscales: Tuple[float, ...] = ()   # additive: per-component s_e^2
 
     @property
     def m_total(self) -> int:
-        return int(np.prod(self.m))
+        return int(np.sum(self.m)) if self.kind == "additive" else int(np.prod(self.m))
+
+    @property
+    def offsets(self) -> np.ndarray:
+        """additive: first node of component e in the stacked inducing set"""
+        return np.concatenate([[0], np.cumsum(self.m)[:-1]]).astype(np.int64)
 
     @property
     def n(self) -> int:
@@ -237,6 +249,72 @@ def build_model(X, y, m, lo, h, lengthscale, outputscale, sigma2) -> SKIModel:
     idx, w = interp(X, m, lo, h)
     return SKIModel(m, tuple(lo), tuple(h), cols, float(outputscale), tuple(lengthscale),
                     float(sigma2), idx, w, np.asarray(y, dtype=np.float64))
+
+
+# --------------------------------------------------------------------------------------
+# Additive compositions (Eq. 16): k~(x, x') = sum_e w^(e)_x^T K^(e)_UU w^(e)_x',
+# i.e. stacked interpolation vectors [w^(1); ..; w^(d)] (4 nonzeros per component, 4d per
+# point) and a block-diagonal K_UU = diag(K^(1), .., K^(d)) of 1-D Toeplitz blocks.
+# --------------------------------------------------------------------------------------
+def interp_additive(X: np.ndarray, m: Sequence[int], lo: Sequence[float], h: Sequence[float]
+                    ) -> Tuple[np.ndarray, np.ndarray]:
+    """Stacked block interpolation vectors of Eq. 16: component e contributes its 1-D cubic
+    stencil on its own grid, at node offset sum_{e' < e} m_e'.  Returns (n, 4d)."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim == 1:
+        X = X[:, None]
+    off = 0
+    idxs, ws = [], []
+    for e in range(X.shape[1]):
+        i_e, w_e = interp_1d(X[:, e], lo[e], h[e], m[e])
+        idxs.append(i_e + off)
+        ws.append(w_e)
+        off += int(m[e])
+    return np.concatenate(idxs, axis=1), np.concatenate(ws, axis=1)
+
+
+def build_model_additive(X, y, m, lo, h, lengthscale, outputscales, sigma2) -> SKIModel:
+    """SKI model of the additive kernel sum_e s_e^2 exp(-(x_e - x'_e)^2 / (2 l_e^2)) (Eq. 16;
+    RBF components as in the paper's Styblinski-Tang model)."""
+    m = tuple(int(v) for v in m)
+    cols = [rbf_column(m[i], h[i], lengthscale[i]) for i in range(len(m))]
+    idx, w = interp_additive(X, m, lo, h)
+    return SKIModel(m, tuple(lo), tuple(h), cols, 1.0, tuple(lengthscale), float(sigma2), idx, w,
+                    np.asarray(y, dtype=np.float64), kind="additive",
+                    outputscales=tuple(float(v) for v in outputscales))
+
+
+def model_interp(model: SKIModel, X: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Interpolation vectors of test points for the model's structure."""
+    if model.kind == "additive":
+        return interp_additive(X, model.m, model.lo, model.h)
+    return interp(X, model.m, model.lo, model.h)
+
+
+def model_kuu_matvec(model: SKIModel, u: np.ndarray) -> np.ndarray:
+    """K_UU u: Kronecker of Toeplitz, or the block-diagonal K_UU of Eq. 16 (each block
+    s_e^2 T(c_e) applied to its slice)."""
+    if model.kind != "additive":
+        return kuu_matvec(model.cols, model.outputscale, u)
+    out = np.zeros_like(u, dtype=np.float64)
+    off = 0
+    for e, c in enumerate(model.cols):
+        sl = slice(off, off + len(c))
+        out[sl] = model.outputscales[e] * _toeplitz_apply(c, u[sl].reshape(len(c), -1)).reshape(u[sl].shape)
+        off += len(c)
+    return out
+
+
+def model_kuu_dense(model: SKIModel) -> np.ndarray:
+    if model.kind != "additive":
+        return kuu_dense(model.cols, model.outputscale)
+    M = model.m_total
+    K = np.zeros((M, M))
+    off = 0
+    for e, c in enumerate(model.cols):
+        K[off:off + len(c), off:off + len(c)] = model.outputscales[e] * toeplitz_dense(c)
+        off += len(c)
+    return K
 
 
 def W_apply(idx: np.ndarray, w: np.ndarray, v: np.ndarray, m_total: int) -> np.ndarray:
@@ -252,7 +330,7 @@ def WT_apply(idx: np.ndarray, w: np.ndarray, z: np.ndarray) -> np.ndarray:
 def ski_mvm(model: SKIModel, v: np.ndarray) -> np.ndarray:
     """(W_X^T K_UU W_X + sigma^2 I) v  (Eq. 5 P:180 plus noise, mvm_K_XX of Alg. 1)."""
     u = W_apply(model.idx, model.w, v, model.m_total)
-    z = kuu_matvec(model.cols, model.outputscale, u)
+    z = model_kuu_matvec(model, u)
     return WT_apply(model.idx, model.w, z) + model.sigma2 * v
 
 
@@ -377,7 +455,7 @@ def love_precompute(model: SKIModel, k: int, probe: str = "y", tau: float = 1e-1
         b = model.y
     elif probe == "avg":
         ones = np.ones(model.m_total)
-        b = WT_apply(model.idx, model.w, kuu_matvec(model.cols, model.outputscale, ones))
+        b = WT_apply(model.idx, model.w, model_kuu_matvec(model, ones))
         b = b / model.m_total
     else:
         raise ValueError(probe)
@@ -387,7 +465,7 @@ def love_precompute(model: SKIModel, k: int, probe: str = "y", tau: float = 1e-1
     R = np.zeros((kk, model.m_total))
     for i in range(kk):                      # mvm_K_UX(q_i) = K_UU (W_X q_i)
         u = W_apply(model.idx, model.w, lz.Q[:, i], model.m_total)
-        R[i] = kuu_matvec(model.cols, model.outputscale, u)
+        R[i] = model_kuu_matvec(model, u)
     Rp = tridiag_solve(Ld, Ls, R)
     if probe == "y":
         e1 = np.zeros(kk)
@@ -404,6 +482,21 @@ def prior_ski(model: SKIModel, idx_i, w_i, idx_j, w_j) -> np.ndarray:
     K_UU[p,q] = s^2 prod_d c_d[|p_d - q_d|]."""
     t = idx_i.shape[0]
     out = np.zeros(t)
+    if model.kind == "additive":
+        # K_UU[p, q] = s_e^2 c_e[|p - q|] when p, q are nodes of the same component e, else 0
+        off = model.offsets
+        comp_i = np.searchsorted(off, idx_i, side="right") - 1
+        comp_j = np.searchsorted(off, idx_j, side="right") - 1
+        for a in range(idx_i.shape[1]):
+            for b in range(idx_j.shape[1]):
+                same = comp_i[:, a] == comp_j[:, b]
+                e = comp_i[:, a]
+                kv = np.zeros(t)
+                for ee in np.unique(e[same]):
+                    sel = same & (e == ee)
+                    kv[sel] = model.outputscales[ee] * model.cols[ee][np.abs(idx_i[sel, a] - idx_j[sel, b])]
+                out += w_i[:, a] * w_j[:, b] * kv
+        return out
     coords_i = np.stack(np.unravel_index(idx_i, model.m), axis=-1)   # (t, 4^d, d)
     coords_j = np.stack(np.unravel_index(idx_j, model.m), axis=-1)
     for a in range(idx_i.shape[1]):
@@ -423,6 +516,11 @@ def _as2d(X: np.ndarray) -> np.ndarray:
 def prior_exact(model: SKIModel, Xi: np.ndarray, Xj: np.ndarray) -> np.ndarray:
     """Exact prior k(x_i, x_j) = s^2 prod_d exp(-(x_id - x_jd)^2 / (2 l_d^2)) (Eq. 10)."""
     Xi, Xj = _as2d(Xi), _as2d(Xj)
+    if model.kind == "additive":          # sum_e s_e^2 exp(-(x_e - x'_e)^2 / (2 l_e^2))  (Eq. 16)
+        out = np.zeros(Xi.shape[0])
+        for e, l in enumerate(model.lengthscale):
+            out += model.outputscales[e] * np.exp(-0.5 * (Xi[:, e] - Xj[:, e]) ** 2 / (l * l))
+        return out
     r2 = np.zeros(Xi.shape[0])
     for d, l in enumerate(model.lengthscale):
         r2 += (Xi[:, d] - Xj[:, d]) ** 2 / (l * l)
@@ -431,7 +529,7 @@ def prior_exact(model: SKIModel, Xi: np.ndarray, Xj: np.ndarray) -> np.ndarray:
 
 def predict_mean(model: SKIModel, cache: LoveCache, Xs: np.ndarray) -> np.ndarray:
     """mu(x*) = w_{x*}^T a (Eq. 6; zero prior mean, reading A19)."""
-    idx, w = interp(Xs, model.m, model.lo, model.h)
+    idx, w = model_interp(model, Xs)
     return (w * cache.a[idx]).sum(1)
 
 
@@ -444,8 +542,8 @@ def predict_covar(model: SKIModel, cache: LoveCache, Xa: np.ndarray, Xb: np.ndar
     out = np.zeros(Xa.shape[0])
     for s in range(0, Xa.shape[0], 16384):                   # chunked only to bound memory
         e = min(s + 16384, Xa.shape[0])
-        ia, wa = interp(Xa[s:e], model.m, model.lo, model.h)
-        ib, wb = interp(Xb[s:e], model.m, model.lo, model.h)
+        ia, wa = model_interp(model, Xa[s:e])
+        ib, wb = model_interp(model, Xb[s:e])
         u = np.einsum("tl,ktl->tk", wa, cache.R[:, ia])       # R w_i   (t, k)
         v = np.einsum("tl,ktl->tk", wb, cache.Rp[:, ib])      # R' w_j  (t, k)
         if prior == "ski":
@@ -482,7 +580,7 @@ def sampling_cache(model: SKIModel, cache: LoveCache, k_sample: int, tau: float 
     S = Q' T'^{1/2} (P:357 with L_{T_k} read as the root of T'_k, reading A18), so that
     S S^T = Q' T' Q'^T (Eq. 14-15)."""
     def mvm(v):
-        return kuu_matvec(model.cols, model.outputscale, v) - cache.R.T @ (cache.Rp @ v)
+        return model_kuu_matvec(model, v) - cache.R.T @ (cache.Rp @ v)
 
     b = mvm(np.ones(model.m_total))
     lz = lanczos(mvm, b, k_sample, tau=tau, reorth_passes=2)
@@ -495,7 +593,7 @@ def draw_samples(model: SKIModel, cache: LoveCache, scache: SamplingCache, Xs: n
                  zeta: np.ndarray) -> np.ndarray:
     """Posterior samples mu(X*) + W_{X*}^T S zeta (Eq. 11).
     zeta: (k'_eff, s) standard normals (columns = samples).  Returns (t, s)."""
-    idx, w = interp(Xs, model.m, model.lo, model.h)
+    idx, w = model_interp(model, Xs)
     mu = (w * cache.a[idx]).sum(1)
     G = np.einsum("tl,tlk->tk", w, scache.S[idx])          # W_{X*}^T S   (t, k')
     return mu[:, None] + G @ zeta
@@ -509,11 +607,11 @@ def dense_ski_gp(model: SKIModel, Xs: np.ndarray) -> Tuple[np.ndarray, np.ndarra
     k~(x, x') = w_x^T K_UU w_x' (Eq. 5), by dense Cholesky of
     K_hat = W_X^T K_UU W_X + sigma^2 I:
         mu = k~_{X x*}^T K_hat^{-1} y,  var = w*^T K_UU w* - k~^T K_hat^{-1} k~  (Eq. 7)."""
-    Kuu = kuu_dense(model.cols, model.outputscale)
+    Kuu = model_kuu_dense(model)
     W = dense_W(model.idx, model.w, model.m_total)          # m x n
     Khat = W.T @ Kuu @ W + model.sigma2 * np.eye(model.n)
     L = np.linalg.cholesky(Khat)
-    ids, ws = interp(Xs, model.m, model.lo, model.h)
+    ids, ws = model_interp(model, Xs)
     Ws = dense_W(ids, ws, model.m_total)                    # m x t
     Kxs = W.T @ Kuu @ Ws                                    # n x t
     alpha = np.linalg.solve(L.T, np.linalg.solve(L, model.y))

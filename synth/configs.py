@@ -29,6 +29,7 @@ class Problem:
     k_sample: int = 0            # k' of the sampling cache (config 5)
     s: int = 0                   # samples drawn (config 5)
     seed: int = 0
+    kind: str = "product"        # "product" (Kronecker grid) | "additive" (Eq. 16)
 
     @property
     def h(self) -> Tuple[float, ...]:
@@ -36,6 +37,8 @@ class Problem:
 
     @property
     def m_total(self) -> int:
+        if self.kind == "additive":
+            return sum(self.m)
         out = 1
         for mm in self.m:
             out *= mm
@@ -53,6 +56,12 @@ CONFIGS = {
                (0.5, 0.5, 0.5), 1.0, 0.1 ** 2, 100, 4_000_000, "fp32", "rsinr3d", 0.1),
     5: Problem("cfg5_sampling", 1, 100_000, (10_000,), (-0.05,), (1.05,), (0.05,), 1.0, 0.01,
                100, 10_000, "fp32", "sin6pi", 0.1, k_sample=100, s=1000),
+    # SURVEY 8(f) NEXT #2 (not a BASELINE config): additive composition of 10 1-D RBF kernels
+    # with m = 100 inducing points each, the paper's Styblinski-Tang model;
+    # x ~ U(-5, 5)^10, grid [-5.5, 5.5] per axis (reading A5), y a scaled Styblinski-Tang
+    # function + N(0, 0.1^2).
+    6: Problem("cfg6_additive10", 10, 100_000, (100,) * 10, (-5.5,) * 10, (5.5,) * 10, (1.0,) * 10, 1.0, 0.01,
+               100, 100_000, "fp32", "styblinski_tang", 0.1, kind="additive"),
 }
 
 

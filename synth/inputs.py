@@ -45,6 +45,11 @@ def _draw(p: Problem, rng: np.random.Generator, n: int, t: int) -> Inputs:
         y = r * np.sin(r) + rng.normal(0.0, p.noise_sd, n)
         Xs = np.clip(rng.normal(0.0, 1.0, (t, 3)), -3.0, 3.0)
         return Inputs(X, y, Xs)
+    if p.data == "styblinski_tang":   # config 6 (additive): 0.5 sum_i (x_i^4 - 16 x_i^2 + 5 x_i), / 100
+        X = rng.uniform(-5.0, 5.0, (n, p.d))
+        y = 0.5 * (X ** 4 - 16.0 * X ** 2 + 5.0 * X).sum(1) / 100.0 + rng.normal(0.0, p.noise_sd, n)
+        Xs = rng.uniform(-5.0, 5.0, (t, p.d))
+        return Inputs(X, y, Xs)
     raise ValueError(f"unknown data recipe {p.data}")
 
 
@@ -79,6 +84,10 @@ def tiny_problem(kind: str, seed: int = 0):
         p = _dc.replace(CONFIGS[4], name="tiny_3d", n=500, m=(8, 8, 8), lo=(-4.5,) * 3,
                         hi=(4.5,) * 3, t=50, k=600, sigma2=0.01, lengthscale=(1.0, 1.0, 1.0),
                         precision="fp64")
+    elif kind == "additive3":
+        # 3 additive components, 15 nodes per axis on [-7, 7] (x in [-5, 5] stays 2 cells inside)
+        p = _dc.replace(CONFIGS[6], name="tiny_additive3", d=3, n=200, m=(15,) * 3, lo=(-7.0,) * 3,
+                        hi=(7.0,) * 3, lengthscale=(1.5, 1.0, 2.0), t=50, k=400, precision="fp64")
     else:
         raise ValueError(kind)
     return p, make_inputs(p, seed)

@@ -380,3 +380,59 @@ def test_sampling_monte_carlo_moments():
 def test_smae_definition():
     y = np.array([1.0, 3.0])                                # population variance 1
     assert O.smae(np.array([0.5, 0.5]), np.array([0.0, 1.0]), y) == pytest.approx(0.5)
+
+
+# ----------------------------------------------------------------- additive kernels (Eq. 16)
+def _additive_model(p, inp):
+    return O.build_model_additive(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, [0.7, 1.3, 1.0][:p.d],
+                                  p.sigma2)
+
+
+def test_additive_kuu_closed_form():
+    """Block-diagonal K_UU of Eq. 16: entry (p, q) is s_e^2 exp(-((p-q) h_e)^2 /
+    (2 l_e^2)) when p, q are nodes of component e, zero across components."""
+    p, inp = tiny_problem("additive3")
+    model = _additive_model(p, inp)
+    K = O.model_kuu_dense(model)
+    s2 = [0.7, 1.3, 1.0]
+    off = np.cumsum([0] + list(p.m))
+    for a in range(model.m_total):
+        for b in range(model.m_total):
+            ea = np.searchsorted(off, a, side="right") - 1
+            eb = np.searchsorted(off, b, side="right") - 1
+            want = 0.0
+            if ea == eb:
+                want = s2[ea] * math.exp(-((a - b) * p.h[ea]) ** 2 / (2 * p.lengthscale[ea] ** 2))
+            assert abs(K[a, b] - want) < 1e-15
+    u = np.random.default_rng(3).normal(size=model.m_total)
+    np.testing.assert_allclose(O.model_kuu_matvec(model, u), K @ u, rtol=1e-12, atol=1e-12)
+
+
+def test_additive_kernel_exact_on_nodes():
+    """On grid nodes the cubic weights are (0, 1, 0, 0), so the SKI additive kernel
+    w_x^T K_UU w_x' equals the exact sum of 1-D kernels (Eq. 16 first line)."""
+    p, inp = tiny_problem("additive3")
+    model = _additive_model(p, inp)
+    rng = np.random.default_rng(5)
+    Xa = np.array([[p.lo[e] + rng.integers(2, 12) * p.h[e] for e in range(p.d)] for _ in range(40)])
+    Xb = np.array([[p.lo[e] + rng.integers(2, 12) * p.h[e] for e in range(p.d)] for _ in range(40)])
+    ia, wa = O.model_interp(model, Xa)
+    ib, wb = O.model_interp(model, Xb)
+    ski = O.prior_ski(model, ia, wa, ib, wb)
+    exact = sum([0.7, 1.3, 1.0][e] * np.exp(-(Xa[:, e] - Xb[:, e]) ** 2 / (2 * p.lengthscale[e] ** 2))
+                for e in range(p.d))
+    np.testing.assert_allclose(ski, exact, rtol=1e-12, atol=1e-14)
+    np.testing.assert_allclose(O.prior_exact(model, Xa, Xb), exact, rtol=1e-14)
+
+
+def test_additive_love_equals_dense_gp_at_full_krylov():
+    """Eq. 16: Algorithm 1 with the block forms run to breakdown equals the dense
+    GP with the additive SKI kernel (Eq. 7 bridge)."""
+    p, inp = tiny_problem("additive3")
+    model = _additive_model(p, inp)
+    cache = O.love_precompute(model, p.k)
+    assert cache.lanczos.k_eff < p.k
+    mean_d, var_d = O.dense_ski_gp(model, inp.Xs)
+    var = O.predict_var(model, cache, inp.Xs)
+    np.testing.assert_allclose(var, var_d, rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(O.predict_mean(model, cache, inp.Xs), mean_d, rtol=1e-8, atol=1e-10)
