@@ -142,6 +142,34 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
                              const love_opts* opts, const love_dist* dist, void* stream,
                              love_cache** out);
 
+/* ---------------------------------------------------------------------------------------
+ * Additive kernel compositions (Eq. 16): k(x, x') = sum_e k_e(x_e, x'_e) with one
+ * 1-D SKI component per input dimension.  The interpolation vectors stack the components'
+ * 1-D cubic stencils (4 nonzeros each, 4d per point) and K_UU is block diagonal with the
+ * components' Toeplitz blocks; Algorithm 1 runs unchanged on these block forms.
+ * Component e: grid u_{e,i} = lo + i*h (i < m, 4 <= m <= 1024), RBF
+ * outputscale * exp(-r^2 / (2 lengthscale^2)); its inducing points are numbered after those of
+ * components 0..e-1 (m_total = sum_e m_e).
+ * ------------------------------------------------------------------------------------ */
+typedef struct {
+    int64_t m;
+    double lo;
+    double h;
+    double lengthscale;
+    double outputscale;
+} love_axis;
+#define LOVE_MAX_ADDITIVE 32
+
+/* love_build_cache for an additive composition of d (1..LOVE_MAX_ADDITIVE) components.
+ *   axes : HOST array of d love_axis.  X : n_local x d fp64 row-major (device).  Other
+ *   arguments as love_build_cache.  opts->k_sample must be 0 (LOVE_ERR_ARG otherwise) and
+ *   opts->var_blocks is ignored (variances come from the Rc rows of the 4d stencil nodes).
+ * The cache answers love_predict_var / love_predict_covar / love_kuu_mvm / love_ski_mvm /
+ * love_cache_export like a grid cache; training points keep their original order. */
+love_status love_build_cache_additive(const love_axis* axes, int32_t d, double sigma2, const double* X,
+                                      const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                                      const love_dist* dist, void* stream, love_cache** out);
+
 /* Predictive variances (Eq. 10 with x*_i = x*_j; Alg. 1):
  *   var(x*) = prior(x*) - || Rc^T w_{x*} ||^2,   prior = w*^T K_UU w* (SKI) or k(x*,x*).
  *   Xs       : t x d fp64 (device).  var_out : t values of V (device).

@@ -34,6 +34,11 @@ class love_opts(ctypes.Structure):
                 ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32), ("var_blocks", ctypes.c_int32)]
 
 
+class love_axis(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("lo", ctypes.c_double), ("h", ctypes.c_double),
+                ("lengthscale", ctypes.c_double), ("outputscale", ctypes.c_double)]
+
+
 class love_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p)]
@@ -55,6 +60,10 @@ SIGNATURES = {
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
                                         ctypes.POINTER(love_opts), ctypes.POINTER(love_dist), ctypes.c_void_p,
                                         ctypes.POINTER(ctypes.c_void_p)]),
+    "love_build_cache_additive": (ctypes.c_int, [ctypes.POINTER(love_axis), ctypes.c_int32, ctypes.c_double,
+                                                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                                 ctypes.POINTER(love_opts), ctypes.POINTER(love_dist),
+                                                 ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
     "love_predict_var": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p]),
     "love_predict_covar": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,

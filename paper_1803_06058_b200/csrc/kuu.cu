@@ -806,6 +806,10 @@ void setup_kuu(Cache& c, cudaStream_t s) {
 }
 
 void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc) {
+    if (c.additive) {
+        add_kuu(c, u, z, s);
+        return;
+    }
     if (c.g.d > 1) kuu_axes(c, u, z, s);
     else fft_run(c, u, Mc, c.g.m[0], z, (C*)c.fft_buf, nullptr, 0, s);
 }

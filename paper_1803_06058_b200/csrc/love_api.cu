@@ -146,62 +146,31 @@ void validate_build(const love_grid* grid, const love_rbf* rbf, double sigma2, c
 
 }  // namespace love
 
-using namespace love;
+namespace love {
+namespace {
 
-extern "C" {
+love_opts checked_opts(const love_opts* opts) {
+    love_opts o{};
+    o.precision = LOVE_FP32;
+    if (opts) o = *opts;
+    if (o.precision != LOVE_FP32 && o.precision != LOVE_FP64) throw LoveError{LOVE_ERR_ARG, "bad precision"};
+    if (o.probe != LOVE_PROBE_Y && o.probe != LOVE_PROBE_AVGCOL) throw LoveError{LOVE_ERR_ARG, "bad probe"};
+    if (o.prior != LOVE_PRIOR_SKI && o.prior != LOVE_PRIOR_EXACT) throw LoveError{LOVE_ERR_ARG, "bad prior"};
+    if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
+    if (o.var_blocks != LOVE_VAR_BLOCKS_AUTO && o.var_blocks != LOVE_VAR_BLOCKS_OFF)
+        throw LoveError{LOVE_ERR_ARG, "bad var_blocks"};
 
-const char* love_last_error(void) { return t_err.c_str(); }
-int64_t love_launch_count(void) { return g_launch_count.load(); }
-int32_t love_abi_version(void) { return LOVE_ABI_VERSION; }
-
-love_status love_nccl_unique_id(void* out) {
-    if (!out) {
-        set_error("NULL out");
-        return LOVE_ERR_ARG;
-    }
-    return nccl_get_unique_id(out);
+    return o;
 }
 
-love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
-                             const double* y, int64_t n_local, int32_t k, const love_opts* opts,
-                             const love_dist* dist, void* stream, love_cache** out) {
-    Cache* c = nullptr;
-    cudaStream_t s = nullptr;
+// Cache creation and everything both model structures share before the structure-specific
+// setup: options, NCCL communicator, global n, k clamp, Q's leading dimension.
+Cache* begin_build(const love_opts& o, double sigma2, int64_t n_local, int32_t& k, const love_dist* dist,
+                   cudaStream_t s) {
+    Cache* c = new Cache();
     try {
-        if (out) *out = nullptr;
-        validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
-        int dev = 0;
-        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-        s = work_stream(dev);
-        order_after(s, (cudaStream_t)stream);
-        love_opts o{};
-        o.precision = LOVE_FP32;
-        if (opts) o = *opts;
-        if (o.precision != LOVE_FP32 && o.precision != LOVE_FP64) throw LoveError{LOVE_ERR_ARG, "bad precision"};
-        if (o.probe != LOVE_PROBE_Y && o.probe != LOVE_PROBE_AVGCOL) throw LoveError{LOVE_ERR_ARG, "bad probe"};
-        if (o.prior != LOVE_PRIOR_SKI && o.prior != LOVE_PRIOR_EXACT) throw LoveError{LOVE_ERR_ARG, "bad prior"};
-        if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
-        if (o.var_blocks != LOVE_VAR_BLOCKS_AUTO && o.var_blocks != LOVE_VAR_BLOCKS_OFF)
-            throw LoveError{LOVE_ERR_ARG, "bad var_blocks"};
-
-        c = new Cache();
         cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
         keep_pool_memory(c->device);
-        GridDev& g = c->g;
-        g.d = grid->d;
-        g.m_total = 1;
-        for (int d = 0; d < 3; ++d) {
-            g.m[d] = d < g.d ? (int)grid->m[d] : 1;
-            g.lo[d] = d < g.d ? grid->lo[d] : 0.0;
-            g.h[d] = d < g.d ? grid->h[d] : 1.0;
-        }
-        for (int d = g.d - 1, st = 1; d >= 0; --d) {
-            g.stride[d] = st;
-            st *= g.m[d];
-        }
-        for (int d = g.d; d < 3; ++d) g.stride[d] = 0;
-        for (int d = 0; d < g.d; ++d) g.m_total *= g.m[d];
-        c->rbf = *rbf;
         c->sigma2 = sigma2;
         c->precision = o.precision;
         c->vsize = o.precision == LOVE_FP64 ? 8 : 4;
@@ -239,11 +208,136 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         if (c->n_global < 1) throw LoveError{LOVE_ERR_ARG, "no training points"};
         if (k > c->n_global) k = (int32_t)c->n_global;     // a Krylov space has at most n dimensions
         c->k_req = k;
+        c->ldq = round_up(std::max<int64_t>(c->n, 1), 4);
+    } catch (...) {
+        cudaStreamSynchronize(s);
+        release(c);
+        throw;
+    }
+    return c;
+}
+
+// Lanczos state, the k steps, host copies of T, the cache finish (Rc, mean,
+// variance blocks, sampling root).  Leaves the cache complete; throws on numerical errors.
+void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
+    const int M = c->g.m_total;
+    const size_t vs = c->vsize;
+    // ---- Lanczos state
+    c->r = dalloc(*c, vs * c->ldq, s);
+    c->u = dalloc(*c, sizeof(double) * M, s);
+    c->z[0] = dalloc(*c, sizeof(double) * (M + 4), s);      // padded: tiles stage z in 16-byte units
+    c->z[1] = dalloc(*c, sizeof(double) * (M + 4), s);
+    c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
+    c->a = dalloc(*c, sizeof(double) * M, s);
+    c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
+    {
+        const size_t K = k;
+        const size_t nd = K + K + 2 * K * (K + 1) + 1 + (K + 1) + 5 * K + 2 + 1;
+        c->scal = (double*)dalloc(*c, sizeof(double) * nd, s);
+        double* p = c->scal;
+        LanczosState& st = c->st;
+        st.alpha_acc = p; p += K;
+        st.beta2_acc = p; p += K;
+        st.c_acc = p; p += 2 * K * (K + 1);
+        st.bnorm2 = p; p += 1;
+        st.qscale = p; p += K + 1;
+        st.alpha = p; p += K;
+        st.beta = p; p += K;
+        st.Ld = p; p += K;
+        st.Ls = p; p += K;
+        st.g = p; p += K;
+        st.amax_bmax = p; p += 2;
+        c->one = p; p += 1;
+        st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
+        st.jdev = st.flags + 4;
+        st.step_ctr = st.flags + 5;
+        LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
+    }
+
+    // ---- probe b = (1/m) W_X^T K_UU 1 (average column of K_XU K_UU..., Alg. 1)
+    if (c->probe == LOVE_PROBE_AVGCOL) avgcol_probe(*c, s);
+
+    // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
+    if (c->fused) setup_fused(*c, s);
+    if (c->fused) run_lanczos_fused(*c, s);
+    else run_lanczos(*c, s);
+    int hfl[4];
+    double bn2 = 0;
+    cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
+    cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaStreamSynchronize(s), "lanczos sync");
+    cuda_check(cudaGetLastError(), "lanczos kernels");
+    if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
+    if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
+    c->k_eff = hfl[1];
+    c->b_norm = std::sqrt(bn2);
+    c->h_alpha.resize(c->k_eff);
+    c->h_beta.resize(std::max(c->k_eff - 1, 0));
+    cuda_check(cudaMemcpy(c->h_alpha.data(), c->st.alpha, sizeof(double) * c->k_eff, cudaMemcpyDeviceToHost),
+               "alpha d2h");
+    if (c->k_eff > 1)
+        cuda_check(cudaMemcpy(c->h_beta.data(), c->st.beta, sizeof(double) * (c->k_eff - 1),
+                              cudaMemcpyDeviceToHost), "beta d2h");
+    if (c->probe == LOVE_PROBE_AVGCOL) mean_cache_eq4(*c, s);   // a = R^T T^{-1} Q^T y
+    finish_cache(*c, s);
+    c->var_blocks_off = o.var_blocks == LOVE_VAR_BLOCKS_OFF;
+    build_var_blocks(*c, s);
+    if (c->k_sample_req > 0) build_sampling_cache(*c, s);
+    cuda_check(cudaStreamSynchronize(s), "build sync");
+    cuda_check(cudaGetLastError(), "build kernels");
+}
+
+}  // namespace
+}  // namespace love
+
+using namespace love;
+
+extern "C" {
+
+const char* love_last_error(void) { return t_err.c_str(); }
+int64_t love_launch_count(void) { return g_launch_count.load(); }
+int32_t love_abi_version(void) { return LOVE_ABI_VERSION; }
+
+love_status love_nccl_unique_id(void* out) {
+    if (!out) {
+        set_error("NULL out");
+        return LOVE_ERR_ARG;
+    }
+    return nccl_get_unique_id(out);
+}
+
+love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
+                             const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                             const love_dist* dist, void* stream, love_cache** out) {
+    Cache* c = nullptr;
+    cudaStream_t s = nullptr;
+    try {
+        if (out) *out = nullptr;
+        validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        s = work_stream(dev);
+        order_after(s, (cudaStream_t)stream);
+        const love_opts o = checked_opts(opts);
+        c = begin_build(o, sigma2, n_local, k, dist, s);
+        GridDev& g = c->g;
+        g.d = grid->d;
+        g.m_total = 1;
+        for (int d = 0; d < 3; ++d) {
+            g.m[d] = d < g.d ? (int)grid->m[d] : 1;
+            g.lo[d] = d < g.d ? grid->lo[d] : 0.0;
+            g.h[d] = d < g.d ? grid->h[d] : 1.0;
+        }
+        for (int d = g.d - 1, st = 1; d >= 0; --d) {
+            g.stride[d] = st;
+            st *= g.m[d];
+        }
+        for (int d = g.d; d < 3; ++d) g.stride[d] = 0;
+        for (int d = 0; d < g.d; ++d) g.m_total *= g.m[d];
+        c->rbf = *rbf;
         const int M = g.m_total;
         const size_t vs = c->vsize;
-        c->ldq = round_up(std::max<int64_t>(c->n, 1), 4);
-        if (const char* e = std::getenv("LOVE_LDQ_PAD")) c->ldq = round_up(c->ldq, 64) + std::atoll(e);
-
+        TempPool tmp(s);
         // ---- interpolation records + cell sort
         int* cell = (int*)tmp.get(sizeof(int) * std::max<int64_t>(c->n, 1));
         double* frac64 = (double*)tmp.get(sizeof(double) * std::max<int64_t>(c->n, 1) * g.d);
@@ -291,69 +385,106 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         setup_kuu(*c, s);
         prof_end(LOVE_PROF_SETUP, s);
 
-        // ---- Lanczos state
-        c->r = dalloc(*c, vs * c->ldq, s);
-        c->u = dalloc(*c, sizeof(double) * M, s);
-        c->z[0] = dalloc(*c, sizeof(double) * (M + 4), s);      // padded: tiles stage z in 16-byte units
-        c->z[1] = dalloc(*c, sizeof(double) * (M + 4), s);
-        c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
-        c->a = dalloc(*c, sizeof(double) * M, s);
-        c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
-        {
-            const size_t K = k;
-            const size_t nd = K + K + 2 * K * (K + 1) + 1 + (K + 1) + 5 * K + 2 + 1;
-            c->scal = (double*)dalloc(*c, sizeof(double) * nd, s);
-            double* p = c->scal;
-            LanczosState& st = c->st;
-            st.alpha_acc = p; p += K;
-            st.beta2_acc = p; p += K;
-            st.c_acc = p; p += 2 * K * (K + 1);
-            st.bnorm2 = p; p += 1;
-            st.qscale = p; p += K + 1;
-            st.alpha = p; p += K;
-            st.beta = p; p += K;
-            st.Ld = p; p += K;
-            st.Ls = p; p += K;
-            st.g = p; p += K;
-            st.amax_bmax = p; p += 2;
-            c->one = p; p += 1;
-            st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
-            st.jdev = st.flags + 4;
-            st.step_ctr = st.flags + 5;
-            LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
+        finish_build(c, o, k, s);
+        *out = reinterpret_cast<love_cache*>(c);
+        return LOVE_OK;
+    } catch (const LoveError& e) {
+        if (c) {
+            if (s) cudaStreamSynchronize(s);
+            release(c);
         }
+        return fail(e);
+    }
+}
 
-        // ---- probe b = (1/m) W_X^T K_UU 1 (average column of K_XU K_UU..., Alg. 1)
-        if (c->probe == LOVE_PROBE_AVGCOL) avgcol_probe(*c, s);
-
-        // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
-        if (c->fused) setup_fused(*c, s);
-        if (c->fused) run_lanczos_fused(*c, s);
-        else run_lanczos(*c, s);
-        int hfl[4];
-        double bn2 = 0;
-        cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
-        cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
-        cuda_check(cudaStreamSynchronize(s), "lanczos sync");
-        cuda_check(cudaGetLastError(), "lanczos kernels");
-        if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
-        if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
-        c->k_eff = hfl[1];
-        c->b_norm = std::sqrt(bn2);
-        c->h_alpha.resize(c->k_eff);
-        c->h_beta.resize(std::max(c->k_eff - 1, 0));
-        cuda_check(cudaMemcpy(c->h_alpha.data(), c->st.alpha, sizeof(double) * c->k_eff, cudaMemcpyDeviceToHost),
-                   "alpha d2h");
-        if (c->k_eff > 1)
-            cuda_check(cudaMemcpy(c->h_beta.data(), c->st.beta, sizeof(double) * (c->k_eff - 1),
-                                  cudaMemcpyDeviceToHost), "beta d2h");
-        if (c->probe == LOVE_PROBE_AVGCOL) mean_cache_eq4(*c, s);   // a = R^T T^{-1} Q^T y
-        finish_cache(*c, s);
-        c->var_blocks_off = o.var_blocks == LOVE_VAR_BLOCKS_OFF;
-        build_var_blocks(*c, s);
-        if (c->k_sample_req > 0) build_sampling_cache(*c, s);
-        cuda_check(cudaStreamSynchronize(s), "build sync");
-        cuda_check(cudaGetLastError(), "build kernels");
+love_status love_build_cache_additive(const love_axis* axes, int32_t d, double sigma2, const double* X,
+                                      const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                                      const love_dist* dist, void* stream, love_cache** out) {
+    Cache* c = nullptr;
+    cudaStream_t s = nullptr;
+    try {
+        if (out) *out = nullptr;
+        if (!axes || !out) throw LoveError{LOVE_ERR_ARG, "NULL axes/out"};
+        if (d < 1 || d > LOVE_MAX_ADDITIVE) throw LoveError{LOVE_ERR_ARG, "d must be 1..LOVE_MAX_ADDITIVE"};
+        int64_t mt = 0;
+        for (int e = 0; e < d; ++e) {
+            const love_axis& x = axes[e];
+            if (x.m < 4 || x.m > 1024) throw LoveError{LOVE_ERR_ARG, "axis m must be 4..1024"};
+            if (!(x.h > 0.0) || !std::isfinite(x.lo) || !(x.lengthscale > 0.0) || !(x.outputscale > 0.0))
+                throw LoveError{LOVE_ERR_ARG, "axis h, lengthscale, outputscale must be > 0 and lo finite"};
+            mt += x.m;
+        }
+        if (!(sigma2 > 0.0)) throw LoveError{LOVE_ERR_ARG, "sigma^2 must be > 0"};
+        if (k < 1 || k > 2048) throw LoveError{LOVE_ERR_ARG, "k must be 1..2048"};
+        if (n_local < 0 || n_local >= (int64_t(1) << 31)) throw LoveError{LOVE_ERR_ARG, "bad n_local"};
+        if (n_local > 0 && (!X || !y)) throw LoveError{LOVE_ERR_ARG, "NULL X/y"};
+        int dev = 0;
+        cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        s = work_stream(dev);
+        order_after(s, (cudaStream_t)stream);
+        love_opts o = checked_opts(opts);
+        if (o.k_sample > 0) throw LoveError{LOVE_ERR_ARG, "k_sample is not supported for additive caches"};
+        if (o.lanczos_mode == LOVE_LANCZOS_ONE_READ)
+            throw LoveError{LOVE_ERR_ARG, "the one-read Lanczos pass is grid-only"};
+        o.lanczos_mode = LOVE_LANCZOS_TWO_PASS;
+        c = begin_build(o, sigma2, n_local, k, dist, s);
+        c->fused = false;
+        c->additive = true;
+        AddDev& a = c->ad;
+        a.d = d;
+        a.off[0] = 0;
+        for (int e = 0; e < d; ++e) {
+            a.m[e] = (int)axes[e].m;
+            a.lo[e] = axes[e].lo;
+            a.h[e] = axes[e].h;
+            a.ls[e] = axes[e].lengthscale;
+            a.s2[e] = axes[e].outputscale;
+            a.off[e + 1] = a.off[e] + a.m[e];
+            for (int i = 0; i < 4; ++i) {
+                const double r = (double)i * a.h[e];
+                a.c4[e][i] = std::exp(-(r * r) / (2.0 * a.ls[e] * a.ls[e]));
+            }
+        }
+        c->g = GridDev{};
+        c->g.d = 0;
+        c->g.m_total = (int)mt;
+        c->rbf = love_rbf{};
+        c->rbf.outputscale = 1.0;
+        const size_t vs = c->vsize;
+        TempPool tmp(s);
+        int* dflag = (int*)tmp.get(sizeof(int) * 2);
+        cuda_check(cudaMemsetAsync(dflag, 0, sizeof(int) * 2, s), "memset");
+        c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        prof_begin(LOVE_PROF_SETUP, s);
+        additive_setup(*c, X, y, dflag, s);
+        {   // the range check is global: every rank must agree before continuing
+            int hflag = 0;
+            cuda_check(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
+            cuda_check(cudaStreamSynchronize(s), "sync");
+            if (c->comm != nullptr) {
+                float fl = (float)hflag;
+                float* df = (float*)tmp.get(sizeof(float));
+                cuda_check(cudaMemcpyAsync(df, &fl, sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
+                allreduce_sum(*c, df, 1, false, s);
+                cuda_check(cudaMemcpyAsync(&fl, df, sizeof(float), cudaMemcpyDeviceToHost, s), "d2h");
+                cuda_check(cudaStreamSynchronize(s), "sync");
+                hflag = fl > 0.f;
+            }
+            if (hflag) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside its component grid"};
+        }
+        // probe y: the targets (original order) are the first Lanczos column; probe avg: kept
+        // for the mean cache (Eq. 4) and column 0 is filled by the probe
+        void* ydst = c->Q;
+        if (c->probe == LOVE_PROBE_AVGCOL) ydst = c->ysort = dalloc(*c, vs * c->ldq, s);
+        if (c->n > 0) {
+            if (c->precision == LOVE_FP64)
+                cuda_check(cudaMemcpyAsync(ydst, y, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s), "y copy");
+            else
+                launch_convert<double, float>(y, (float*)ydst, c->n, s);
+        }
+        c->n_items = c->n;
+        prof_end(LOVE_PROF_SETUP, s);
+        finish_build(c, o, k, s);
         *out = reinterpret_cast<love_cache*>(c);
         return LOVE_OK;
     } catch (const LoveError& e) {

@@ -22,6 +22,17 @@ struct GridDev {
     int m_total;
 };
 
+// Additive composition (Eq. 16): per component e a 1-D grid and RBF; component e's
+// inducing points are nodes off[e] .. off[e] + m[e] - 1 of the stacked set.
+constexpr int kMaxAdd = LOVE_MAX_ADDITIVE;
+struct AddDev {
+    int d;
+    int m[kMaxAdd];
+    int off[kMaxAdd + 1];          // off[d] = m_total
+    double lo[kMaxAdd], h[kMaxAdd], ls[kMaxAdd], s2[kMaxAdd];
+    double c4[kMaxAdd][4];         // c_e[0..3] (variance prior)
+};
+
 // Which Lanczos column a step kernel works on.  Step kernels read the step index j from
 // device memory (so one captured step graph can be replayed k times); the vector they use
 // is base + j * ld, scaled by scale[j]; they do nothing once flags[0] (done) is set.
@@ -85,6 +96,15 @@ struct Cache {
     void* comm = nullptr;               // ncclComm_t
     int device = 0;
     size_t vsize = 4;                   // sizeof(V)
+
+    // ---------------- additive composition (love_build_cache_additive)
+    bool additive = false;
+    AddDev ad{};
+    int* acell = nullptr;                // [d][n] cell per component, original point order
+    void* afrac = nullptr;               // V[d][n] fractional offsets
+    int* aperm = nullptr;                // [d][n] component-e cell-sorted position -> point
+    int* astart = nullptr;               // component e: cell starts at astart + off[e] + e (m_e + 1)
+    void* aMc = nullptr;                 // double[4][m_total] per-cell scatter moments
 
     // ---------------- training points (sorted by flat cell)
     int64_t n = 0, n_global = 0, ldq = 0;
@@ -224,6 +244,14 @@ void mean_cache_eq4(Cache& c, cudaStream_t s);  // a = Rc L^{-1} Q^T y after the
 template <typename V> void launch_predict(const Cache& c, const double* Xa, const double* Xb,
                                           int64_t t, V* out, V* mean_out, cudaStream_t s);
 void build_var_blocks(Cache& c, cudaStream_t s);   // per-cell fp64 variance blocks (d <= 2)
+// additive.cu
+void additive_setup(Cache& c, const double* X, const double* y, int* range_flag, cudaStream_t s);
+template <typename V> void add_scatter(const Cache& c, const V* qbase, StepRef ref, double* u, cudaStream_t s);
+void add_kuu(const Cache& c, const double* u, double* z, cudaStream_t s);
+template <typename V> void add_gather(const Cache& c, const double* z, const V* qbase, StepRef ref, V* r,
+                                      double* alpha_base, cudaStream_t s, const RcStream* rs);
+template <typename V> void add_predict(const Cache& c, const double* Xa, const double* Xb, int64_t t, V* out,
+                                       V* mean_out, cudaStream_t s);
 // sample.cu
 void build_sampling_cache(Cache& c, cudaStream_t s);
 template <typename V> void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns,

@@ -493,7 +493,7 @@ __global__ void nan_fill_kernel(const int* __restrict__ qstart, int m, const int
 }
 
 void build_var_blocks(Cache& c, cudaStream_t s) {
-    if (c.g.d > 2 || c.var_blocks_off || c.k_eff < 1) return;
+    if (c.additive || c.g.d > 2 || c.var_blocks_off || c.k_eff < 1) return;
     ProfScope ps(LOVE_PROF_FINISH, s);
     const int m = c.g.m_total;
     c.vblk = dalloc(c, sizeof(double) * (size_t)m * blk_size(c.g.d), s);
@@ -510,6 +510,10 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
                     cudaStream_t s) {
     if (t <= 0) return;
     ProfScope ps(LOVE_PROF_QUERY, s);
+    if (c.additive) {
+        add_predict<V>(c, Xa, Xb, t, out, mean_out, s);
+        return;
+    }
     if (Xb == nullptr && c.vblk != nullptr) {
         C4 c4{};
         for (int d = 0; d < c.g.d; ++d)

@@ -278,6 +278,10 @@ void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s) {
 
 template <typename V>
 void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStream_t s, bool moments_only) {
+    if (c.additive) {
+        add_scatter<V>(c, q, ref, u, s);
+        return;
+    }
     if (c.g.d == 1 && c.Mc != nullptr) {
         const int m = c.g.m_total;
         LOVE_LAUNCH(moments_cell1_kernel<V>, (int)ceil_div(m, 256), 256, 0, s, m, c.cell_start, (const V*)c.frac[0],
@@ -325,6 +329,10 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
 template <typename V>
 void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* r, double* alpha_base,
                    cudaStream_t s, const RcStream* rsp) {
+    if (c.additive) {
+        add_gather<V>(c, z, q, ref, r, alpha_base, s, rsp);
+        return;
+    }
     const int64_t ni = c.n_items;
     const int gi = (int)ceil_div(ni, 256);
     RcStream rs{};

@@ -112,6 +112,41 @@ class LoveCache:
                                        ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
         return cls(out.value, o.precision, d, int(np.prod(m)))
 
+    @classmethod
+    def build_additive(cls, X, y, m: Sequence[int], lo: Sequence[float], h: Sequence[float],
+                       lengthscale: Sequence[float], outputscale, sigma2: float, k: int,
+                       precision: str = "fp32", prior: str = "ski", probe: str = "y",
+                       reorth_passes: int = 0, breakdown_tol: float = 0.0,
+                       rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
+                       stream=None) -> "LoveCache":
+        """Additive composition of len(m) 1-D RBF components (Eq. 16, P:406-441);
+        outputscale: one value for every component or one per component."""
+        d = len(m)
+        Xd = _dev(X, torch.float64).reshape(-1, d)
+        yd = _dev(y, torch.float64).reshape(-1)
+        s2 = list(outputscale) if hasattr(outputscale, "__len__") else [float(outputscale)] * d
+        axes = (_abi.love_axis * d)()
+        for e in range(d):
+            axes[e].m, axes[e].lo, axes[e].h = int(m[e]), float(lo[e]), float(h[e])
+            axes[e].lengthscale, axes[e].outputscale = float(lengthscale[e]), float(s2[e])
+        o = _abi.love_opts()
+        o.precision = _abi.LOVE_FP64 if precision == "fp64" else _abi.LOVE_FP32
+        o.probe = {"y": _abi.LOVE_PROBE_Y, "avg": _abi.LOVE_PROBE_AVGCOL}[probe]
+        o.prior = _abi.LOVE_PRIOR_EXACT if prior == "exact" else _abi.LOVE_PRIOR_SKI
+        o.reorth_passes = int(reorth_passes)
+        o.breakdown_tol = float(breakdown_tol)
+        dist = None
+        idbuf = None
+        if world > 1 or nccl_id is not None:
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            dist = _abi.love_dist(rank, world, ctypes.cast(idbuf, ctypes.c_void_p))
+        out = ctypes.c_void_p()
+        _check(_lib().love_build_cache_additive(axes, d, float(sigma2), _ptr(Xd), _ptr(yd), int(Xd.shape[0]),
+                                                int(k), ctypes.byref(o),
+                                                ctypes.byref(dist) if dist is not None else None,
+                                                ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
+        return cls(out.value, o.precision, d, int(sum(m)))
+
     # ------------------------------------------------------------------ queries
     def predict_var(self, Xs, return_mean: bool = False, stream=None):
         Xd = _dev(Xs, torch.float64).reshape(-1, self.d)

@@ -64,7 +64,7 @@ def test_struct_layouts_match_header(tmp_path):
     import subprocess
     from paper_1803_06058_b200 import _abi
     structs = {"love_grid": _abi.love_grid, "love_rbf": _abi.love_rbf, "love_opts": _abi.love_opts,
-               "love_dist": _abi.love_dist, "love_info": _abi.love_info}
+               "love_dist": _abi.love_dist, "love_info": _abi.love_info, "love_axis": _abi.love_axis}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for name, cls in structs.items():
         lines.append(f'printf("{name} sizeof %zu\\n", sizeof({name}));')
