@@ -84,6 +84,8 @@ def query_bytes(p, k_pad: int):
     result (the cell-sorted kernel stages those rows once per cell, so this is an upper bound
     on what it reads)."""
     sv = 8 if p.precision == "fp64" else 4
+    if p.kind == "additive":
+        return 4 * p.d * k_pad * sv + 8 * p.d + sv, "gathered rows of the 4d block stencil (Eq. 16)"
     if p.d <= 2:
         nb = 4 ** p.d
         return 8 * p.d + 8 * nb * (nb + 1) // 2 + sv, "cell-block (x*, fp64 block of its cell, result)"
@@ -153,7 +155,11 @@ def run_oracle_step(p, inp, t_sample):
     points.  Returns (build_s, query_s)."""
     import oracle as O
     t0 = time.perf_counter()
-    model = O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+    if p.kind == "additive":
+        model = O.build_model_additive(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, [p.outputscale] * p.d,
+                                       p.sigma2)
+    else:
+        model = O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
     cache = O.love_precompute(model, p.k)
     t1 = time.perf_counter()
     O.predict_var(model, cache, inp.Xs[:t_sample])
@@ -249,11 +255,18 @@ def main():
     kw = dict(m=p.m, lo=p.lo, h=p.h, lengthscale=p.lengthscale, outputscale=p.outputscale, sigma2=p.sigma2,
               k=p.k, precision=p.precision, rank=rank, world=world, nccl_id=nccl_id, k_sample=p.k_sample)
     lib = _abi.load()
+    if p.kind == "additive":                      # Eq. 16 block forms (NEXT #2): no sampling cache
+        kw.pop("k_sample")
+
+    def build(Xd, yd):
+        if p.kind == "additive":
+            return LoveCache.build_additive(Xd, yd, **kw)
+        return LoveCache.build(Xd, yd, **kw)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)   # > 126 MB L2
     lib.love_profile_enable(0)
 
     def step(Xd, yd, Xsd, e2e=False):
-        c = LoveCache.build(Xd, yd, **kw)
+        c = build(Xd, yd)
         var = c.predict_var(Xsd)
         if p.k_sample:
             F = c.sample(Xsd, p.s, seed=0)
@@ -287,7 +300,7 @@ def main():
         flush.zero_()
         e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
         e0.record(stream)
-        c = LoveCache.build(X, y, **kw)
+        c = build(X, y)
         e1.record(stream)
         c.predict_var(Xs)
         e2.record(stream)
@@ -318,7 +331,7 @@ def main():
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        c = LoveCache.build(X, y, **kw)
+        c = build(X, y)
         c.predict_var(Xs)
         e1.record(stream)
         e1.synchronize()

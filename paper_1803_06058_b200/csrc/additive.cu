@@ -9,7 +9,7 @@
 // the streamed cache and the queries are the grid code's; this file supplies the
 // structure-specific operators:
 //   scatter  u = W q       : per component, points counting-sorted by their component cell;
-//                            one thread per cell sums its 4 stencil moments (fixed order, no
+//                            one warp per cell sums its 4 stencil moments (fixed order, no
 //                            atomics), then a node pass u[off_e + i] = sum_s M_s[off_e + i+1-s]
 //   K_UU u                 : one CTA per component
 //   gather   r = W^T z + s2 q, alpha : one thread per point, 4d z values
@@ -61,6 +61,8 @@ __global__ void iota_kernel(int* __restrict__ p, int64_t n) {
         p[i] = (int)i;
 }
 
+// one warp per component cell (a component cell holds ~n / m_e points): lanes stride over the
+// cell's points in fixed order, four fp64 partial sums per lane, then a warp reduction
 template <typename V>
 __global__ void __launch_bounds__(256) add_moments_kernel(AddDev a, int64_t n, const int* __restrict__ aperm,
                                                           const int* __restrict__ astart, const V* __restrict__ afrac,
@@ -68,7 +70,8 @@ __global__ void __launch_bounds__(256) add_moments_kernel(AddDev a, int64_t n, c
                                                           double* __restrict__ Mc) {
     pdl_wait();
     const int M = a.off[a.d];
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    const int g = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (g >= M || step_done(ref)) return;
     const int j = step_j(ref);
     const V* __restrict__ q = qbase + j * ref.ld;
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(256) add_moments_kernel(AddDev a, int64_t n, c
     const V* __restrict__ fe = afrac + (int64_t)e * n;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     const int i1 = st[c + 1];
-    for (int i = st[c]; i < i1; ++i) {
+    for (int i = st[c] + lane; i < i1; i += 32) {
         const int p = pe[i];
         double w[4];
         keys4<double>((double)fe[p], w);
@@ -86,6 +89,9 @@ __global__ void __launch_bounds__(256) add_moments_kernel(AddDev a, int64_t n, c
 #pragma unroll
         for (int s = 0; s < 4; ++s) acc[s] += w[s] * qv;
     }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) acc[s] = warp_sum(acc[s]);
+    if (lane != 0) return;
     const double sc = ref.scale[j];
 #pragma unroll
     for (int s = 0; s < 4; ++s) Mc[(int64_t)s * M + g] = acc[s] * sc;
@@ -309,7 +315,7 @@ void additive_setup(Cache& c, const double* X, const double* y, int* range_flag,
 template <typename V>
 void add_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStream_t s) {
     const int M = c.ad.off[c.ad.d];
-    LOVE_LAUNCH(add_moments_kernel<V>, (int)ceil_div(M, 256), 256, 0, s, c.ad, c.n, c.aperm, c.astart,
+    LOVE_LAUNCH(add_moments_kernel<V>, (int)ceil_div((int64_t)M * 32, 256), 256, 0, s, c.ad, c.n, c.aperm, c.astart,
                 (const V*)c.afrac, q, ref, (double*)c.aMc);
     LOVE_LAUNCH(add_nodepass_kernel, (int)ceil_div(M, 256), 256, 0, s, c.ad, (const double*)c.aMc, ref, u);
 }

@@ -36,11 +36,13 @@ def main():
         y = torch.from_numpy(inp.y).cuda()
         Xs = torch.from_numpy(inp.Xs).cuda()
         for mode in a.modes.split(","):
-            if mode == "one_read" and p.precision != "fp32":
+            if mode == "one_read" and (p.precision != "fp32" or p.kind == "additive"):
                 continue
-            kw = dict(precision=p.precision, lanczos_mode=mode)
+            kw = dict(precision=p.precision)
+            if p.kind != "additive":
+                kw["lanczos_mode"] = mode
             try:
-                c = LoveCache.build(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
+                c = (LoveCache.build_additive if p.kind == 'additive' else LoveCache.build)(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
                 c.free()
             except Exception as e:  # report and continue
                 print(json.dumps({"config": p.name, "mode": mode, "error": str(e)}), flush=True)
@@ -50,7 +52,7 @@ def main():
                 flush.zero_()
                 e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
                 e0.record()
-                c = LoveCache.build(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
+                c = (LoveCache.build_additive if p.kind == 'additive' else LoveCache.build)(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
                 e1.record()
                 c.predict_var(Xs)
                 e2.record()
@@ -61,7 +63,7 @@ def main():
                 c.free()
             lib.love_profile_read(None, None, 1)
             lib.love_profile_enable(1)
-            c = LoveCache.build(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
+            c = (LoveCache.build_additive if p.kind == 'additive' else LoveCache.build)(X, y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k, **kw)
             c.predict_var(Xs)
             torch.cuda.synchronize()
             c.free()
