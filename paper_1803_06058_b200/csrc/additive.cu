@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) add_gather_kernel(AddDev a, int64_t n, co
     }
     if (alpha_base != nullptr) {
         alpha = block_sum(alpha, red);
-        if (threadIdx.x == 0) atomicAdd(alpha_base + j, alpha);
+        if (threadIdx.x == 0) atomicAdd(alpha_base, alpha);
     }
 }
 

@@ -78,7 +78,7 @@ __global__ void step_prologue_kernel(LanczosState st, int k, double tol, int m,
     }
     const int i = j - 1;
     if (fl[1] <= i || fl[2] || fl[3]) return;           // stopped at an earlier step
-    const double al = st.alpha_acc[i];
+    const double al = st.alpha_cur[0];
     const double amax = fmax(st.amax_bmax[0], fabs(al));
     const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
     const double piv = al - lsub * lsub;
@@ -97,7 +97,7 @@ __global__ void step_prologue_kernel(LanczosState st, int k, double tol, int m,
             fl[0] = 1;
             fl[1] = k;
         } else {
-            const double b = sqrt(st.beta2_acc[i]);
+            const double b = sqrt(st.beta2_cur[0]);
             const double bmax = fmax(st.amax_bmax[1], b);
             st.amax_bmax[1] = bmax;
             if (!(b >= tol * (amax + 2.0 * bmax))) {
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
     const int64_t rows = min(tile_rows, ldq - row0);
     if (rows <= 0) return;
     const double sj = st.qscale[j];
-    const double aj = st.alpha_acc[j] * sj;
+    const double aj = st.alpha_cur[0] * sj;
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
     const int nchunk = (int)(rows / W);
     for (int q = threadIdx.x; q < nchunk; q += blockDim.x) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ 
         if (lane == 0) csum[sp * ncols + col] = dp;
     }
     __syncthreads();
-    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
+    double* __restrict__ c_out = st.c_cur + (int64_t)pass * (k + 1);
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
         double tot = 0.0;
         for (int sp = 0; sp < S; ++sp) tot += csum[sp * ncols + i];
@@ -239,12 +239,12 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     const int j = *st.jdev;
     if (st.flags[0] || j >= k - 1) return;
     const int from_r = pass == 0;
-    double* __restrict__ c_out = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
+    double* __restrict__ c_out = st.c_cur + (int64_t)pass * (k + 1);
     const int ncols = j + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* csum = smd;                                   // [nw][ncols]
     const double sj = st.qscale[j];
-    const double aj = st.alpha_acc[j] * sj;
+    const double aj = st.alpha_cur[0] * sj;
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
     const int64_t nvec = ldq / W;
     V src[CPT][W];
@@ -319,13 +319,26 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     }
 }
 
+// the current step's accumulators back to zero (one thread)
+__device__ __forceinline__ void clear_step_acc(const LanczosState& st, int k) {
+    st.alpha_cur[0] = 0.0;
+    st.beta2_cur[0] = 0.0;
+    for (int i = 0; i < 2 * (k + 1); ++i) st.c_cur[i] = 0.0;
+}
+
+// multi-GPU path: after the prologue has consumed the previous step's accumulators
+__global__ void clear_acc_kernel(LanczosState st, int k) {
+    pdl_wait();
+    if (threadIdx.x == 0 && blockIdx.x == 0) clear_step_acc(st, k);
+}
+
 // Scalars of index i once alpha_i and beta_i^2 are complete (same rules as the prologue):
 // alpha_i, row i of the Cholesky of T, g_i = (L^{-1} e_1)_i, beta_i, the
 // breakdown test (reading A12) and the scale of q_{i+1}.  One thread.
 __device__ __forceinline__ void finalize_index(const LanczosState& st, int i, int k, double tol) {
     int* fl = st.flags;
     if (fl[1] <= i || fl[2] || fl[3]) return;
-    const double al = st.alpha_acc[i];
+    const double al = st.alpha_cur[0];
     const double amax = fmax(st.amax_bmax[0], fabs(al));
     const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
     const double piv = al - lsub * lsub;
@@ -345,7 +358,7 @@ __device__ __forceinline__ void finalize_index(const LanczosState& st, int i, in
         fl[1] = k;
         return;
     }
-    const double b = sqrt(st.beta2_acc[i]);
+    const double b = sqrt(st.beta2_cur[0]);
     const double bmax = fmax(st.amax_bmax[1], b);
     st.amax_bmax[1] = bmax;
     if (!(b >= tol * (amax + 2.0 * bmax))) {
@@ -363,17 +376,29 @@ __device__ __forceinline__ void finalize_index(const LanczosState& st, int i, in
 // update has added its part) and writes j + 1 to the step index.
 __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
                                              double tol = 0.0) {
+    __shared__ int last;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(st.step_ctr), 1u);
-        if (prev == gridDim.x - 1) {
-            __threadfence();
-            if (fin) finalize_index(st, j, k, tol);
-            st.step_ctr[0] = 0;
-            st.jdev[0] = j + 1;
-            __threadfence();
+        last = prev == gridDim.x - 1;
+        if (last) __threadfence();
+    }
+    __syncthreads();
+    if (!last) return;
+    if (fin) {
+        if (threadIdx.x == 0) finalize_index(st, j, k, tol);
+        __syncthreads();                             // scalars read before the accumulators clear
+        for (int i = threadIdx.x; i < 2 * (k + 1); i += blockDim.x) st.c_cur[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        if (fin) {
+            st.alpha_cur[0] = 0.0;
+            st.beta2_cur[0] = 0.0;
         }
+        st.step_ctr[0] = 0;
+        st.jdev[0] = j + 1;
+        __threadfence();
     }
 }
 
@@ -394,13 +419,13 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         return;
     }
     const int from_r = pass == 0;
-    const double* __restrict__ c_in = st.c_acc + ((int64_t)pass * k + j) * (k + 1);
-    double* __restrict__ beta2_out = last_pass ? st.beta2_acc + j : nullptr;
+    const double* __restrict__ c_in = st.c_cur + (int64_t)pass * (k + 1);
+    double* __restrict__ beta2_out = last_pass ? st.beta2_cur : nullptr;
     const int ncols = j + 1;
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) cf[i] = c_in[i] * st.qscale[i];
     __syncthreads();
     const double sj = st.qscale[j];
-    const double aj = st.alpha_acc[j] * sj;
+    const double aj = st.alpha_cur[0] * sj;
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
     double b2 = 0.0;
     const int64_t nchunks = ldq / W;
@@ -495,8 +520,8 @@ struct StepPlan {
     size_t smd, smu;
 };
 
-// Enqueue one Lanczos step (the step index lives in device memory).  j_host is only used
-// for the addresses of the multi-GPU all-reduces (eager mode).
+// Enqueue one Lanczos step (the step index lives in device memory).  j_host only picks the
+// z buffer of the step (z_j alternates between two buffers).
 template <typename V>
 void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     Cache& c = *pl.c;
@@ -509,6 +534,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(step_prologue_kernel, pl.gm, 256, 0, s, st, pl.k, c.tol, pl.m, (const double*)c.z[0],
                     (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.mean_y);
+        LOVE_LAUNCH(clear_acc_kernel, 1, 32, 0, s, st, pl.k);
     }
     {
         ProfScope ps(LOVE_PROF_SCATTER, s);
@@ -525,11 +551,11 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_GATHER, s);
-        launch_gather<V>(c, zj, Q, ref, r, st.alpha_acc, s, pl.fold ? &pl.rs : nullptr);
+        launch_gather<V>(c, zj, Q, ref, r, st.alpha_cur, s, pl.fold ? &pl.rs : nullptr);
     }
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
-        allreduce_sum(c, st.alpha_acc + j_host, 1, true, s);
+        allreduce_sum(c, st.alpha_cur, 1, true, s);
     }
     for (int pass = 0; pass < pl.P; ++pass) {
         {
@@ -543,9 +569,9 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
                 LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 2>), (int)ceil_div(pl.ldq / VecT<V>::W, 512), 256,
                             sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
         }
-        if (c.comm != nullptr && j_host < pl.k - 1) {
+        if (c.comm != nullptr) {
             ProfScope ps(LOVE_PROF_COMM, s);
-            allreduce_sum(c, st.c_acc + ((int64_t)pass * pl.k + j_host) * (pl.k + 1), j_host + 1, true, s);
+            allreduce_sum(c, st.c_cur + (int64_t)pass * (pl.k + 1), pl.k + 1, true, s);
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
@@ -553,9 +579,9 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
                         pass == pl.P - 1 ? 1 : 0, r, st, c.tol, pl.fold ? 1 : 0);
         }
     }
-    if (c.comm != nullptr && j_host < pl.k - 1) {
+    if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
-        allreduce_sum(c, st.beta2_acc + j_host, 1, true, s);
+        allreduce_sum(c, st.beta2_cur, 1, true, s);
     }
 }
 
@@ -597,7 +623,8 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st);
     }
-    const bool graph = c.comm == nullptr && !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    // the step graph is also captured on several GPUs: its all-reduces have fixed addresses
+    const bool graph = !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
     // every kernel of a step starts with pdl_wait(): its launch can overlap the previous
     // kernel's drain (programmatic dependent launch)
     PdlScope pdl(std::getenv("LOVE_NO_PDL") == nullptr);

@@ -236,9 +236,9 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         c->scal = (double*)dalloc(*c, sizeof(double) * nd, s);
         double* p = c->scal;
         LanczosState& st = c->st;
-        st.alpha_acc = p; p += K;
-        st.beta2_acc = p; p += K;
-        st.c_acc = p; p += 2 * K * (K + 1);
+        st.alpha_cur = p; p += 1;
+        st.beta2_cur = p; p += 1;
+        st.c_cur = p; p += 2 * (K + 1);
         st.bnorm2 = p; p += 1;
         st.qscale = p; p += K + 1;
         st.alpha = p; p += K;

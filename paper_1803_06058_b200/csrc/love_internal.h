@@ -45,13 +45,14 @@ struct StepRef {
 __device__ __forceinline__ int step_j(const StepRef& r) { return r.jdev ? *r.jdev : 0; }
 __device__ __forceinline__ bool step_done(const StepRef& r) { return r.flags != nullptr && r.flags[0] != 0; }
 
-// Device-resident Lanczos state (fp64).  Written only by lanczos_scalars_kernel / the
-// finalize kernel; the accumulators are summed into with atomics by the step kernels and
-// (multi-GPU) all-reduced between kernels.
+// Device-resident Lanczos state (fp64).  The current step's accumulators live at fixed
+// addresses (summed into with atomics by the step kernels, all-reduced between kernels on
+// several GPUs, so a captured step graph can be replayed) and are cleared once the step's
+// scalars are finalised.
 struct LanczosState {
-    double* alpha_acc;     // [k]        q_j^T A q_j partial sums
-    double* beta2_acc;     // [k]        ||q~_{j+1}||^2 partial sums
-    double* c_acc;         // [2][k][k+1] reorthogonalisation dots (pass 0 and pass 1)
+    double* alpha_cur;     // [1]        q_j^T A q_j of the current step
+    double* beta2_cur;     // [1]        ||q~_{j+1}||^2 of the current step
+    double* c_cur;         // [2][k+1]   reorthogonalisation dots of the current step (passes 0, 1)
     double* bnorm2;        // [1]        ||b||^2
     double* qscale;        // [k+1]      1/||q~_j|| (lazy normalisation of Q's columns)
     double* alpha;         // [k]

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
     }
     if (alpha_base != nullptr) {
         alpha = block_sum(alpha, red);
-        if (threadIdx.x == 0) atomicAdd(alpha_base + j, alpha);
+        if (threadIdx.x == 0) atomicAdd(alpha_base, alpha);
     }
 }
 
