@@ -340,18 +340,21 @@ __device__ __forceinline__ void finalize_index(const LanczosState& st, int i, in
     if (fl[1] <= i || fl[2] || fl[3]) return;
     const double al = st.alpha_cur[0];
     const double amax = fmax(st.amax_bmax[0], fabs(al));
-    const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
-    const double piv = al - lsub * lsub;
-    if (!(piv > 0.0)) {
-        fl[2] = 1;
-        fl[0] = 1;
-        fl[1] = i;
-        return;
+    double ld = 1.0;
+    if (st.chol) {                                  // row i of the Cholesky of T
+        const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
+        const double piv = al - lsub * lsub;
+        if (!(piv > 0.0)) {
+            fl[2] = 1;
+            fl[0] = 1;
+            fl[1] = i;
+            return;
+        }
+        ld = sqrt(piv);
+        st.Ld[i] = ld;
+        st.g[i] = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
     }
-    const double ld = sqrt(piv);
     st.alpha[i] = al;
-    st.Ld[i] = ld;
-    st.g[i] = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
     st.amax_bmax[0] = amax;
     if (i + 1 == k) {
         fl[0] = 1;
@@ -366,7 +369,7 @@ __device__ __forceinline__ void finalize_index(const LanczosState& st, int i, in
         fl[1] = i + 1;
     } else {
         st.beta[i] = b;
-        st.Ls[i] = b / ld;
+        if (st.chol) st.Ls[i] = b / ld;
         st.qscale[i + 1] = 1.0 / b;
     }
 }
@@ -732,6 +735,23 @@ void eq4_impl(Cache& c, cudaStream_t s) {
 }
 
 }  // namespace
+
+// One CGS pass of the reorthogonalisation of step *st.jdev on an fp64 basis (used by the
+// sampling-cache Lanczos, sample.cu): dots then update; the last pass's update finalises
+// the step's scalars (no Cholesky when st.chol == 0) and advances the step index.
+void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int64_t n, int k, int pass,
+                            int last_pass, const double* r, double tol, cudaStream_t s) {
+    const size_t smd = sizeof(double) * 8 * (k + 1);
+    ensure_smem((const void*)reorth_dots_sweep_kernel<double, 1>, smd);
+    LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), (int)ceil_div(ldq / 2, 256), 256, smd, s, (const double*)Q, ldq,
+                k, pass, r, st);
+    const int gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ldq / 2, 256), 148 * 8));
+    const size_t smu = sizeof(double) * (k + 1);
+    ensure_smem((const void*)reorth_update_kernel<double>, smu);
+    LOVE_LAUNCH(reorth_update_kernel<double>, gu, 256, smu, s, Q, ldq, n, k, pass, last_pass, r, st, tol, 1);
+}
+
+void launch_init_q0(const LanczosState& st, cudaStream_t s) { LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st); }
 
 void run_lanczos(Cache& c, cudaStream_t s) {
     if (c.precision == LOVE_FP64) lanczos_impl<double>(c, s);

@@ -64,6 +64,7 @@ struct LanczosState {
     int* flags;            // [4]        done, k_eff, notpd, zero_probe
     int* jdev;             // [1]        current step index j
     int* step_ctr;         // [1]        CTAs done in the step's last kernel (advance_step)
+    int chol = 1;          // finalise the Cholesky row of T too (0: sampling Lanczos on M, reading A15)
     // fused (one-read) mode
     double* AB;            // [k][2][k+1] Gram sums A_i = Q~_i^T r~_j, B_i = Q~_i^T Q~_j of pass j
     double* cvec;          // [k+1]      reorthogonalisation coefficients on Q~_i for the next pass
@@ -236,6 +237,9 @@ void setup_kuu(Cache& c, cudaStream_t s);
 void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
+void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int64_t n, int k, int pass,
+                            int last_pass, const double* r, double tol, cudaStream_t s);
+void launch_init_q0(const LanczosState& st, cudaStream_t s);
 void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu
 void setup_fused(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
