@@ -99,8 +99,10 @@ enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ =
  * returned caches are identical replicas.  nccl_unique_id: 128 bytes (HOST memory) from
  * love_nccl_unique_id on rank 0, broadcast by the caller.  NULL love_dist => one GPU, no
  * collectives.  world == 1 with an id runs the sharded code path with a one-rank
- * communicator (every all-reduce an identity).  Errors: LOVE_ERR_ARG (rank/world/id
- * inconsistent), LOVE_ERR_NCCL (NCCL missing or failing). */
+ * communicator (every all-reduce an identity).  The library keeps one communicator per
+ * (id, rank, world, device) for the life of the process, so repeated builds with the same id
+ * bootstrap NCCL once.  Errors: LOVE_ERR_ARG (rank/world/id inconsistent), LOVE_ERR_NCCL
+ * (NCCL missing or failing). */
 typedef struct {
     int32_t rank;
     int32_t world;

@@ -9,6 +9,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "love_internal.h"
 
@@ -86,21 +88,40 @@ love_status nccl_get_unique_id(void* out128) {
     return LOVE_OK;
 }
 
+// Communicators are created once per (unique id, rank, world, device) and shared by every
+// cache built with that id: ncclCommInitRank is a collective bootstrap costing milliseconds,
+// far more than a build, so a process that builds repeatedly (training loops, the benchmark)
+// passes the same id and pays it once.  They live until the process exits.
+struct CommKey {
+    std::string id;
+    int rank, world, device;
+    bool operator==(const CommKey& o) const {
+        return id == o.id && rank == o.rank && world == o.world && device == o.device;
+    }
+};
+
 love_status nccl_comm_init(Cache& c, const void* id128) {
     NcclApi& a = api();
     if (!a.ok) throw LoveError{LOVE_ERR_NCCL, a.why};
+    static std::mutex mu;
+    static std::vector<std::pair<CommKey, NcclComm>> comms;
+    const CommKey key{std::string(reinterpret_cast<const char*>(id128), 128), c.rank, c.world, c.device};
+    std::lock_guard<std::mutex> g(mu);
+    for (const auto& kv : comms)
+        if (kv.first == key) {
+            c.comm = kv.second;
+            return LOVE_OK;
+        }
     NcclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
     NcclComm comm = nullptr;
     nccl_check(a.CommInitRank(&comm, c.world, id, c.rank), "ncclCommInitRank");
+    comms.emplace_back(key, comm);
     c.comm = comm;
     return LOVE_OK;
 }
 
-void nccl_comm_destroy(Cache& c) {
-    if (c.comm && api().ok) api().CommDestroy((NcclComm)c.comm);
-    c.comm = nullptr;
-}
+void nccl_comm_destroy(Cache& c) { c.comm = nullptr; }   // shared; see nccl_comm_init
 
 void allreduce_sum(const Cache& c, void* buf, int64_t count, bool is_double, cudaStream_t s) {
     if (c.comm == nullptr || count <= 0) return;
