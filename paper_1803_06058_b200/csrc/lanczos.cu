@@ -17,9 +17,6 @@
 
 #include "love_internal.h"
 
-#ifndef LOVE_DOTS_U
-#define LOVE_DOTS_U 8
-#endif
 #ifndef LOVE_SWEEP_NB
 #define LOVE_SWEEP_NB 1
 #endif
@@ -152,76 +149,6 @@ __device__ __forceinline__ void load_src(const V* __restrict__ Q, int64_t ldq, c
         vload<V>(Q + (int64_t)(j + 1) * ldq + p, x);
 #pragma unroll
         for (int e = 0; e < W; ++e) out[e] = (double)x[e];
-    }
-}
-
-// ---- reorthogonalisation dots: c[i] += q_i^T src over this CTA's rows, i = 0..j.
-// One row tile per CTA (~4 CTAs per SM).  Work units (column, row split) are spread over the
-// warps -- a column gets several warps while j is small -- and each lane keeps U 16-byte
-// loads of Q~ in flight against the tile of src staged in shared memory.
-template <typename V>
-__global__ void __launch_bounds__(256) reorth_dots_kernel(const V* __restrict__ Q, int64_t ldq,
-                                                          int64_t tile_rows, int k, int pass,
-                                                          const V* __restrict__ r, LanczosState st) {
-    pdl_wait();
-    constexpr int W = VecT<V>::W;
-    constexpr int U = LOVE_DOTS_U;
-    extern __shared__ __align__(16) double smd[];
-    const int j = *st.jdev;
-    if (st.flags[0] || j >= k - 1) return;
-    const int from_r = pass == 0;
-    const int ncols = j + 1;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int S = ncols < nw ? nw / ncols : 1;            // row splits per column
-    double* csum = smd;                                   // [S][ncols]
-    V* src = reinterpret_cast<V*>(smd + round_up((k + 1) * nw, 2));    // [tile_rows]
-    const int64_t row0 = (int64_t)blockIdx.x * tile_rows;
-    const int64_t rows = min(tile_rows, ldq - row0);
-    if (rows <= 0) return;
-    const double sj = st.qscale[j];
-    const double aj = st.alpha_cur[0] * sj;
-    const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
-    const int nchunk = (int)(rows / W);
-    for (int q = threadIdx.x; q < nchunk; q += blockDim.x) {
-        double v[W];
-        load_src<V>(Q, ldq, r, from_r, j, aj, bj1, row0 + (int64_t)q * W, v);
-#pragma unroll
-        for (int e = 0; e < W; ++e) src[q * W + e] = (V)v[e];
-    }
-    __syncthreads();
-    for (int unit = wid; unit < ncols * S; unit += nw) {
-        const int col = unit % ncols, sp = unit / ncols;
-        const int lo = (int)((int64_t)nchunk * sp / S), hi = (int)((int64_t)nchunk * (sp + 1) / S);
-        const V* qc = Q + (int64_t)col * ldq + row0;
-        V part = V(0);
-        for (int q0 = lo + lane; q0 < hi; q0 += 32 * U) {
-            V a[U][W];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int q = q0 + 32 * u;
-                if (q < hi) vload<V>(qc + q * W, a[u]);
-                else
-#pragma unroll
-                    for (int e = 0; e < W; ++e) a[u][e] = V(0);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int q = min(q0 + 32 * u, hi - 1);
-                V b[W];
-                vload<V>(src + q * W, b);
-#pragma unroll
-                for (int e = 0; e < W; ++e) part += a[u][e] * b[e];
-            }
-        }
-        const double dp = warp_sum((double)part);
-        if (lane == 0) csum[sp * ncols + col] = dp;
-    }
-    __syncthreads();
-    double* __restrict__ c_out = st.c_cur + (int64_t)pass * (k + 1);
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
-        double tot = 0.0;
-        for (int sp = 0; sp < S; ++sp) tot += csum[sp * ncols + i];
-        atomicAdd(&c_out[i], tot * st.qscale[i]);
     }
 }
 
@@ -483,12 +410,6 @@ __global__ void rc_transpose_kernel(const double* __restrict__ Rcc, int m, int k
     }
 }
 
-// rows per dots tile: ~4 CTAs per SM, a multiple of 32 vector chunks
-template <typename V>
-int64_t reorth_tile_rows(int64_t ldq) {
-    const int64_t quantum = 32 * VecT<V>::W;
-    return std::max<int64_t>(quantum, round_up(ceil_div(ldq, 148 * 4), quantum));
-}
 
 
 
@@ -514,13 +435,12 @@ __global__ void stream_rc_kernel(RcStream rs) {
 template <typename V>
 struct StepPlan {
     Cache* c;
-    int k, m, P, mean_y, gm, gr, gu;
+    int k, m, P, mean_y, gm, gu;
     bool fold;                    // single GPU: scalars in the update's last CTA, cache column in the gather
     RcStream rs;
-    int dots_mode;                // 1 (default): column sweep, 1 chunk per thread; 2: 2 chunks; 0: row tiles
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
-    int64_t ldq, tile_rows;
-    size_t smd, smu;
+    int64_t ldq;
+    size_t smu;
 };
 
 // Enqueue one Lanczos step (the step index lives in device memory).  j_host only picks the
@@ -563,14 +483,8 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     for (int pass = 0; pass < pl.P; ++pass) {
         {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
-            if (pl.dots_mode == 0)
-                LOVE_LAUNCH(reorth_dots_kernel<V>, pl.gr, 256, pl.smd, s, Q, pl.ldq, pl.tile_rows, pl.k, pass, r, st);
-            else if (pl.dots_mode == 1)
-                LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
-                            sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
-            else
-                LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 2>), (int)ceil_div(pl.ldq / VecT<V>::W, 512), 256,
-                            sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
+            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
+                        sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
         }
         if (c.comm != nullptr) {
             ProfScope ps(LOVE_PROF_COMM, s);
@@ -596,21 +510,15 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.m = c.g.m_total;
     pl.P = c.reorth_passes;
     pl.mean_y = c.probe == LOVE_PROBE_Y;
-    pl.dots_mode = std::getenv("LOVE_DOTS") ? std::atoi(std::getenv("LOVE_DOTS")) : 1;
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
     pl.fold = c.comm == nullptr && std::getenv("LOVE_NO_FOLD") == nullptr;
     pl.rs = RcStream{c.st, (const double*)c.z[0], (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.m,
                      pl.mean_y};
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
-    pl.tile_rows = reorth_tile_rows<V>(c.ldq);
-    pl.gr = (int)ceil_div(c.ldq, pl.tile_rows);
     pl.gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.ldq / VecT<V>::W, 256), 148 * 8));
-    pl.smd = sizeof(double) * round_up((pl.k + 1) * 8, 2) + sizeof(V) * pl.tile_rows;
     pl.smu = sizeof(double) * (pl.k + 1);
-    ensure_smem((const void*)reorth_dots_kernel<V>, pl.smd);
     ensure_smem((const void*)reorth_dots_sweep_kernel<V, 1>, sizeof(double) * 8 * (pl.k + 1));
-    ensure_smem((const void*)reorth_dots_sweep_kernel<V, 2>, sizeof(double) * 8 * (pl.k + 1));
     ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
     const LanczosState& st = c.st;
     {
