@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lanczos", default="full", choices=["full", "partial"],
+                    help="partial: opt-in partial reorthogonalisation (SURVEY 8(f) NEXT #1); the default "
+                         "hot path reorthogonalises fully every step")
     return ap.parse_args()
 
 
@@ -257,6 +260,8 @@ def main():
     lib = _abi.load()
     if p.kind == "additive":                      # Eq. 16 block forms (NEXT #2): no sampling cache
         kw.pop("k_sample")
+    if args.lanczos == "partial":
+        kw["lanczos_mode"] = "partial"
 
     def build(Xd, yd):
         if p.kind == "additive":
@@ -294,7 +299,7 @@ def main():
     launches0 = launch_count()
     total_ms = 0.0
     build_ms, query_ms, sample_ms = [], [], []
-    k_pad = 0
+    k_pad, n_reorth = 0, 0
     barrier()
     for _ in range(args.steps):
         flush.zero_()
@@ -312,7 +317,8 @@ def main():
         build_ms.append(e0.elapsed_time(e1))
         query_ms.append(e1.elapsed_time(e2))
         sample_ms.append(e2.elapsed_time(e3))
-        k_pad = c.info()["k_pad"]
+        inf = c.info()
+        k_pad, n_reorth = inf["k_pad"], inf["n_reorth_steps"]
         c.free()
     barrier()
     launches = launch_count() - launches0
@@ -430,6 +436,7 @@ def main():
             "query_variances_per_s": p.t / (float(np.mean(query_ms)) / 1e3),
             "build_roofline": build_rf, "query_roofline": query_rf,
             "sampling": sampling,
+            "lanczos": {"reorthogonalisation": args.lanczos, "steps_reorthogonalised": n_reorth},
             "phase_ms_per_step": {k: round(v, 4) for k, v in prof_ms.items() if v > 0},
             "profiled_step_ms": prof_step_ms,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LOVE_ABI_VERSION 2
+#define LOVE_ABI_VERSION 3
 
 typedef struct love_cache love_cache;   /* opaque */
 
@@ -83,16 +83,23 @@ typedef struct {
     int32_t k_sample;       /* k' of the sampling cache; 0 => no sampling cache */
     int32_t lanczos_mode;   /* LOVE_LANCZOS_AUTO (0) | LOVE_LANCZOS_TWO_PASS (1): classical Gram-Schmidt,
                                Q read twice per step | LOVE_LANCZOS_ONE_READ (2, fp32 only): the
-                               lagged one-read fused pass (lanczos_fused.cu) */
+                               lagged one-read fused pass (lanczos_fused.cu) | LOVE_LANCZOS_PARTIAL (3,
+                               one GPU, fp32): partial reorthogonalisation (SURVEY 8(f)
+                               NEXT #1): Simon's omega recurrence estimates q_{j+1}^T q_i from T; one CGS
+                               pass runs only when it exceeds reorth_tol (and on the following step).
+                               Opt-in: valid far from convergence; near convergence (var << prior)
+                               use the default full reorthogonalisation */
     int32_t var_blocks;     /* LOVE_VAR_BLOCKS_AUTO (0): for d <= 2 the build also stores, per cell c, the
                                fp64 block B_c = (K_UU - Rc Rc^T) restricted to the 4^d stencil nodes of c
                                (SURVEY 8(f) NEXT #3b), and love_predict_var returns w*^T B_c w* (the same
                                Eq. 10 value, reassociated: 4^d(4^d+1)/2 doubles read per query instead of
                                4^d rows of Rc, and the cancellation happens in fp64) |
                                LOVE_VAR_BLOCKS_OFF (1): variances from the Rc rows */
+    double reorth_tol;      /* LOVE_LANCZOS_PARTIAL only: reorthogonalise when the estimated loss of
+                               orthogonality max_i |q_{j+1}^T q_i| exceeds it; 0 => sqrt(eps) of V */
 } love_opts;
 enum { LOVE_VAR_BLOCKS_AUTO = 0, LOVE_VAR_BLOCKS_OFF = 1 };
-enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ = 2 };
+enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ = 2, LOVE_LANCZOS_PARTIAL = 3 };
 
 /* Data-parallel sharding of the training points.  Every rank calls
  * love_build_cache with its own X/y shard and identical grid/kernel/sigma^2/k/opts; the
@@ -123,6 +130,9 @@ typedef struct {
     const double* beta;     /* HOST, k_eff-1 entries: off-diagonal of T_k */
     int64_t n_negative_var; /* variance queries that returned < 0 (returned raw, reading A20) */
     int64_t n_out_of_range; /* query points outside the grid (NaN returned) */
+    int32_t n_reorth_steps; /* Lanczos steps that ran the reorthogonalisation (all but the last one,
+                               except in LOVE_LANCZOS_PARTIAL) */
+    int32_t reserved0;
 } love_info;
 
 /* ---------------------------------------------------------------------------------------

@@ -31,7 +31,8 @@ class love_rbf(ctypes.Structure):
 class love_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("probe", ctypes.c_int32), ("prior", ctypes.c_int32),
                 ("reorth_passes", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
-                ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32), ("var_blocks", ctypes.c_int32)]
+                ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32), ("var_blocks", ctypes.c_int32),
+                ("reorth_tol", ctypes.c_double)]
 
 
 class love_axis(ctypes.Structure):
@@ -51,7 +52,7 @@ class love_info(ctypes.Structure):
                 ("m_total", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("b_norm", ctypes.c_double),
                 ("alpha", ctypes.POINTER(ctypes.c_double)), ("beta", ctypes.POINTER(ctypes.c_double)),
-                ("n_negative_var", ctypes.c_int64), ("n_out_of_range", ctypes.c_int64)]
+                ("n_negative_var", ctypes.c_int64), ("n_out_of_range", ctypes.c_int64), ("n_reorth_steps", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/love.h declares

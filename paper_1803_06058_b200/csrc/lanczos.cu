@@ -159,12 +159,14 @@ __device__ __forceinline__ void load_src(const V* __restrict__ Q, int64_t ldq, c
 // 8b + (l & 7) summed over the warp; lanes 0..7 park it in shared memory (fp64).
 template <typename V, int CPT>
 __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restrict__ Q, int64_t ldq, int k, int pass,
-                                                                const V* __restrict__ r, LanczosState st) {
+                                                                const V* __restrict__ r, LanczosState st,
+                                                                const int* __restrict__ gate) {
     pdl_wait();
     constexpr int W = VecT<V>::W;
     extern __shared__ __align__(16) double smd[];
     const int j = *st.jdev;
     if (st.flags[0] || j >= k - 1) return;
+    if (gate != nullptr && !*gate) return;
     const int from_r = pass == 0;
     double* __restrict__ c_out = st.c_cur + (int64_t)pass * (k + 1);
     const int ncols = j + 1;
@@ -333,25 +335,34 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
 }
 
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
+// update modes: accumulate beta^2 / advance the step (the step's last kernel) / three-term
+// only (no reorthogonalisation columns; partial reorthogonalisation)
+constexpr int kUpdBeta = 1, kUpdAdvance = 2, kUpd3T = 4;
+
 template <typename V>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
-                                                            int pass, int last_pass, const V* __restrict__ r,
-                                                            LanczosState st, double tol, int fold) {
+                                                            int pass, int mode, const V* __restrict__ r,
+                                                            LanczosState st, double tol, int fold,
+                                                            const int* __restrict__ gate) {
     pdl_wait();
     constexpr int W = VecT<V>::W;
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
     __shared__ double red[32];
     const int j = *st.jdev;
     // the last pass's update is the last kernel of step j: its last CTA to finish advances
-    // the device step index (every CTA has read j by then), also on the early-exit path
+    // the device step index (every CTA has read j by then), also on the early-exit paths
     if (st.flags[0] || j >= k - 1) {
-        if (last_pass) advance_step(st, j, fold && j == k - 1, k, tol);
+        if (mode & kUpdAdvance) advance_step(st, j, fold && j == k - 1, k, tol);
+        return;
+    }
+    if (gate != nullptr && !*gate) {           // partial: no reorthogonalisation this step
+        if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
         return;
     }
     const int from_r = pass == 0;
     const double* __restrict__ c_in = st.c_cur + (int64_t)pass * (k + 1);
-    double* __restrict__ beta2_out = last_pass ? st.beta2_cur : nullptr;
-    const int ncols = j + 1;
+    double* __restrict__ beta2_out = (mode & kUpdBeta) ? st.beta2_cur : nullptr;
+    const int ncols = (mode & kUpd3T) ? 0 : j + 1;
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) cf[i] = c_in[i] * st.qscale[i];
     __syncthreads();
     const double sj = st.qscale[j];
@@ -389,8 +400,8 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     if (beta2_out != nullptr) {
         b2 = block_sum(b2, red);
         if (threadIdx.x == 0) atomicAdd(beta2_out, b2);
-        advance_step(st, j, fold != 0, k, tol);
     }
+    if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
 }
 
 // Rc (fp64, m x k_eff column-major) -> V, m x k_pad row-major (zero padded)
@@ -412,6 +423,66 @@ __global__ void rc_transpose_kernel(const double* __restrict__ Rcc, int m, int k
 
 
 
+
+// ---- partial reorthogonalisation.  Simon's recurrence
+// estimates omega_{j+1,i} ~ q_{j+1}^T q_i from T alone, after the three-term vector
+// r' = r - alpha_j q_j - beta_{j-1} q_{j-1} and its norm beta_j (three-term) are known:
+//   beta_j omega_{j+1,i} = beta_i omega_{j,i+1} + (alpha_i - alpha_j) omega_{j,i}
+//                          + beta_{i-1} omega_{j,i-1} - beta_{j-1} omega_{j-1,i}  +/- eps (beta_i + beta_j)
+//   omega_{j+1,j} = eps, omega_{j+1,j+1} = 1.
+// If max_i |omega_{j+1,i}| > tol, q~_{j+1} gets one CGS pass against Q_j (and so does the
+// next vector); the estimates of both rows are then reset to eps.  omega rows rotate over
+// three slots: row j lives in slot j % 3.
+__global__ void __launch_bounds__(256) pro_decide_kernel(LanczosState st, int k) {
+    pdl_wait();
+    __shared__ double red[32];
+    __shared__ int reo;
+    const int j = *st.jdev;
+    if (st.flags[0] || j >= k - 1) {
+        if (threadIdx.x == 0) st.pro[0] = 0;
+        return;
+    }
+    const double eps = st.pro_eps;
+    const double bj = sqrt(st.beta2_cur[0]);
+    const double aj = st.alpha_cur[0];
+    const double bjm1 = j > 0 ? st.beta[j - 1] : 0.0;
+    const int64_t ld = k + 1;
+    double* __restrict__ wp = st.omega + ((j + 2) % 3) * ld;    // row j - 1
+    double* __restrict__ wc = st.omega + (j % 3) * ld;          // row j
+    double* __restrict__ wn = st.omega + ((j + 1) % 3) * ld;    // row j + 1
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) {
+        double t = st.beta[i] * wc[i + 1] + (st.alpha[i] - aj) * wc[i] - bjm1 * wp[i];
+        if (i > 0) t += st.beta[i - 1] * wc[i - 1];
+        const double w = (t + copysign(eps * (st.beta[i] + bj), t)) / bj;
+        wn[i] = w;
+        mx = fmax(mx, fabs(w));
+    }
+    mx = warp_max(mx);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        const int force = st.pro[1];
+        const int r = force || !(m <= st.pro_tol) || !(bj > 0.0);
+        reo = r;
+        st.pro[0] = r;
+        st.pro[1] = r ? !force : 0;
+        if (r) {
+            st.pro[2] += 1;
+            st.beta2_cur[0] = 0.0;       // the reorthogonalising update recomputes beta_j^2
+        }
+    }
+    __syncthreads();
+    if (reo) {
+        for (int i = threadIdx.x; i <= j; i += blockDim.x) wn[i] = eps;
+        for (int i = threadIdx.x; i < j; i += blockDim.x) wc[i] = eps;
+    } else if (threadIdx.x == 0) {
+        wn[j] = eps;
+    }
+    if (threadIdx.x == 0) wn[j + 1] = 1.0;
+}
 
 // q_0 = b / ||b|| (scale of column 0) or the zero-probe flag (folded-prologue path)
 __global__ void init_q0_kernel(LanczosState st) {
@@ -439,6 +510,7 @@ struct StepPlan {
     bool fold;                    // single GPU: scalars in the update's last CTA, cache column in the gather
     RcStream rs;
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
+    bool partial;                 // partial reorthogonalisation (single GPU)
     int64_t ldq;
     size_t smu;
 };
@@ -480,11 +552,35 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_COMM, s);
         allreduce_sum(c, st.alpha_cur, 1, true, s);
     }
+    if (pl.partial) {
+        // three-term vector and its norm, the omega recurrence, then (gated) one CGS pass of
+        // q~_{j+1} against Q_j whose update finalises the step
+        {
+            ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
+            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0, kUpdBeta | kUpd3T, r,
+                        st, c.tol, 1, (const int*)nullptr);
+        }
+        {
+            ProfScope ps(LOVE_PROF_SCALARS, s);
+            LOVE_LAUNCH(pro_decide_kernel, 1, 256, 0, s, st, pl.k);
+        }
+        {
+            ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
+            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
+                        sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, 1, r, st, (const int*)st.pro);
+        }
+        {
+            ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
+            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 1,
+                        kUpdBeta | kUpdAdvance, r, st, c.tol, 1, (const int*)st.pro);
+        }
+        return;
+    }
     for (int pass = 0; pass < pl.P; ++pass) {
         {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
             LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
-                        sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st);
+                        sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st, (const int*)nullptr);
         }
         if (c.comm != nullptr) {
             ProfScope ps(LOVE_PROF_COMM, s);
@@ -493,7 +589,8 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
             LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
-                        pass == pl.P - 1 ? 1 : 0, r, st, c.tol, pl.fold ? 1 : 0);
+                        pass == pl.P - 1 ? kUpdBeta | kUpdAdvance : 0, r, st, c.tol, pl.fold ? 1 : 0,
+                        (const int*)nullptr);
         }
     }
     if (c.comm != nullptr) {
@@ -512,6 +609,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.mean_y = c.probe == LOVE_PROBE_Y;
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
     pl.fold = c.comm == nullptr && std::getenv("LOVE_NO_FOLD") == nullptr;
+    pl.partial = c.partial;
     pl.rs = RcStream{c.st, (const double*)c.z[0], (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.m,
                      pl.mean_y};
     pl.ldq = c.ldq;
@@ -652,11 +750,12 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
     const size_t smd = sizeof(double) * 8 * (k + 1);
     ensure_smem((const void*)reorth_dots_sweep_kernel<double, 1>, smd);
     LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), (int)ceil_div(ldq / 2, 256), 256, smd, s, (const double*)Q, ldq,
-                k, pass, r, st);
+                k, pass, r, st, (const int*)nullptr);
     const int gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ldq / 2, 256), 148 * 8));
     const size_t smu = sizeof(double) * (k + 1);
     ensure_smem((const void*)reorth_update_kernel<double>, smu);
-    LOVE_LAUNCH(reorth_update_kernel<double>, gu, 256, smu, s, Q, ldq, n, k, pass, last_pass, r, st, tol, 1);
+    LOVE_LAUNCH(reorth_update_kernel<double>, gu, 256, smu, s, Q, ldq, n, k, pass,
+                last_pass ? kUpdBeta | kUpdAdvance : 0, r, st, tol, 1, (const int*)nullptr);
 }
 
 void launch_init_q0(const LanczosState& st, cudaStream_t s) { LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st); }

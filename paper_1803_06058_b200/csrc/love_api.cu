@@ -180,10 +180,16 @@ Cache* begin_build(const love_opts& o, double sigma2, int64_t n_local, int32_t& 
         c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (o.precision == LOVE_FP64 ? 2 : 1);
         int mode = o.lanczos_mode;
         if (const char* e = std::getenv("LOVE_LANCZOS_MODE")) mode = std::atoi(e);
-        if (mode < 0 || mode > 2) throw LoveError{LOVE_ERR_ARG, "bad lanczos_mode"};
+        if (mode < 0 || mode > 3) throw LoveError{LOVE_ERR_ARG, "bad lanczos_mode"};
         if (mode == LOVE_LANCZOS_ONE_READ && o.precision != LOVE_FP32)
             throw LoveError{LOVE_ERR_ARG, "the one-read Lanczos pass is fp32 only"};
         c->fused = mode == LOVE_LANCZOS_ONE_READ;
+        c->partial = mode == LOVE_LANCZOS_PARTIAL;
+        if (c->partial && dist && (dist->world > 1 || dist->nccl_unique_id))
+            throw LoveError{LOVE_ERR_ARG, "partial reorthogonalisation runs on one GPU"};
+        if (c->partial && o.precision != LOVE_FP32)
+            throw LoveError{LOVE_ERR_ARG, "partial reorthogonalisation is fp32 only"};
+        if (!(o.reorth_tol >= 0.0)) throw LoveError{LOVE_ERR_ARG, "reorth_tol must be >= 0"};
         c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
         c->k_sample_req = o.k_sample;
         c->n = n_local;
@@ -251,6 +257,15 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         st.flags = (int*)dalloc(*c, sizeof(int) * 8, s);
         st.jdev = st.flags + 4;
         st.step_ctr = st.flags + 5;
+        if (c->partial) {
+            st.omega = (double*)dalloc(*c, sizeof(double) * 3 * (K + 1), s);
+            st.pro = (int*)dalloc(*c, sizeof(int) * 4, s);
+            const double one = 1.0;                      // omega_{0,0} = q_0^T q_0
+            cuda_check(cudaMemcpyAsync(st.omega, &one, sizeof(double), cudaMemcpyHostToDevice, s), "omega init");
+            const double eps = c->precision == LOVE_FP64 ? 1.1102230246251565e-16 : 5.9604644775390625e-08;
+            st.pro_eps = eps;
+            st.pro_tol = o.reorth_tol > 0.0 ? o.reorth_tol : std::sqrt(eps);
+        }
         LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
     }
 
@@ -271,6 +286,12 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
     c->k_eff = hfl[1];
     c->b_norm = std::sqrt(bn2);
+    c->n_reorth_steps = std::max(c->k_eff - 1, 0);
+    if (c->partial) {
+        int pro[4];
+        cuda_check(cudaMemcpy(pro, c->st.pro, sizeof(pro), cudaMemcpyDeviceToHost), "pro d2h");
+        c->n_reorth_steps = pro[2];
+    }
     c->h_alpha.resize(c->k_eff);
     c->h_beta.resize(std::max(c->k_eff - 1, 0));
     cuda_check(cudaMemcpy(c->h_alpha.data(), c->st.alpha, sizeof(double) * c->k_eff, cudaMemcpyDeviceToHost),
@@ -426,7 +447,7 @@ love_status love_build_cache_additive(const love_axis* axes, int32_t d, double s
         if (o.k_sample > 0) throw LoveError{LOVE_ERR_ARG, "k_sample is not supported for additive caches"};
         if (o.lanczos_mode == LOVE_LANCZOS_ONE_READ)
             throw LoveError{LOVE_ERR_ARG, "the one-read Lanczos pass is grid-only"};
-        o.lanczos_mode = LOVE_LANCZOS_TWO_PASS;
+        if (o.lanczos_mode != LOVE_LANCZOS_PARTIAL) o.lanczos_mode = LOVE_LANCZOS_TWO_PASS;
         c = begin_build(o, sigma2, n_local, k, dist, s);
         c->fused = false;
         c->additive = true;
@@ -507,6 +528,7 @@ love_status love_cache_info(const love_cache* cache, love_info* info) {
         cuda_check(cudaMemcpy(cnt, c->counters, sizeof(cnt), cudaMemcpyDeviceToHost), "counters d2h");
         std::memset(info, 0, sizeof(*info));
         info->k_eff = c->k_eff;
+        info->n_reorth_steps = c->n_reorth_steps;
         info->k_pad = c->k_pad;
         info->k_sample_eff = c->k_sample_eff;
         info->precision = c->precision;

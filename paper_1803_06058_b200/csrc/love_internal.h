@@ -65,6 +65,10 @@ struct LanczosState {
     int* jdev;             // [1]        current step index j
     int* step_ctr;         // [1]        CTAs done in the step's last kernel (advance_step)
     int chol = 1;          // finalise the Cholesky row of T too (0: sampling Lanczos on M, reading A15)
+    // partial reorthogonalisation (LOVE_LANCZOS_PARTIAL)
+    double* omega;         // [3][k+1]   rows j-1, j, j+1 of Simon's estimates omega_{j,i} ~ q_j^T q_i
+    int* pro;              // [4]        reorthogonalise this step, force the next, steps reorthogonalised
+    double pro_tol, pro_eps;
     // fused (one-read) mode
     double* AB;            // [k][2][k+1] Gram sums A_i = Q~_i^T r~_j, B_i = Q~_i^T Q~_j of pass j
     double* cvec;          // [k+1]      reorthogonalisation coefficients on Q~_i for the next pass
@@ -149,6 +153,7 @@ struct Cache {
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)
     // fused (one-read) Lanczos mode
     bool fused = false;
+    bool partial = false;                // LOVE_LANCZOS_PARTIAL
     int tile_cap = 0;                    // max points per fused-pass tile
     int64_t n_tiles = 0;
     int* tile_first = nullptr;           // [n_tiles+1] first item of each tile
@@ -169,6 +174,7 @@ struct Cache {
 
     // ---------------- results
     int k_eff = 0, k_pad = 0;
+    int n_reorth_steps = 0;
     int k_sample_eff = 0, ks_pad = 0;
     void* S = nullptr;                   // V[m * ks_pad] row-major sampling root
     double b_norm = 0;

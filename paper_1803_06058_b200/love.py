@@ -77,7 +77,7 @@ class LoveCache:
               lengthscale: Sequence[float], outputscale: float, sigma2: float, k: int,
               precision: str = "fp32", prior: str = "ski", k_sample: int = 0, probe: str = "y",
               reorth_passes: int = 0, breakdown_tol: float = 0.0, lanczos_mode: str = "auto",
-              var_blocks: str = "auto",
+              var_blocks: str = "auto", reorth_tol: float = 0.0,
               rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
               stream=None) -> "LoveCache":
         d = len(m)
@@ -98,7 +98,8 @@ class LoveCache:
         o.reorth_passes = int(reorth_passes)
         o.breakdown_tol = float(breakdown_tol)
         o.k_sample = int(k_sample)
-        o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2}[lanczos_mode]
+        o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2, "partial": 3}[lanczos_mode]
+        o.reorth_tol = float(reorth_tol)
         o.var_blocks = {"auto": 0, "off": 1}[var_blocks]
         dist = None
         idbuf = None
@@ -199,7 +200,8 @@ class LoveCache:
             n_global=inf.n_global, m_total=inf.m_total, n_items=inf.n_items, b_norm=inf.b_norm,
             alpha=np.array([inf.alpha[i] for i in range(k)]),
             beta=np.array([inf.beta[i] for i in range(max(k - 1, 0))]),
-            n_negative_var=inf.n_negative_var, n_out_of_range=inf.n_out_of_range)
+            n_negative_var=inf.n_negative_var, n_out_of_range=inf.n_out_of_range,
+            n_reorth_steps=inf.n_reorth_steps)
 
     def export(self, what: str, stream=None) -> torch.Tensor:
         code = {"rc": _abi.LOVE_EXPORT_RC, "mean": _abi.LOVE_EXPORT_MEAN, "S": _abi.LOVE_EXPORT_S,
