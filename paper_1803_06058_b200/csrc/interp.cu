@@ -162,10 +162,11 @@ template <typename V>
 __global__ void gather_sorted_kernel(int d, const int* __restrict__ perm, int64_t n,
                                      const double* __restrict__ frac64, const double* __restrict__ y,
                                      V* __restrict__ f0, V* __restrict__ f1, V* __restrict__ f2,
-                                     V* __restrict__ b) {
+                                     V* __restrict__ b, const int* __restrict__ cell, int* __restrict__ pcell) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         const int o = perm[p];
+        if (pcell != nullptr) pcell[p] = cell[o];
         f0[p] = (V)frac64[(int64_t)o * d + 0];
         if (d > 1) f1[p] = (V)frac64[(int64_t)o * d + 1];
         if (d > 2) f2[p] = (V)frac64[(int64_t)o * d + 2];
@@ -233,11 +234,11 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
         if (c.precision == LOVE_FP64)
             LOVE_LAUNCH(gather_sorted_kernel<double>, grid_for(n, 256), 256, 0, s, c.g.d, c.perm, n,
                         frac64, y, (double*)c.frac[0], (double*)c.frac[1], (double*)c.frac[2],
-                        (double*)b_out);
+                        (double*)b_out, cell, c.pcell);
         else
             LOVE_LAUNCH(gather_sorted_kernel<float>, grid_for(n, 256), 256, 0, s, c.g.d, c.perm, n,
                         frac64, y, (float*)c.frac[0], (float*)c.frac[1], (float*)c.frac[2],
-                        (float*)b_out);
+                        (float*)b_out, cell, c.pcell);
     }
     LOVE_LAUNCH(items_per_cell_kernel, (int)ceil_div(M, 256), 256, 0, s, c.cell_start, M, count);
     exclusive_scan(count, M, c.cell_item_start, s);

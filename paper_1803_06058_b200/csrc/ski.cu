@@ -202,6 +202,75 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
     }
 }
 
+// d = 1 gather, thread per 4 consecutive sorted points (coalesced q / frac / cell loads and r
+// stores; the z stencil loads of neighbouring points hit the same lines):
+//   r_p = sum_l w_l(p) z[cell(p) - 1 + l] + sigma^2 s_j Q~_j[p],   alpha += s_j Q~_j[p] r_p
+// Same per-point arithmetic as gather_kernel<V, 1>; points past n get r = 0.
+template <typename V>
+__device__ __forceinline__ void ld4(const V* __restrict__ p, V o[4]) {
+    if constexpr (sizeof(V) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else {
+        const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+        o[0] = a.x; o[1] = a.y; o[2] = b.x; o[3] = b.y;
+    }
+}
+template <typename V>
+__device__ __forceinline__ void st4(V* __restrict__ p, const V o[4]) {
+    if constexpr (sizeof(V) == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+    } else {
+        reinterpret_cast<double2*>(p)[0] = make_double2(o[0], o[1]);
+        reinterpret_cast<double2*>(p)[1] = make_double2(o[2], o[3]);
+    }
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t nquads, const int* __restrict__ pcell,
+                                                          const V* __restrict__ f0, const double* __restrict__ z,
+                                                          const V* __restrict__ qbase, StepRef ref, double sigma2,
+                                                          V* __restrict__ r, double* __restrict__ alpha_base,
+                                                          RcStream rs, int ngather) {
+    pdl_wait();
+    if ((int)blockIdx.x >= ngather) {
+        stream_rc_column(rs, (blockIdx.x - ngather) * blockDim.x + threadIdx.x, (gridDim.x - ngather) * blockDim.x);
+        return;
+    }
+    __shared__ double red[32];
+    if (step_done(ref)) return;
+    const int j = step_j(ref);
+    const V* __restrict__ q = qbase + j * ref.ld;
+    const double sc = ref.scale[j];
+    const double vsc = sc, vsig = sigma2 * sc;
+    double alpha = 0.0;
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t < nquads) {
+        const int64_t p0 = t * 4;
+        V qv[4], fa[4], rv[4];
+        ld4<V>(q + p0, qv);
+        ld4<V>(f0 + p0, fa);
+        const int4 cl = *reinterpret_cast<const int4*>(pcell + p0);
+        const int cells[4] = {cl.x, cl.y, cl.z, cl.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            rv[u] = V(0);
+            if (p0 + u < n) {
+                double zl[4], w0[4];
+                load_stencil<double, 1>(GridDev{}, z, cells[u] - 1, zl);
+                keys4<double>((double)fa[u], w0);
+                rv[u] = (V)(stencil_dot<double, 1>(w0, w0, w0, zl) + vsig * (double)qv[u]);
+                alpha += (double)(vsc * (double)qv[u]) * (double)rv[u];
+            }
+        }
+        st4<V>(r + p0, rv);
+    }
+    if (alpha_base != nullptr) {
+        alpha = block_sum(alpha, red);
+        if (threadIdx.x == 0) atomicAdd(alpha_base, alpha);
+    }
+}
+
 // d = 1: per-cell stencil moments, one thread per cell, already scaled by q_j's column scale:
 //   Mc[l][c + 2] = s_j * sum_{p in cell c} w_l(p) Q~_j[p]      (l = 0..3, rows of length m + 4)
 // so that (W q_j)[i] = Mc[0][i+3] + Mc[1][i+2] + Mc[2][i+1] + Mc[3][i]  (no atomics, fixed order)
@@ -333,14 +402,22 @@ void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* 
         add_gather<V>(c, z, q, ref, r, alpha_base, s, rsp);
         return;
     }
-    const int64_t ni = c.n_items;
-    const int gi = (int)ceil_div(ni, 256);
     RcStream rs{};
     int extra = 0;
     if (rsp != nullptr) {
         rs = *rsp;
         extra = (int)std::min<int64_t>(ceil_div(rs.m, 256), 148 * 2);
     }
+    if (c.g.d == 1 && c.pcell != nullptr) {
+        const int64_t nq = c.ldq / 4;
+        const int gq = (int)ceil_div(nq, 256);
+        if (gq + extra > 0)
+            LOVE_LAUNCH(gather_pts1_kernel<V>, gq + extra, 256, 0, s, c.n, nq, (const int*)c.pcell,
+                        (const V*)c.frac[0], z, q, ref, c.sigma2, r, alpha_base, rs, gq);
+        return;
+    }
+    const int64_t ni = c.n_items;
+    const int gi = (int)ceil_div(ni, 256);
     if (gi + extra == 0) return;
     const V* f0 = (const V*)c.frac[0];
     const V* f1 = (const V*)c.frac[1];
