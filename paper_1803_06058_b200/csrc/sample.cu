@@ -58,9 +58,10 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
                                                           double* __restrict__ Wout, double* __restrict__ evals) {
     extern __shared__ double sm[];
     const int N = n + (n & 1);                   // even order (a padded zero row/column)
-    double* A = sm;                              // [N][N]
-    double* V = A + N * N;                       // [N][N]
-    double* cs = V + N * N;                      // [N/2] cos
+    const int L = N + 1;                         // row stride: odd, so column sweeps hit distinct banks
+    double* A = sm;                              // [N][L]
+    double* V = A + N * L;                       // [N][L]
+    double* cs = V + N * L;                      // [N/2] cos
     double* sn = cs + N / 2;                     // [N/2] sin
     int* pp = (int*)(sn + N / 2);                // [N/2]
     int* qq = pp + N / 2;                        // [N/2]
@@ -73,8 +74,8 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
             else if (r == c + 1) v = beta[c];
             else if (c == r + 1) v = beta[r];
         }
-        A[e] = v;
-        V[e] = r == c ? 1.0 : 0.0;
+        A[r * L + c] = v;
+        V[r * L + c] = r == c ? 1.0 : 0.0;
     }
     __syncthreads();
     for (int sweep = 0; sweep < 16; ++sweep) {
@@ -83,8 +84,9 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
         double loc = 0.0, dia = 0.0;
         for (int e = threadIdx.x; e < N * N; e += blockDim.x) {
             const int r = e / N, c = e % N;
-            if (r != c) loc += A[e] * A[e];
-            else dia += A[e] * A[e];
+            const double x = A[r * L + c];
+            if (r != c) loc += x * x;
+            else dia += x * x;
         }
         loc = warp_sum(loc);
         dia = warp_sum(dia);
@@ -101,6 +103,7 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
         // are quadratic in it; T' has a cluster of ~0 eigenvalues at breakdown that
         // keeps a tighter test from ever triggering -- measured: all 30 sweeps at 1e-13)
         if (offn <= 1e-22 * (diag_norm + 1e-300)) break;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
         for (int round = 0; round < N - 1; ++round) {
             // round-robin pairs: position 0 fixed, the others rotate
             for (int pi = threadIdx.x; pi < N / 2; pi += blockDim.x) {
@@ -109,50 +112,59 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
                 if (a > b) { const int t = a; a = b; b = t; }
                 pp[pi] = a;
                 qq[pi] = b;
-                const double apq = A[a * N + b];
+                const double apq = A[a * L + b];
                 double c = 1.0, s = 0.0;
                 if (apq != 0.0) {
-                    const double theta = (A[b * N + b] - A[a * N + a]) / (2.0 * apq);
-                    const double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
-                    c = 1.0 / sqrt(t * t + 1.0);
+                    // t = tan of the rotation = sgn(theta) / (|theta| + sqrt(theta^2 + 1)),
+                    // theta = d / (2 apq), d = a_bb - a_aa; written with one sqrt and one division
+                    const double d = A[b * L + b] - A[a * L + a];
+                    const double sg = (d == 0.0 || ((d > 0.0) == (apq > 0.0))) ? 1.0 : -1.0;
+                    const double t = sg * 2.0 * fabs(apq) / (fabs(d) + sqrt(d * d + 4.0 * apq * apq));
+                    c = rsqrt(t * t + 1.0);
                     s = t * c;
                 }
                 cs[pi] = c;
                 sn[pi] = s;
             }
             __syncthreads();
-            // rows: A <- J^T A
-            for (int e = threadIdx.x; e < (N / 2) * N; e += blockDim.x) {
-                const int pi = e / N, col = e % N;
+            // rows: A <- J^T A (a warp per pair, lanes along the row)
+            for (int pi = warp; pi < N / 2; pi += nwarp) {
                 const int a = pp[pi], b = qq[pi];
                 const double c = cs[pi], s = sn[pi];
-                const double xa = A[a * N + col], xb = A[b * N + col];
-                A[a * N + col] = c * xa - s * xb;
-                A[b * N + col] = s * xa + c * xb;
+                for (int col = lane; col < N; col += 32) {
+                    const double xa = A[a * L + col], xb = A[b * L + col];
+                    A[a * L + col] = c * xa - s * xb;
+                    A[b * L + col] = s * xa + c * xb;
+                }
             }
             __syncthreads();
-            // columns: A <- A J, V <- V J
-            for (int e = threadIdx.x; e < (N / 2) * N; e += blockDim.x) {
-                const int pi = e / N, row = e % N;
+            // columns: A <- A J, V <- V J (lanes down the column; the odd stride L spreads banks)
+            for (int pi = warp; pi < N / 2; pi += nwarp) {
                 const int a = pp[pi], b = qq[pi];
                 const double c = cs[pi], s = sn[pi];
-                const double xa = A[row * N + a], xb = A[row * N + b];
-                A[row * N + a] = c * xa - s * xb;
-                A[row * N + b] = s * xa + c * xb;
-                const double va = V[row * N + a], vb = V[row * N + b];
-                V[row * N + a] = c * va - s * vb;
-                V[row * N + b] = s * va + c * vb;
+                for (int row = lane; row < N; row += 32) {
+                    const double xa = A[row * L + a], xb = A[row * L + b];
+                    A[row * L + a] = c * xa - s * xb;
+                    A[row * L + b] = s * xa + c * xb;
+                    const double va = V[row * L + a], vb = V[row * L + b];
+                    V[row * L + a] = c * va - s * vb;
+                    V[row * L + b] = s * va + c * vb;
+                }
             }
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) evals[i] = A[i * N + i];
+    double* sl = cs;                             // sqrt(max(lambda, 0)) (cs, sn are free now)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        evals[i] = A[i * L + i];
+        sl[i] = sqrt(fmax(A[i * L + i], 0.0));
+    }
     __syncthreads();
     // W[r][c] = sum_i V[r][i] sqrt(max(lambda_i, 0)) V[c][i]
     for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
         const int r = e / n, c = e % n;
         double acc = 0.0;
-        for (int i = 0; i < n; ++i) acc += V[r * N + i] * sqrt(fmax(A[i * N + i], 0.0)) * V[c * N + i];
+        for (int i = 0; i < n; ++i) acc += V[r * L + i] * sl[i] * V[c * L + i];
         Wout[e] = acc;
     }
 }
@@ -496,7 +508,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     double* W = (double*)dalloc(c, sizeof(double) * ke * ke, s);
     double* ev = (double*)dalloc(c, sizeof(double) * ke, s);
     const int N = ke + (ke & 1);
-    const size_t smj = sizeof(double) * (2 * (size_t)N * N + N) + sizeof(int) * N;
+    const size_t smj = sizeof(double) * (2 * (size_t)N * (N + 1) + N) + sizeof(int) * N;
     ensure_smem((const void*)jacobi_root_kernel, smj);
     LOVE_LAUNCH(jacobi_root_kernel, 1, 512, smj, s, st.alpha, st.beta, ke, W, ev);
     c.S = dalloc(c, c.vsize * (size_t)m * c.ks_pad, s);
