@@ -271,37 +271,46 @@ __global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t nqu
     }
 }
 
-// d = 1: per-cell stencil moments, one thread per cell, already scaled by q_j's column scale:
+// d = 1: per-cell stencil moments, TPC (= 2) lanes per cell, already scaled by q_j's column scale:
 //   Mc[l][c + 2] = s_j * sum_{p in cell c} w_l(p) Q~_j[p]      (l = 0..3, rows of length m + 4)
 // so that (W q_j)[i] = Mc[0][i+3] + Mc[1][i+2] + Mc[2][i+1] + Mc[3][i]  (no atomics, fixed order)
-template <typename V>
+template <typename V, int TPC>
 __global__ void __launch_bounds__(256) moments_cell1_kernel(int m, const int* __restrict__ cell_start,
                                                             const V* __restrict__ f0, const V* __restrict__ qbase,
                                                             StepRef ref, double* __restrict__ Mc) {
     pdl_wait();
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= m || step_done(ref)) return;
+    // TPC lanes per cell (aligned lane groups): lane `sub` takes points p0 + sub, p0 + sub + TPC, ...
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c = gt / TPC, sub = gt % TPC;
+    if (step_done(ref)) return;
+    const bool live = c < m;
     const int j = step_j(ref);
     const V* __restrict__ q = qbase + j * ref.ld;
-    const int p0 = cell_start[c], p1 = cell_start[c + 1];
+    const int p0 = live ? cell_start[c] : 0, p1 = live ? cell_start[c + 1] : 0;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int pb = p0; pb < p1; pb += kBatch) {
-        double qv[kBatch], fa[kBatch];
+    constexpr int B = kBatch / TPC > 2 ? kBatch / TPC : 2;
+    for (int pb = p0 + sub; pb < p1; pb += B * TPC) {
+        double qv[B], fa[B];
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            const int p = pb + u;
+        for (int u = 0; u < B; ++u) {
+            const int p = pb + u * TPC;
             const bool in = p < p1;
             qv[u] = in ? (double)q[p] : 0.0;
             fa[u] = in ? (double)f0[p] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
+        for (int u = 0; u < B; ++u) {
             double w[4];
             keys4<double>(fa[u], w);
 #pragma unroll
             for (int l = 0; l < 4; ++l) acc[l] += w[l] * qv[u];
         }
     }
+#pragma unroll
+    for (int o = 1; o < TPC; o <<= 1)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], o);
+    if (!live || sub != 0) return;
     const double sc = ref.scale[j];
     const int ld = m + 4;
 #pragma unroll
@@ -353,8 +362,8 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
     }
     if (c.g.d == 1 && c.Mc != nullptr) {
         const int m = c.g.m_total;
-        LOVE_LAUNCH(moments_cell1_kernel<V>, (int)ceil_div(m, 256), 256, 0, s, m, c.cell_start, (const V*)c.frac[0],
-                    q, ref, (double*)c.Mc);
+        LOVE_LAUNCH((moments_cell1_kernel<V, 2>), (int)ceil_div(2 * (int64_t)m, 256), 256, 0, s, m, c.cell_start,
+                    (const V*)c.frac[0], q, ref, (double*)c.Mc);
         if (!moments_only)
             LOVE_LAUNCH(nodepass_cell1_kernel, (int)ceil_div(m, 256), 256, 0, s, m, (const double*)c.Mc, ref, u);
         return;
