@@ -302,9 +302,15 @@ __global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
-    load_tw(tws, tw2, N2);
     const int n1_0 = blockIdx.x * G;
     const int Np = N1 * N2;
+    C ow[8];                                    // output twiddles, loaded before the transform
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        ow[e] = twiddleN<-1>(((n1_0 + t / N2) * (t % N2)) & (Np - 1), N1, tw2, twF);
+    }
+    load_tw(tws, tw2, N2);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
@@ -320,8 +326,7 @@ __global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __
     for (int e = 0; e < 8; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N2, k2 = t % N2;
-        const int n1 = n1_0 + g;
-        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(t)], twiddleN<-1>((n1 * k2) & (Np - 1), N1, tw2, twF));
+        Y[(int64_t)(n1_0 + g) * N2 + k2] = cmul(buf[pad(t)], ow[e]);
     }
 }
 
@@ -336,10 +341,26 @@ __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N1;
-    load_tw(tws, tw1, N1);
     const int b = blockIdx.x;
     const int kl[2] = {b == 0 ? 0 : b, b == 0 ? N2 / 2 : N2 - b};
     const int Np = N1 * N2;
+    // element e of this thread: line g = t / N1, position t % N1 (k1 in the middle, n1 at the
+    // ends).  Its untangle twiddle, lambdas and output twiddle do not depend on the data: load
+    // them first, so their latency overlaps the input loads and the forward transform.
+    C uw[8], ow[8];
+    double l1v[8], l2v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int t = threadIdx.x + e * blockDim.x;
+        const int g = t / N1, x = t % N1;
+        const int k2 = kl[g];
+        uw[e] = cmul(__ldg(&twU1[x]), __ldg(&twU2[k2]));
+        const int K = N2 * x + k2;
+        l1v[e] = __ldg(&lamN[K]);
+        l2v[e] = __ldg(&lamN[Np - K]);
+        ow[e] = twiddleN<+1>((x * k2) & (Np - 1), N1, tw2, twF);
+    }
+    load_tw(tws, tw1, N1);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
@@ -363,10 +384,9 @@ __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __
         const C E = make_double2(0.5 * (zk.x + zq.x), 0.5 * (zk.y + zq.y));
         const C D = make_double2(0.5 * (zk.x - zq.x), 0.5 * (zk.y - zq.y));   // O = -i D
         const C O = make_double2(D.y, -D.x);
-        const C w = cmul(__ldg(&twU1[k1]), __ldg(&twU2[k2]));
+        const C w = uw[e];
         const C wO = cmul(w, O);
-        const int K = N2 * k1 + k2;
-        const double l1 = lamN[K], l2 = lamN[Np - K];   // lambda[K + N'] = lambda[N' - K]
+        const double l1 = l1v[e], l2 = l2v[e];          // lambda[K + N'] = lambda[N' - K]
         const C Y1 = make_double2(l1 * (E.x + wO.x), l1 * (E.y + wO.y));
         const C Y2 = make_double2(l2 * (E.x - wO.x), l2 * (E.y - wO.y));
         const C S = cadd(Y1, Y2);
@@ -382,8 +402,7 @@ __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __
     for (int e = 0; e < 8; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N1, n1 = t % N1;
-        const int k2 = kl[g];
-        Y[(int64_t)n1 * N2 + k2] = cmul(buf[pad(t)], twiddleN<+1>((n1 * k2) & (Np - 1), N1, tw2, twF));
+        Y[(int64_t)n1 * N2 + kl[g]] = cmul(buf[pad(t)], ow[e]);
     }
 }
 
