@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                                                      V* __restrict__ r, double* __restrict__ alpha_base,
                                                      RcStream rs, int ngather) {
     pdl_wait();
-    if ((int)blockIdx.x >= ngather) {          // extra CTAs: the streamed cache column
+    if ((int)blockIdx.x >= ngather) {          // extra CTAs: the streamed cache column (last: the
+        // d >= 2 gather is the longer job, its CTAs go first)
         stream_rc_column(rs, (blockIdx.x - ngather) * blockDim.x + threadIdx.x, (gridDim.x - ngather) * blockDim.x);
         return;
     }
@@ -226,15 +227,16 @@ __device__ __forceinline__ void st4(V* __restrict__ p, const V o[4]) {
     }
 }
 
-template <typename V>
-__global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t nquads, const int* __restrict__ pcell,
+template <typename V, int PPT>
+__global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t ngroups, const int* __restrict__ pcell,
                                                           const V* __restrict__ f0, const double* __restrict__ z,
                                                           const V* __restrict__ qbase, StepRef ref, double sigma2,
                                                           V* __restrict__ r, double* __restrict__ alpha_base,
-                                                          RcStream rs, int ngather) {
+                                                          RcStream rs, int nstream) {
     pdl_wait();
-    if ((int)blockIdx.x >= ngather) {
-        stream_rc_column(rs, (blockIdx.x - ngather) * blockDim.x + threadIdx.x, (gridDim.x - ngather) * blockDim.x);
+    // the first nstream CTAs stream the cache column (they start first and overlap the gather)
+    if ((int)blockIdx.x < nstream) {
+        stream_rc_column(rs, blockIdx.x * blockDim.x + threadIdx.x, nstream * blockDim.x);
         return;
     }
     __shared__ double red[32];
@@ -244,16 +246,26 @@ __global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t nqu
     const double sc = ref.scale[j];
     const double vsc = sc, vsig = sigma2 * sc;
     double alpha = 0.0;
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t < nquads) {
-        const int64_t p0 = t * 4;
-        V qv[4], fa[4], rv[4];
-        ld4<V>(q + p0, qv);
-        ld4<V>(f0 + p0, fa);
-        const int4 cl = *reinterpret_cast<const int4*>(pcell + p0);
-        const int cells[4] = {cl.x, cl.y, cl.z, cl.w};
+    const int64_t t = (blockIdx.x - nstream) * (int64_t)blockDim.x + threadIdx.x;
+    if (t < ngroups) {
+        const int64_t p0 = t * PPT;
+        V qv[PPT], fa[PPT], rv[PPT];
+        int cells[PPT];
+        if constexpr (PPT == 4) {
+            ld4<V>(q + p0, qv);
+            ld4<V>(f0 + p0, fa);
+            const int4 cl = *reinterpret_cast<const int4*>(pcell + p0);
+            cells[0] = cl.x; cells[1] = cl.y; cells[2] = cl.z; cells[3] = cl.w;
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < PPT; ++u) {
+                qv[u] = q[p0 + u];
+                fa[u] = f0[p0 + u];
+                cells[u] = pcell[p0 + u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
             rv[u] = V(0);
             if (p0 + u < n) {
                 double zl[4], w0[4];
@@ -263,7 +275,12 @@ __global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t nqu
                 alpha += (double)(vsc * (double)qv[u]) * (double)rv[u];
             }
         }
-        st4<V>(r + p0, rv);
+        if constexpr (PPT == 4) {
+            st4<V>(r + p0, rv);
+        } else {
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) r[p0 + u] = rv[u];
+        }
     }
     if (alpha_base != nullptr) {
         alpha = block_sum(alpha, red);
@@ -418,11 +435,11 @@ void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* 
         extra = (int)std::min<int64_t>(ceil_div(rs.m, 256), 148 * 2);
     }
     if (c.g.d == 1 && c.pcell != nullptr) {
-        const int64_t nq = c.ldq / 4;
-        const int gq = (int)ceil_div(nq, 256);
+        const int64_t ng = c.ldq / 4;
+        const int gq = (int)ceil_div(ng, 256);
         if (gq + extra > 0)
-            LOVE_LAUNCH(gather_pts1_kernel<V>, gq + extra, 256, 0, s, c.n, nq, (const int*)c.pcell,
-                        (const V*)c.frac[0], z, q, ref, c.sigma2, r, alpha_base, rs, gq);
+            LOVE_LAUNCH((gather_pts1_kernel<V, 4>), gq + extra, 256, 0, s, c.n, ng, (const int*)c.pcell,
+                        (const V*)c.frac[0], z, q, ref, c.sigma2, r, alpha_base, rs, extra);
         return;
     }
     const int64_t ni = c.n_items;
