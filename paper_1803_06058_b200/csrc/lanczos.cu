@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     if (st.flags[0] || j >= k - 1) return;
     if (gate != nullptr && !*gate) return;
     const int from_r = pass == 0;
-    double* __restrict__ c_out = st.c_cur + (int64_t)pass * (k + 1);
+    double* __restrict__ c_out = st.c_cur + ((int64_t)pass * st.crep + blockIdx.x % st.crep) * c_stride(st, k);
     const int ncols = j + 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* csum = smd;                                   // [nw][ncols]
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
 __device__ __forceinline__ void clear_step_acc(const LanczosState& st, int k) {
     st.alpha_cur[0] = 0.0;
     st.beta2_cur[0] = 0.0;
-    for (int i = 0; i < 2 * (k + 1); ++i) st.c_cur[i] = 0.0;
+    for (int64_t i = 0; i < 2 * st.crep * c_stride(st, k); ++i) st.c_cur[i] = 0.0;
 }
 
 // multi-GPU path: after the prologue has consumed the previous step's accumulators
@@ -321,7 +321,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
     if (fin) {
         if (threadIdx.x == 0) finalize_index(st, j, k, tol);
         __syncthreads();                             // scalars read before the accumulators clear
-        for (int i = threadIdx.x; i < 2 * (k + 1); i += blockDim.x) st.c_cur[i] = 0.0;
+        for (int64_t i = threadIdx.x; i < 2 * st.crep * c_stride(st, k); i += blockDim.x) st.c_cur[i] = 0.0;
     }
     if (threadIdx.x == 0) {
         if (fin) {
@@ -360,10 +360,15 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         return;
     }
     const int from_r = pass == 0;
-    const double* __restrict__ c_in = st.c_cur + (int64_t)pass * (k + 1);
+    const int64_t cst = c_stride(st, k);
+    const double* __restrict__ c_in = st.c_cur + (int64_t)pass * st.crep * cst;
     double* __restrict__ beta2_out = (mode & kUpdBeta) ? st.beta2_cur : nullptr;
     const int ncols = (mode & kUpd3T) ? 0 : j + 1;
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) cf[i] = c_in[i] * st.qscale[i];
+    for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+        double ci = 0.0;
+        for (int rp = 0; rp < st.crep; ++rp) ci += c_in[rp * cst + i];
+        cf[i] = ci * st.qscale[i];
+    }
     __syncthreads();
     const double sj = st.qscale[j];
     const double aj = st.alpha_cur[0] * sj;

@@ -266,6 +266,11 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
             st.pro_eps = eps;
             st.pro_tol = o.reorth_tol > 0.0 ? o.reorth_tol : std::sqrt(eps);
         }
+        if (c->comm == nullptr) {                        // one GPU: spread the dot atomics
+            st.crep = 4;                                 // measured: 4 beats 8 and 16 (cfg2, cfg3)
+            st.cld = (int)(round_up((int64_t)K + 1, 16) + 16);
+            st.c_cur = (double*)dalloc(*c, sizeof(double) * 2 * st.crep * st.cld, s);
+        }
         LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
     }
 

@@ -52,7 +52,10 @@ __device__ __forceinline__ bool step_done(const StepRef& r) { return r.flags != 
 struct LanczosState {
     double* alpha_cur;     // [1]        q_j^T A q_j of the current step
     double* beta2_cur;     // [1]        ||q~_{j+1}||^2 of the current step
-    double* c_cur;         // [2][k+1]   reorthogonalisation dots of the current step (passes 0, 1)
+    double* c_cur;         // [2][crep][cld] reorthogonalisation dots of the current step (passes 0, 1)
+    int crep = 1;          // copies of each pass's dots (CTA b adds to copy b % crep: same-address
+                           // fp64 atomics serialise in L2; the update sums the copies)
+    int cld = 0;           // stride between copies (0: k + 1)
     double* bnorm2;        // [1]        ||b||^2
     double* qscale;        // [k+1]      1/||q~_j|| (lazy normalisation of Q's columns)
     double* alpha;         // [k]
@@ -79,6 +82,10 @@ struct LanczosState {
 // a += ||b|| g_i Rc[:, i] (probe y), computed by extra CTAs of the next step's gather
 // kernel once the update kernel's last CTA has finalised the scalars of index i
 // (single-GPU Lanczos; i = *jdev - 1, z_i in z[i & 1]).
+__host__ __device__ __forceinline__ int64_t c_stride(const LanczosState& st, int k) {
+    return st.cld > 0 ? st.cld : k + 1;
+}
+
 struct RcStream {
     LanczosState st;
     const double* z0;
