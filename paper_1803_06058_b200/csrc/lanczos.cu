@@ -365,8 +365,13 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     double* __restrict__ beta2_out = (mode & kUpdBeta) ? st.beta2_cur : nullptr;
     const int ncols = (mode & kUpd3T) ? 0 : j + 1;
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
-        double ci = 0.0;
-        for (int rp = 0; rp < st.crep; ++rp) ci += c_in[rp * cst + i];
+        double ci;
+        if (st.crep == 4) {                     // independent loads (one L2 round trip)
+            ci = (c_in[i] + c_in[cst + i]) + (c_in[2 * cst + i] + c_in[3 * cst + i]);
+        } else {
+            ci = 0.0;
+            for (int rp = 0; rp < st.crep; ++rp) ci += c_in[rp * cst + i];
+        }
         cf[i] = ci * st.qscale[i];
     }
     __syncthreads();
