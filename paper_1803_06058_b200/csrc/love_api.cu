@@ -373,7 +373,7 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         c->cell_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
         c->cell_item_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
         for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * (c->ldq + 4), s);   // padded to 16 B units
-        if (g.d == 1 && !c->fused) c->pcell = (int*)dalloc(*c, sizeof(int) * (c->ldq + 4), s);
+        if (g.d <= 2 && !c->fused) c->pcell = (int*)dalloc(*c, sizeof(int) * (c->ldq + 4), s);
         c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
         prof_begin(LOVE_PROF_SETUP, s);
         launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);

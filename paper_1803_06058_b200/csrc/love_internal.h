@@ -124,7 +124,7 @@ struct Cache {
     int64_t n_items = 0;
     void* frac[3] = {nullptr, nullptr, nullptr};   // V[n] per dim (sorted order)
     int* perm = nullptr;                 // [n] sorted -> original
-    int* pcell = nullptr;                // d = 1: [ldq + 4] cell of each sorted point (0 past n)
+    int* pcell = nullptr;                // d <= 2: [ldq + 4] cell of each sorted point (0 past n)
     int* cell_start = nullptr;           // [m_total+1]
     int* cell_item_start = nullptr;      // [m_total+1]
     int* item_cell = nullptr;            // [n_items]

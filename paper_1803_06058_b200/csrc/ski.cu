@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
     }
 }
 
-// d = 1 gather, thread per 4 consecutive sorted points (coalesced q / frac / cell loads and r
+// d <= 2 gather, thread per 4 consecutive sorted points (coalesced q / frac / cell loads and r
 // stores; the z stencil loads of neighbouring points hit the same lines):
 //   r_p = sum_l w_l(p) z[cell(p) - 1 + l] + sigma^2 s_j Q~_j[p],   alpha += s_j Q~_j[p] r_p
 // Same per-point arithmetic as gather_kernel<V, 1>; points past n get r = 0.
@@ -227,9 +227,10 @@ __device__ __forceinline__ void st4(V* __restrict__ p, const V o[4]) {
     }
 }
 
-template <typename V, int PPT>
-__global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t ngroups, const int* __restrict__ pcell,
-                                                          const V* __restrict__ f0, const double* __restrict__ z,
+template <typename V, int D>
+__global__ void __launch_bounds__(256) gather_pts1_kernel(GridDev g, int64_t n, int64_t ngroups,
+                                                          const int* __restrict__ pcell, const V* __restrict__ f0,
+                                                          const V* __restrict__ f1, const double* __restrict__ z,
                                                           const V* __restrict__ qbase, StepRef ref, double sigma2,
                                                           V* __restrict__ r, double* __restrict__ alpha_base,
                                                           RcStream rs, int nstream) {
@@ -239,48 +240,37 @@ __global__ void __launch_bounds__(256) gather_pts1_kernel(int64_t n, int64_t ngr
         stream_rc_column(rs, blockIdx.x * blockDim.x + threadIdx.x, nstream * blockDim.x);
         return;
     }
+    using A = typename AccT<V, D>::type;
     __shared__ double red[32];
     if (step_done(ref)) return;
     const int j = step_j(ref);
     const V* __restrict__ q = qbase + j * ref.ld;
     const double sc = ref.scale[j];
-    const double vsc = sc, vsig = sigma2 * sc;
+    const A vsc = (A)sc, vsig = (A)(sigma2 * sc);
     double alpha = 0.0;
     const int64_t t = (blockIdx.x - nstream) * (int64_t)blockDim.x + threadIdx.x;
     if (t < ngroups) {
-        const int64_t p0 = t * PPT;
-        V qv[PPT], fa[PPT], rv[PPT];
-        int cells[PPT];
-        if constexpr (PPT == 4) {
-            ld4<V>(q + p0, qv);
-            ld4<V>(f0 + p0, fa);
-            const int4 cl = *reinterpret_cast<const int4*>(pcell + p0);
-            cells[0] = cl.x; cells[1] = cl.y; cells[2] = cl.z; cells[3] = cl.w;
-        } else {
+        const int64_t p0 = t * 4;
+        V qv[4], fa[4], fb[4], rv[4];
+        ld4<V>(q + p0, qv);
+        ld4<V>(f0 + p0, fa);
+        if (D > 1) ld4<V>(f1 + p0, fb);
+        const int4 cl = *reinterpret_cast<const int4*>(pcell + p0);
+        const int cells[4] = {cl.x, cl.y, cl.z, cl.w};
 #pragma unroll
-            for (int u = 0; u < PPT; ++u) {
-                qv[u] = q[p0 + u];
-                fa[u] = f0[p0 + u];
-                cells[u] = pcell[p0 + u];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < PPT; ++u) {
+        for (int u = 0; u < 4; ++u) {
             rv[u] = V(0);
             if (p0 + u < n) {
-                double zl[4], w0[4];
-                load_stencil<double, 1>(GridDev{}, z, cells[u] - 1, zl);
-                keys4<double>((double)fa[u], w0);
-                rv[u] = (V)(stencil_dot<double, 1>(w0, w0, w0, zl) + vsig * (double)qv[u]);
-                alpha += (double)(vsc * (double)qv[u]) * (double)rv[u];
+                A zl[Slots<D>::value], w0[4], w1[4];
+                load_stencil<A, D>(g, z, D == 1 ? cells[u] - 1 : stencil_base<D>(g, cells[u]), zl);
+                keys4<A>((A)fa[u], w0);
+                if (D > 1) keys4<A>((A)fb[u], w1);
+                const A qa = (A)qv[u];
+                rv[u] = (V)(stencil_dot<A, D>(w0, w1, w1, zl) + vsig * qa);
+                alpha += (double)(vsc * qa) * (double)rv[u];
             }
         }
-        if constexpr (PPT == 4) {
-            st4<V>(r + p0, rv);
-        } else {
-#pragma unroll
-            for (int u = 0; u < PPT; ++u) r[p0 + u] = rv[u];
-        }
+        st4<V>(r + p0, rv);
     }
     if (alpha_base != nullptr) {
         alpha = block_sum(alpha, red);
@@ -434,12 +424,17 @@ void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* 
         rs = *rsp;
         extra = (int)std::min<int64_t>(ceil_div(rs.m, 256), 148 * 2);
     }
-    if (c.g.d == 1 && c.pcell != nullptr) {
+    if (c.g.d <= 2 && c.pcell != nullptr) {
         const int64_t ng = c.ldq / 4;
         const int gq = (int)ceil_div(ng, 256);
-        if (gq + extra > 0)
-            LOVE_LAUNCH((gather_pts1_kernel<V, 4>), gq + extra, 256, 0, s, c.n, ng, (const int*)c.pcell,
-                        (const V*)c.frac[0], z, q, ref, c.sigma2, r, alpha_base, rs, extra);
+        if (gq + extra > 0) {
+            if (c.g.d == 1)
+                LOVE_LAUNCH((gather_pts1_kernel<V, 1>), gq + extra, 256, 0, s, c.g, c.n, ng, (const int*)c.pcell,
+                            (const V*)c.frac[0], (const V*)c.frac[0], z, q, ref, c.sigma2, r, alpha_base, rs, extra);
+            else
+                LOVE_LAUNCH((gather_pts1_kernel<V, 2>), gq + extra, 256, 0, s, c.g, c.n, ng, (const int*)c.pcell,
+                            (const V*)c.frac[0], (const V*)c.frac[1], z, q, ref, c.sigma2, r, alpha_base, rs, extra);
+        }
         return;
     }
     const int64_t ni = c.n_items;
