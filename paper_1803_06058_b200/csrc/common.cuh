@@ -22,6 +22,14 @@ struct PdlScope {
     explicit PdlScope(bool on) : prev(t_pdl) { t_pdl = on; }
     ~PdlScope() { t_pdl = prev; }
 };
+// Inside a DoneScope the K_UU kernels get the Lanczos `done` flag and return at once when it
+// is set: steps launched past a breakdown (graph replays are fixed) then cost only launches.
+extern thread_local const int* t_done;
+struct DoneScope {
+    const int* prev;
+    explicit DoneScope(const int* f) : prev(t_done) { t_done = f; }
+    ~DoneScope() { t_done = prev; }
+};
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 

@@ -147,8 +147,9 @@ __device__ __forceinline__ double u_at(const double* __restrict__ u, const doubl
 // ---- single-CTA convolution (mode 0) / forward transform (mode 1), N <= 4096
 __global__ void fft_small_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N,
                                  const C* __restrict__ tw, const double* __restrict__ lam, double* __restrict__ z,
-                                 C* __restrict__ outc, int mode) {
+                                 C* __restrict__ outc, int mode, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N;
@@ -181,8 +182,9 @@ __global__ void fft_small_kernel(const double* __restrict__ u, const double* __r
 // ---- four-step pass A: for each n1, FFT over n2 of x[n1 + N1 n2], times w_N^{n1 k2}
 template <int G>
 __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
-                                 const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y) {
+                                 const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -213,8 +215,9 @@ __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __r
 template <int G>
 __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
                                  const C* __restrict__ tw2, const C* __restrict__ twF,
-                                 const double* __restrict__ lamB, C* __restrict__ outc, int mode) {
+                                 const double* __restrict__ lamB, C* __restrict__ outc, int mode, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N1;
@@ -260,8 +263,9 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
 // ---- four-step pass C: for each n1, inverse FFT over k2; z[n1 + N1 n2] = Re(.)
 template <int G>
 __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
-                                 double* __restrict__ z) {
+                                 double* __restrict__ z, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -297,8 +301,9 @@ __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2,
 // pass A': for each n1, FFT over n2 of zeta[n1 + N1 n2], times w_N'^{n1 k2}
 template <int G>
 __global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
-                                  const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y) {
+                                  const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -336,8 +341,9 @@ __global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __
 //   lamN[K] = lambda[K] * s^2 / N for K = 0..N'
 __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
                                   const C* __restrict__ tw2, const C* __restrict__ twF, const C* __restrict__ twU1,
-                                  const C* __restrict__ twU2, const double* __restrict__ lamN) {
+                                  const C* __restrict__ twU2, const double* __restrict__ lamN, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N1;
@@ -409,8 +415,9 @@ __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __
 // pass C': for each n1, inverse FFT over k2; z[2n] = Re, z[2n+1] = Im at n = n1 + N1 n2
 template <int G>
 __global__ void rfft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
-                                  double* __restrict__ z) {
+                                  double* __restrict__ z, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N2;
@@ -445,8 +452,9 @@ __global__ void lambda_natural_kernel(const C* __restrict__ X, int count, double
 // 32-row chunks of the input staged in shared memory; 4 independent accumulators/thread.
 constexpr int kAxRows = 16, kAxInner = 32, kAxK = 32;
 __global__ void __launch_bounds__(128) axis_inner_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                                         const double* __restrict__ c, int L, int I, double scale) {
+                                                         const double* __restrict__ c, int L, int I, double scale, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     __shared__ double cs[1024];
     __shared__ double tile[kAxK][kAxInner + 1];
     const int i0 = blockIdx.x * kAxInner;
@@ -485,8 +493,9 @@ __global__ void __launch_bounds__(128) axis_inner_kernel(const double* __restric
 // 256-row slice of one line), 4 partial sums per output.
 __global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                         const double* __restrict__ c, int64_t O, int L,
-                                                        double scale) {
+                                                        double scale, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     __shared__ double cs[1024];
     __shared__ double lines[2 * 1024 + 256];
     const int64_t first = (int64_t)blockIdx.x * 256;           // first output of this CTA
@@ -526,8 +535,9 @@ __global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict
 template <bool LFAST>
 __global__ void axis_conv_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ lam,
                                  const C* __restrict__ tw, int L, int I, int64_t O, int N, int P, int64_t npairs,
-                                 double scale) {
+                                 double scale, const int* __restrict__ done) {
     pdl_wait();
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
     C* buf = tws + N;
@@ -650,7 +660,7 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
     if (N1 == 0) {
         const size_t sm = sizeof(C) * (padded(N) + N);
         ensure_smem((const void*)fft_small_kernel, sm);
-        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, Mc, m, N, tw1, lam, z, outc, mode);
+        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, Mc, m, N, tw1, lam, z, outc, mode, t_done);
         return;
     }
     constexpr int G = kLinesPerCta;
@@ -663,19 +673,19 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
         ensure_smem((const void*)rfft_passA_kernel<G>, sA);
         ensure_smem((const void*)rfft_passB_kernel, sB);
         ensure_smem((const void*)rfft_passC_kernel<G>, sA);
-        LOVE_LAUNCH(rfft_passA_kernel<G>, R1 / G, G * R2 / 8, sA, s, u, Mc, m, R1, R2, r2, rF, work);
+        LOVE_LAUNCH(rfft_passA_kernel<G>, R1 / G, G * R2 / 8, sA, s, u, Mc, m, R1, R2, r2, rF, work, t_done);
         LOVE_LAUNCH(rfft_passB_kernel, R2 / 2, 2 * R1 / 8, sB, s, work, R1, R2, r1, r2, rF, (const C*)c.rtwU1,
-                    (const C*)c.rtwU2, (const double*)c.rlam);
-        LOVE_LAUNCH(rfft_passC_kernel<G>, R1 / G, G * R2 / 8, sA, s, (const C*)work, m, R1, R2, r2, z);
+                    (const C*)c.rtwU2, (const double*)c.rlam, t_done);
+        LOVE_LAUNCH(rfft_passC_kernel<G>, R1 / G, G * R2 / 8, sA, s, (const C*)work, m, R1, R2, r2, z, t_done);
         return;
     }
     const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
     ensure_smem((const void*)fft_passA_kernel<G>, smA);
     ensure_smem((const void*)fft_passB_kernel<G>, smB);
     ensure_smem((const void*)fft_passC_kernel<G>, smA);
-    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work);
-    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode);
-    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z);
+    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
+    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode, t_done);
+    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
 }
 
 void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
@@ -699,18 +709,18 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
             if (I == 1) {
                 ensure_smem((const void*)axis_conv_kernel<true>, sm);
                 LOVE_LAUNCH(axis_conv_kernel<true>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
-                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale);
+                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale, t_done);
             } else {
                 ensure_smem((const void*)axis_conv_kernel<false>, sm);
                 LOVE_LAUNCH(axis_conv_kernel<false>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
-                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale);
+                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale, t_done);
             }
         } else if (I == 1) {
             const int64_t total = (int64_t)O * L;
-            LOVE_LAUNCH(axis_line_kernel, (int)ceil_div(total, 256), 256, 0, s, in, out, col, (int64_t)O, L, scale);
+            LOVE_LAUNCH(axis_line_kernel, (int)ceil_div(total, 256), 256, 0, s, in, out, col, (int64_t)O, L, scale, t_done);
         } else {
             dim3 grid((unsigned)ceil_div(I, kAxInner), (unsigned)ceil_div(L, kAxRows), (unsigned)O);
-            LOVE_LAUNCH(axis_inner_kernel, grid, 128, 0, s, in, out, col, L, I, scale);
+            LOVE_LAUNCH(axis_inner_kernel, grid, 128, 0, s, in, out, col, L, I, scale, t_done);
         }
         in = out;
         off += L;
@@ -757,7 +767,7 @@ void setup_kuu(Cache& c, cudaStream_t s) {
                 const size_t sm = sizeof(C) * (padded(Nd) + Nd);
                 ensure_smem((const void*)fft_small_kernel, sm);
                 LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, Nd / 8), sm, s, colN, (const double*)nullptr, Nd, Nd,
-                            (const C*)c.ax_tw[d], (const double*)nullptr, (double*)nullptr, X, 1);
+                            (const C*)c.ax_tw[d], (const double*)nullptr, (double*)nullptr, X, 1, t_done);
                 LOVE_LAUNCH(lambda_store_kernel, (int)ceil_div(Nd, 256), 256, 0, s, X, Nd, 0, 0, 0, 1.0 / (double)Nd,
                             (double*)c.ax_lam[d]);
                 cuda_check(cudaFreeAsync(colN, s), "axis lam free");

@@ -23,7 +23,7 @@
 #ifndef LOVE_UPD_U
 #define LOVE_UPD_U 7
 #endif
-namespace love { constexpr int kUpdU = LOVE_UPD_U; }
+namespace love { constexpr int kUpdU = LOVE_UPD_U; constexpr int kCondSteps = 2; }
 
 namespace love {
 
@@ -330,6 +330,10 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
         }
         st.step_ctr[0] = 0;
         st.jdev[0] = j + 1;
+        if (st.cond != 0) {                          // inside the WHILE graph node
+            st.flags[6] += 1;
+            if (st.flags[0] || j + 1 >= st.cond_limit) cudaGraphSetConditional(st.cond, 0);
+        }
         __threadfence();
     }
 }
@@ -552,6 +556,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     double* zj = (double*)c.z[j_host & 1];
     {
         ProfScope ps(LOVE_PROF_KUU, s);
+        DoneScope ds(st.flags);
         launch_kuu(c, u, zj, s, pl.mfuse ? (const double*)c.Mc : nullptr);
     }
     {
@@ -647,7 +652,52 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     // every kernel of a step starts with pdl_wait(): its launch can overlap the previous
     // kernel's drain (programmatic dependent launch)
     PdlScope pdl(std::getenv("LOVE_NO_PDL") == nullptr);
-    if (graph) {
+    // Opt-in (LOVE_COND_STEPS=G): measured, the WHILE node's per-iteration cost (~6 us) and the
+    // host-side instantiation of its body outweigh the launches it saves unless the Lanczos
+    // breaks down well before k (cfg5: 2.58 -> 1.91 ms; cfg2: +0.3 ms at G = 2).
+    const char* ge_env = std::getenv("LOVE_COND_STEPS");
+    int G = ge_env ? std::atoi(ge_env) : kCondSteps;
+    G = std::max(2, G - (G & 1));
+    if (graph && c.comm == nullptr && ge_env != nullptr && pl.k >= G) {
+        // one GPU: a CUDA graph WHILE node whose body is G steps (G even: z buffer parity);
+        // the last update of a step clears the condition on breakdown or at the last full
+        // body, so the host never polls and at most G - 1 early-exiting steps run past a
+        // breakdown (every step kernel returns at once once the Lanczos is done)
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        cuda_check(cudaGraphCreate(&g, 0), "graph create");
+        cudaGraphConditionalHandle h;
+        cuda_check(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault), "conditional handle");
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        cuda_check(cudaGraphAddNode(&node, g, nullptr, 0, &cp), "conditional node");
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        StepPlan<V> pc = pl;
+        LanczosState& cst = c.st;
+        cst.cond = (unsigned long long)h;
+        const int limit = pl.k - pl.k % G;
+        cst.cond_limit = limit;
+        pc.rs.st = cst;
+        const int64_t before = g_launch_count.load();
+        cuda_check(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal),
+                   "begin capture");
+        for (int jj = 0; jj < G; ++jj) enqueue_step<V>(pc, jj, s);
+        cuda_check(cudaStreamEndCapture(s, &body), "end capture");
+        cst.cond = 0;                               // launches after the loop: plain steps
+        cst.cond_limit = 0;
+        c.cond_nodes = g_launch_count.load() - before;
+        c.cond_steps = G;
+        g_launch_count -= c.cond_nodes;             // counted after the build from flags[6]
+        cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+        cuda_check(cudaGraphLaunch(ge, s), "graph launch");
+        for (int j = limit; j < pl.k; ++j) enqueue_step<V>(pl, j, s);
+        cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
+        cuda_check(cudaGraphDestroy(g), "graph destroy");
+    } else if (graph) {
         // one step as a CUDA graph, replayed k times (z buffer parity alternates: capture
         // two steps so both parities are covered and replay the pair)
         cudaGraph_t g = nullptr;

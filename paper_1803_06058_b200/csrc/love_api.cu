@@ -17,6 +17,7 @@ namespace love {
 
 std::atomic<int64_t> g_launch_count{0};
 thread_local bool t_pdl = false;
+thread_local const int* t_done = nullptr;
 
 namespace {
 thread_local std::string t_err;
@@ -281,7 +282,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (c->fused) setup_fused(*c, s);
     if (c->fused) run_lanczos_fused(*c, s);
     else run_lanczos(*c, s);
-    int hfl[4];
+    int hfl[8];
     double bn2 = 0;
     cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
     cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
@@ -290,6 +291,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
     if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
     c->k_eff = hfl[1];
+    g_launch_count += c->cond_nodes * (hfl[6] / c->cond_steps);   // kernels of the device-terminated step loop
     c->b_norm = std::sqrt(bn2);
     c->n_reorth_steps = std::max(c->k_eff - 1, 0);
     if (c->partial) {

@@ -68,6 +68,11 @@ struct LanczosState {
     int* jdev;             // [1]        current step index j
     int* step_ctr;         // [1]        CTAs done in the step's last kernel (advance_step)
     int chol = 1;          // finalise the Cholesky row of T too (0: sampling Lanczos on M, reading A15)
+    // device-terminated step loop (a CUDA graph WHILE node, one GPU): the step's last CTA
+    // clears the loop condition once the Lanczos is done or the step index reaches cond_limit;
+    // it also counts the steps run inside the loop in flags[6] (launch accounting)
+    unsigned long long cond = 0;
+    int cond_limit = 0;
     // partial reorthogonalisation (LOVE_LANCZOS_PARTIAL)
     double* omega;         // [3][k+1]   rows j-1, j, j+1 of Simon's estimates omega_{j,i} ~ q_j^T q_i
     int* pro;              // [4]        reorthogonalise this step, force the next, steps reorthogonalised
@@ -156,6 +161,8 @@ struct Cache {
     void* M = nullptr;                   // double[4^d * n_items] per-item stencil moments
     void* M2 = nullptr;                  // second moments buffer (fused mode: moments of Q~_j)
     void* Mc = nullptr;                  // d = 1: double[4][m+4] per-cell stencil moments of the scatter
+    int64_t cond_nodes = 0;              // kernels per iteration of the device-terminated step loop
+    int cond_steps = 1;                  // Lanczos steps per iteration
     void* pullT = nullptr;               // d >= 2: double[4^(d-1)][m] last-axis pull of the scatter
     void* pullV = nullptr;               // d = 3: double[4][m] middle-axis pull
     void* Rc_col = nullptr;              // double[m * k] column-major (build only)

@@ -463,7 +463,10 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     // one step: q_j -> K_UU q_j, Rc^T q_j -> v, alpha -> two CGS passes (the last finalises)
     auto step = [&]() {
         LOVE_LAUNCH(samp_qcur_kernel, gq, 256, 0, s, st, (const double*)Qp, ldq, m, qcur, t, k);
-        launch_kuu(c, qcur, z, s);
+        {
+            DoneScope ds(st.flags);
+            launch_kuu(c, qcur, z, s);
+        }
         LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, t, st.flags);
         LOVE_LAUNCH(samp_v_kernel, gm, 256, sizeof(double) * std::max(k, 1), s, Rc, m, k, z, t, qcur, v, st);
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 0, 0, v, tol, s);

@@ -368,3 +368,35 @@ def test_partial_reorth_is_fp32_single_gpu_only():
     inp = make_inputs(p)
     with pytest.raises(LoveError):
         _build(p, inp, lanczos_mode="partial")          # fp64 config
+
+
+@pytest.mark.parametrize("G", [2, 8])
+def test_device_terminated_step_loop(monkeypatch, G):
+    """The opt-in CUDA-graph WHILE loop (LOVE_COND_STEPS) stops on the device at breakdown:
+    same k_eff, T and variances as the replayed step graph, and against the oracle.  Config-5
+    shape (m = 10^4, k = 100) breaks down well before k."""
+    from paper_1803_06058_b200 import launch_count
+    p = scaled_config(5, n=30_011, k=100, t=2003, precision="fp64")
+    inp = make_inputs(p)
+    c0 = _build(p, inp)
+    v0 = c0.predict_var(inp.Xs).cpu().numpy().astype(np.float64)
+    i0 = c0.info()
+    monkeypatch.setenv("LOVE_COND_STEPS", str(G))
+    l0 = launch_count()
+    c1 = _build(p, inp)
+    l1 = launch_count() - l0
+    v1 = c1.predict_var(inp.Xs).cpu().numpy().astype(np.float64)
+    i1 = c1.info()
+    assert i1["k_eff"] == i0["k_eff"] < p.k
+    # fp64 atomics sum in a different order on every run: compare at the parity bounds
+    np.testing.assert_allclose(i1["alpha"], i0["alpha"], rtol=1e-9)
+    np.testing.assert_allclose(i1["beta"], i0["beta"], rtol=1e-6, atol=1e-9 * np.max(i0["beta"]))
+    model = _model(p, inp)
+    prior = _prior(model, inp.Xs)
+    _assert_var(v1, v0, prior, fp64=True)
+    # launches past the breakdown are not issued (at most G - 1 early-exiting steps run;
+    # fp64: 9 kernels per step, two CGS passes)
+    assert 0 < l1 < 9 * (i0["k_eff"] + G + 4) + 200
+    oc = O.love_precompute(model, p.k)
+    assert oc.lanczos.k_eff == i1["k_eff"]
+    _assert_var(v1, O.predict_var(model, oc, inp.Xs), prior, fp64=True)
