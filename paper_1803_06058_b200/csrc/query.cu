@@ -389,6 +389,90 @@ __global__ void query_cell3_kernel(GridDev g, const double* __restrict__ Xs, int
     }
 }
 
+// variance (and mean) of one d = 3 query from its stencil, the reduced norm and the mean sum
+template <typename V>
+__device__ __forceinline__ void finish_sorted3(const Stencil& A, const C4& c4, double s2, int prior_mode, double dot,
+                                               double mu, int q, V* __restrict__ out, V* __restrict__ mean_out,
+                                               unsigned long long* __restrict__ counters) {
+    double prior = s2;
+    if (prior_mode != LOVE_PRIOR_EXACT) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc += A.w[d][a] * A.w[d][b] * c4.c[d][a > b ? a - b : b - a];
+            prior *= acc;
+        }
+    }
+    const double v = prior - dot;
+    out[q] = (V)v;
+    if (v < 0.0) atomicAdd(&counters[0], 1ull);
+    if (mean_out) mean_out[q] = (V)mu;
+}
+
+// r = sum_a w0_a sum_b w1_b sum_c w2_c Rc[row(a,b,c)] on W consecutive k of the staged rows,
+// innermost first; the 16-term (b, c) sums in the storage type V (fp32 rows in LOVE_FP32: a
+// few ulp of fp32 on top of what the fp32 storage of Rc already carries, without converting
+// every row element to fp64); the a-sum is fp64; returns sum_e r_e^2
+template <typename V>
+__device__ __forceinline__ double sorted3_chunk(const Stencil& A, const V* rows, int k_pad, int ch) {
+    constexpr int W = QV<V>::W;
+    using VT = typename QV<V>::T;
+    double acc[W];
+#pragma unroll
+    for (int e = 0; e < W; ++e) acc[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        V ra[W];
+#pragma unroll
+        for (int e = 0; e < W; ++e) ra[e] = V(0);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            V rb[W];
+#pragma unroll
+            for (int e = 0; e < W; ++e) rb[e] = V(0);
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const VT v = *reinterpret_cast<const VT*>(rows + (a * 16 + b * 4 + cc) * k_pad + ch * W);
+                const V w = (V)A.w[2][cc];
+                if constexpr (W == 4) {
+                    rb[0] += w * v.x; rb[1] += w * v.y; rb[2] += w * v.z; rb[3] += w * v.w;
+                } else {
+                    rb[0] += w * v.x; rb[1] += w * v.y;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < W; ++e) ra[e] += (V)A.w[1][b] * rb[e];
+        }
+#pragma unroll
+        for (int e = 0; e < W; ++e) acc[e] += A.w[0][a] * (double)ra[e];
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int e = 0; e < W; ++e) dot += acc[e] * acc[e];
+    return dot;
+}
+
+// mean of one d = 3 query, sum over the 64 stencil nodes (one lane)
+__device__ __forceinline__ double sorted3_mean(const Stencil& A, const double* __restrict__ amean, const GridDev& g,
+                                               int base) {
+    double mu = 0.0;
+#pragma unroll 4
+    for (int l = 0; l < 64; ++l) {
+        const double w = A.w[0][l >> 4] * A.w[1][(l >> 2) & 3] * A.w[2][l & 3];
+        mu += w * amean[base + (l >> 4) * g.stride[0] + ((l >> 2) & 3) * g.stride[1] + (l & 3)];
+    }
+    return mu;
+}
+
+// Queries counting-sorted by cell (SURVEY 8(f) NEXT #3a): a CTA stages the 64 stencil rows of
+// Rc of a cell in shared memory once.  Cells with at least kLanePerQuery queries: one lane per
+// query, every lane reading the same row chunk (a shared-memory broadcast feeds 32 queries);
+// sparser cells: a warp per query, lanes over 16-byte chunks of k.
+constexpr int kLanePerQuery = 16;
+
 template <typename V>
 __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
                                                               double l2, int prior_mode, const V* __restrict__ Rc,
@@ -397,11 +481,13 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
                                                               const int* __restrict__ qstart,
                                                               const int* __restrict__ perm, int cells_per_cta,
                                                               V* __restrict__ out, V* __restrict__ mean_out,
-                                                              unsigned long long* __restrict__ counters) {
+                                                              unsigned long long* __restrict__ counters,
+                                                              int lane_mode_min) {
     constexpr int W = QV<V>::W;
     using VT = typename QV<V>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
     V* rows = reinterpret_cast<V*>(smraw);                       // [64][k_pad]
+    __shared__ double part[256];                                 // lane mode: [warp][lane] partial norms
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nch = k_pad / W;
     const int m = g.m_total;
@@ -419,48 +505,49 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
                 __ldg(reinterpret_cast<const VT*>(Rc + (int64_t)node * k_pad + ch * W));
         }
         __syncthreads();
-        for (int pos = p0 + wid; pos < p1; pos += nw) {
+        const int nq = p1 - p0;
+        if (nq >= lane_mode_min) {                              // lane per query
+            // groups of 32 queries; with fewer groups than warps, wpg warps share a group and
+            // split its k chunks (partial norms combined in shared memory)
+            const int groups = (nq + 31) >> 5;
+            if (groups >= nw) {                                 // a warp per group of 32
+                for (int gi = wid; gi < groups; gi += nw) {
+                    const int pos = p0 + gi * 32 + lane;
+                    if (pos >= p1) continue;
+                    const int q = perm[pos];
+                    const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
+                    double dot = 0.0;
+                    for (int ch = 0; ch < nch; ++ch) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+                    finish_sorted3<V>(A, c4, s2, prior_mode, dot,
+                                      mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
+                }
+            } else {                                            // wpg warps per group: split k
+                const int wpg = nw / groups;
+                const int gi = wid / wpg, sub = wid - gi * wpg;
+                const int pos = p0 + gi * 32 + lane;
+                const bool live = gi < groups && pos < p1;
+                const int q = live ? perm[pos] : 0;
+                Stencil A;
+                double dot = 0.0;
+                if (live) {
+                    A = make_stencil<3>(g, Xs + (int64_t)q * 3);
+                    for (int ch = sub; ch < nch; ch += wpg) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+                }
+                part[wid * 32 + lane] = dot;                    // [warp][lane]
+                __syncthreads();
+                if (live && sub == 0) {
+                    for (int t = 1; t < wpg; ++t) dot += part[(wid + t) * 32 + lane];
+                    finish_sorted3<V>(A, c4, s2, prior_mode, dot,
+                                      mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
+                }
+            }
+            continue;
+        }
+        for (int pos = p0 + wid; pos < p1; pos += nw) {         // warp per query
             const int q = perm[pos];
             const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
             double dot = 0.0;
-            for (int ch = lane; ch < nch; ch += 32) {
-                double acc[W];
-#pragma unroll
-                for (int e = 0; e < W; ++e) acc[e] = 0.0;
-                // separable: r = sum_a w0_a sum_b w1_b sum_c w2_c Rc[row(a,b,c)], innermost first
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    V ra[W];
-#pragma unroll
-                    for (int e = 0; e < W; ++e) ra[e] = V(0);
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        // the 16-term (b, c) sums in the storage type V (fp32 rows in LOVE_FP32:
-                        // a few ulp of fp32 on top of what the fp32 storage of Rc already carries,
-                        // without converting every row element to fp64); the a-sum and the
-                        // norm are fp64
-                        V rb[W];
-#pragma unroll
-                        for (int e = 0; e < W; ++e) rb[e] = V(0);
-#pragma unroll
-                        for (int cc = 0; cc < 4; ++cc) {
-                            const VT v = *reinterpret_cast<const VT*>(rows + (a * 16 + b * 4 + cc) * k_pad + ch * W);
-                            const V w = (V)A.w[2][cc];
-                            if constexpr (W == 4) {
-                                rb[0] += w * v.x; rb[1] += w * v.y; rb[2] += w * v.z; rb[3] += w * v.w;
-                            } else {
-                                rb[0] += w * v.x; rb[1] += w * v.y;
-                            }
-                        }
-#pragma unroll
-                        for (int e = 0; e < W; ++e) ra[e] += (V)A.w[1][b] * rb[e];
-                    }
-#pragma unroll
-                    for (int e = 0; e < W; ++e) acc[e] += A.w[0][a] * (double)ra[e];
-                }
-#pragma unroll
-                for (int e = 0; e < W; ++e) dot += acc[e] * acc[e];
-            }
+            for (int ch = lane; ch < nch; ch += 32) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
             // mean: each lane takes 2 of the 64 nodes
             double mu = 0.0;
             if (mean_out) {
@@ -474,25 +561,7 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
             }
             dot = warp_sum(dot);
             if (lane != 0) continue;
-            double prior;
-            if (prior_mode == LOVE_PRIOR_EXACT) {
-                prior = s2;
-            } else {
-                prior = s2;
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    double acc = 0.0;
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) acc += A.w[d][a] * A.w[d][b] * c4.c[d][a > b ? a - b : b - a];
-                    prior *= acc;
-                }
-            }
-            const double v = prior - dot;
-            out[q] = (V)v;
-            if (v < 0.0) atomicAdd(&counters[0], 1ull);
-            if (mean_out) mean_out[q] = (V)mu;
+            finish_sorted3<V>(A, c4, s2, prior_mode, dot, mu, q, out, mean_out, counters);
         }
     }
 }
@@ -562,7 +631,7 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
         ensure_smem((const void*)predict_sorted3_kernel<V>, sm);
         LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm, s, c.g, c4, c.rbf.outputscale,
                     c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters);
+                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters, std::getenv("LOVE_SORTED3_LANE") ? std::atoi(std::getenv("LOVE_SORTED3_LANE")) : kLanePerQuery);
         LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, qstart, m, perm, out, mean_out, c.counters);
         cuda_check(cudaFreeAsync(key, s), "query sort free");
         cuda_check(cudaFreeAsync(perm, s), "query sort free");
