@@ -13,6 +13,7 @@
 // probe y): a = ||y|| Rc L^{-1} e_1, also streamed.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "love_internal.h"
@@ -170,6 +171,10 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     const int from_r = pass == 0;
     double* __restrict__ c_out = st.c_cur + ((int64_t)pass * st.crep + blockIdx.x % st.crep) * c_stride(st, k);
     const int ncols = j + 1;
+    // column groups (blockIdx.y, small n): this CTA sweeps columns [cbeg, cend) only
+    const int cpg = (int)round_up(ceil_div(ncols, gridDim.y), 8);
+    const int cbeg = blockIdx.y * cpg, cend = min(ncols, cbeg + cpg);
+    if (cbeg >= cend) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double* csum = smd;                                   // [nw][ncols]
     const double sj = st.qscale[j];
@@ -191,7 +196,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     }
     const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
     constexpr int NB = LOVE_SWEEP_NB;                    // 8-column blocks whose loads are issued together
-    for (int c00 = 0; c00 < ncols; c00 += 8 * NB) {
+    for (int c00 = cbeg; c00 < cend; c00 += 8 * NB) {
     V pvb[NB][8];
 #pragma unroll
     for (int bb = 0; bb < NB; ++bb)
@@ -200,7 +205,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
             V& pcell = pvb[bb][cc];
             const int cidx = c00 + 8 * bb + cc;
             pcell = V(0);
-            if (cidx < ncols) {
+            if (cidx < cend) {
 #pragma unroll
                 for (int u = 0; u < CPT; ++u) {
                     if (qv[u] < nvec) {
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
 #pragma unroll
     for (int bb = 0; bb < NB; ++bb) {
         const int c0 = c00 + 8 * bb;
-        if (c0 >= ncols) break;
+        if (c0 >= cend) break;
         const V* pv = pvb[bb];
         // reduce-scatter: keep 4 of 8 (xor 4), 2 of 4 (xor 2), 1 of 2 (xor 1)
         double h4[4], h2[2];
@@ -237,11 +242,11 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
         h1 += __shfl_xor_sync(0xffffffffu, h1, 8);
         h1 += __shfl_xor_sync(0xffffffffu, h1, 16);
         const int col = c0 + (b2 << 2 | b1 << 1 | b0);
-        if (lane < 8 && col < ncols) csum[wid * ncols + col] = h1;
+        if (lane < 8 && col < cend) csum[wid * ncols + col] = h1;
     }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
+    for (int i = cbeg + threadIdx.x; i < cend; i += blockDim.x) {
         double tot = 0.0;
         for (int w = 0; w < nw; ++w) tot += csum[w * ncols + i];
         atomicAdd(&c_out[i], tot * st.qscale[i]);
@@ -531,6 +536,13 @@ struct StepPlan {
 
 // Enqueue one Lanczos step (the step index lives in device memory).  j_host only picks the
 // z buffer of the step (z_j alternates between two buffers).
+// dots grid: one CTA per 256 row chunks, and column groups when that leaves the GPU idle
+inline dim3 dots_grid(int64_t ldq, int W, int k) {
+    const int gx = (int)ceil_div(ldq / W, 256);
+    const int cg = std::max(1, std::min({16, (148 * 2) / std::max(gx, 1), (k + 7) / 8}));
+    return dim3((unsigned)gx, (unsigned)cg);
+}
+
 template <typename V>
 void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     Cache& c = *pl.c;
@@ -581,7 +593,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
-            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
+            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), dots_grid(pl.ldq, VecT<V>::W, pl.k), 256,
                         sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, 1, r, st, (const int*)st.pro);
         }
         {
@@ -594,7 +606,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     for (int pass = 0; pass < pl.P; ++pass) {
         {
             ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
-            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), (int)ceil_div(pl.ldq / VecT<V>::W, 256), 256,
+            LOVE_LAUNCH((reorth_dots_sweep_kernel<V, 1>), dots_grid(pl.ldq, VecT<V>::W, pl.k), 256,
                         sizeof(double) * 8 * (pl.k + 1), s, Q, pl.ldq, pl.k, pass, r, st, (const int*)nullptr);
         }
         if (c.comm != nullptr) {
@@ -809,7 +821,7 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
                             int last_pass, const double* r, double tol, cudaStream_t s) {
     const size_t smd = sizeof(double) * 8 * (k + 1);
     ensure_smem((const void*)reorth_dots_sweep_kernel<double, 1>, smd);
-    LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), (int)ceil_div(ldq / 2, 256), 256, smd, s, (const double*)Q, ldq,
+    LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), dots_grid(ldq, 2, k), 256, smd, s, (const double*)Q, ldq,
                 k, pass, r, st, (const int*)nullptr);
     const int gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ldq / 2, 256), 148 * 8));
     const size_t smu = sizeof(double) * (k + 1);
