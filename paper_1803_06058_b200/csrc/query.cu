@@ -631,7 +631,7 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
         ensure_smem((const void*)predict_sorted3_kernel<V>, sm);
         LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm, s, c.g, c4, c.rbf.outputscale,
                     c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters, std::getenv("LOVE_SORTED3_LANE") ? std::atoi(std::getenv("LOVE_SORTED3_LANE")) : kLanePerQuery);
+                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters, kLanePerQuery);
         LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, qstart, m, perm, out, mean_out, c.counters);
         cuda_check(cudaFreeAsync(key, s), "query sort free");
         cuda_check(cudaFreeAsync(perm, s), "query sort free");
