@@ -93,3 +93,45 @@ def test_cfg4_full_size_vs_oracle_fixture():
     # the mean is a Krylov solve (Eq. 3) at k = 100, far from converged at cfg4: fp32 vs fp64
     # Lanczos drift sets its error ("mean parity"), ~2e-3 of max|mean|
     assert np.max(np.abs(mg - d["mean"])) < 5e-3 * np.abs(d["mean"]).max()
+
+
+def test_full_size_cfg6_additive():
+    """Config 6 (Eq. 16 additive composition, 10 components x 100 nodes, n = t = 1e5, k = 100)
+    at full size, through love_build_cache_additive as bench.py runs it: variances and means
+    on a seeded sample of the test points vs the oracle's additive model."""
+    from paper_1803_06058_b200 import LoveCache
+    p = CONFIGS[6]
+    inp = make_inputs(p)
+    s2 = [p.outputscale] * p.d if np.isscalar(p.outputscale) else list(p.outputscale)
+    c = LoveCache.build_additive(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, s2, p.sigma2, p.k,
+                                 precision=p.precision)
+    var, mean = c.predict_var(torch.from_numpy(inp.Xs).cuda(), return_mean=True)
+    model = O.build_model_additive(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, s2, p.sigma2)
+    oc = O.love_precompute(model, p.k)
+    assert c.info()["k_eff"] == oc.lanczos.k_eff
+    idx = np.sort(np.random.default_rng(7).choice(p.t, 5_000, replace=False))
+    ov = O.predict_var(model, oc, inp.Xs[idx])
+    ia, wa = O.model_interp(model, inp.Xs[idx])
+    prior = O.prior_ski(model, ia, wa, ia, wa)
+    got = var.cpu().numpy()[idx].astype(np.float64)
+    err = np.abs(got - ov)
+    assert np.all(err <= 1e-3 * np.abs(ov) + 1e-6 * prior), np.max(err / (1e-3 * np.abs(ov) + 1e-6 * prior))
+    om = O.predict_mean(model, oc, inp.Xs[idx])
+    assert np.max(np.abs(mean.cpu().numpy()[idx] - om)) < 1e-3 * np.abs(om).max()
+
+
+def test_max_k_fp64_equals_dense_gp():
+    """k at the ABI maximum (2048): the dots / update kernels at their largest shared-memory
+    footprint.  With n = 3001 points on m = 256 nodes the Lanczos breaks down near m; LOVE
+    then equals the dense SKI GP (Eq. 7) to fp64 round-off."""
+    from synth import scaled_config
+    p = scaled_config(1, n=3001, t=1001, precision="fp64")
+    inp = make_inputs(p)
+    c = _build(p, inp, k=2048)
+    k_eff = c.info()["k_eff"]
+    assert 1 < k_eff < 2048
+    var, mean = c.predict_var(torch.from_numpy(inp.Xs).cuda(), return_mean=True)
+    model = O.build_model(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2)
+    md, vd = O.dense_ski_gp(model, inp.Xs)
+    np.testing.assert_allclose(var.cpu().numpy(), vd, rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(mean.cpu().numpy(), md, rtol=1e-8, atol=1e-10)
