@@ -397,9 +397,9 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         V acc[W];
 #pragma unroll
         for (int e = 0; e < W; ++e) acc[e] = V(0);
-        // columns are swept LAST to first: every CTA is resident at once, so the dots pass
-        // streamed Q~ column by column and its last columns are the ones still in L2; the
-        // next step's dots pass starts at column 0, the one this pass reads last.
+        // columns are swept LAST to first: the dots pass streamed Q~ from column 0 up, so its
+        // last columns are the ones still in L2; the next step's dots pass starts at column
+        // 0, the one this pass reads last.
 #pragma unroll kUpdU
         for (int i = ncols - 1; i >= 0; --i) {
             V a[W];
