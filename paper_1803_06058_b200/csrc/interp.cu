@@ -186,10 +186,12 @@ __global__ void build_items_kernel(const int* __restrict__ start, const int* __r
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m_total) return;
     const int b = start[c], e = start[c + 1];
-    int it = item0[c];
-    for (int p = b; p < e; p += kItemMax, ++it) {
-        item_cell[it] = c;
-        item_start[it] = p;
+    const int it0 = item0[c];
+    // ceil(cnt / kItemMax) items of (nearly) equal size: the lanes of a warp loop alike
+    const int cnt = e - b, nit = (cnt + kItemMax - 1) / kItemMax;
+    for (int i = 0; i < nit; ++i) {
+        item_cell[it0 + i] = c;
+        item_start[it0 + i] = b + (int)((int64_t)i * cnt / nit);
     }
     if (c == m_total - 1) item_start[item0[m_total]] = (int)n;
 }
