@@ -60,6 +60,50 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
     for (int l = 0; l < S; ++l) M[(int64_t)l * n_items + it] = (MT)acc[l];
 }
 
+// d = 2 item moments with two lanes per item (interleaved points, one load batch each,
+// combined by a shuffle): the 16 fp64 accumulators of an item of ~8 points in half the chain
+template <typename V>
+__global__ void __launch_bounds__(256) moments2_tpc_kernel(int64_t n_items, const int* __restrict__ item_start,
+                                                           const V* __restrict__ f0, const V* __restrict__ f1,
+                                                           const V* __restrict__ qbase, StepRef ref,
+                                                           double* __restrict__ M) {
+    pdl_wait();
+    constexpr int B = 4;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t it = gt >> 1;
+    const int sub = (int)(gt & 1);
+    if (step_done(ref)) return;
+    const bool live = it < n_items;
+    const V* __restrict__ q = qbase + step_j(ref) * ref.ld;
+    const int p0 = live ? item_start[it] : 0, p1 = live ? item_start[it + 1] : 0;
+    double acc[16];
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] = 0.0;
+    for (int pb = p0 + sub; pb < p1; pb += 2 * B) {
+        double qv[B], fa[B], fb[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int p = pb + 2 * u;
+            const bool in = p < p1;
+            qv[u] = in ? (double)q[p] : 0.0;
+            fa[u] = in ? (double)f0[p] : 0.0;
+            fb[u] = in ? (double)f1[p] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            double w0[4], w1[4];
+            keys4<double>(fa[u], w0);
+            keys4<double>(fb[u], w1);
+            stencil_accum<double, 2>(acc, qv[u], w0, w1, w1);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < 16; ++l) acc[l] += __shfl_xor_sync(0xffffffffu, acc[l], 1);
+    if (!live || sub != 0) return;
+#pragma unroll
+    for (int l = 0; l < 16; ++l) M[(int64_t)l * n_items + it] = acc[l];
+}
+
 // ---- separable node pull of the scatter (d >= 2), u = W q from the per-item moments
 // M[l][item], slot l = ((a*4 + b)*4 + c) (d = 3) or a*4 + b (d = 2), last index along the
 // last grid axis.  Node (i_0, .., i_{d-1}) receives slot component s_e from cell i_e - s_e + 1
@@ -384,7 +428,9 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
     const int m = c.g.m_total;
     if (c.g.d >= 2 && c.pullT != nullptr) {
         if (c.g.d == 2) {
-            if (ni) LOVE_LAUNCH((moments_kernel<V, 2, double>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, M);
+            if (ni)
+                LOVE_LAUNCH(moments2_tpc_kernel<V>, (int)ceil_div(2 * ni, 256), 256, 0, s, ni, c.item_start, f0, f1, q,
+                            ref, M);
             LOVE_LAUNCH((pull_last_kernel<2, double>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
                         c.cell_item_start, (const double*)M, ref, (double*)c.pullT);
             LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
