@@ -11,6 +11,7 @@
 //  * gather: one thread per item loads the 4^d z values of its cell's stencil once and
 //    reuses them for every point of the item.
 #include <cuda_runtime.h>
+#include <type_traits>
 
 #include "love_internal.h"
 #include "ski_device.cuh"
@@ -20,6 +21,13 @@ namespace love {
 namespace {
 
 constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
+#ifndef LOVE_PAIRED3
+#define LOVE_PAIRED3 1
+#endif
+constexpr bool kPaired3 = LOVE_PAIRED3;   // 3-D fp32 moments on FFMA2 pairs
+// the paired 3-D gather (two points per FFMA2) is bitwise identical but measured slower
+// (cfg4 gather 3.98 -> 4.19 ms per build): off
+constexpr bool kPairedGather3 = false;
 
 template <typename V, int D, typename MT>
 __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
@@ -33,6 +41,50 @@ __global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int
     if (it >= n_items || step_done(ref)) return;
     const V* __restrict__ q = qbase + step_j(ref) * ref.ld;
     const int p0 = item_start[it], p1 = item_start[it + 1];
+    if constexpr (D == 3 && std::is_same<A, float>::value && kPaired3) {
+        // accumulators in pairs (slots c, c + 1 of one (a, b)): one FFMA2 per pair, the
+        // point's (a, b) factor broadcast; the same FMA per slot as stencil_accum
+        f32x2 acc2[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) acc2[l] = 0ull;
+        for (int pb = p0; pb < p1; pb += kBatch) {
+            float qv[kBatch], fa[kBatch], fb[kBatch], fc[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int p = pb + u;
+                const bool in = p < p1;
+                qv[u] = in ? (float)q[p] : 0.f;
+                fa[u] = in ? (float)f0[p] : 0.f;
+                fb[u] = in ? (float)f1[p] : 0.f;
+                fc[u] = in ? (float)f2[p] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                float w0[4], w1[4], w2[4];
+                keys4<float>(fa[u], w0);
+                keys4<float>(fb[u], w1);
+                keys4<float>(fc[u], w2);
+                const f32x2 w2lo = pk2(w2[0], w2[1]), w2hi = pk2(w2[2], w2[3]);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const float ta = qv[u] * w0[a];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const float tb = ta * w1[b];
+                        const f32x2 tt = pk2(tb, tb);
+                        acc2[(a * 4 + b) * 2] = fma2(tt, w2lo, acc2[(a * 4 + b) * 2]);
+                        acc2[(a * 4 + b) * 2 + 1] = fma2(tt, w2hi, acc2[(a * 4 + b) * 2 + 1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            M[(int64_t)(2 * l) * n_items + it] = (MT)lo2(acc2[l]);
+            M[(int64_t)(2 * l + 1) * n_items + it] = (MT)hi2(acc2[l]);
+        }
+        return;
+    }
     A acc[S];
 #pragma unroll
     for (int l = 0; l < S; ++l) acc[l] = A(0);
@@ -227,6 +279,35 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                 fb[u] = (D > 1 && in) ? (A)f1[p] : A(0);
                 fc[u] = (D > 2 && in) ? (A)f2[p] : A(0);
             }
+            if constexpr (D == 3 && std::is_same<A, float>::value && kPairedGather3) {
+#pragma unroll
+                for (int u = 0; u < kBatch; u += 2) {          // two points per FFMA2
+                    float wa[4], wb[4], ua[4], ub[4], va[4], vb[4];
+                    keys4<float>(fa[u], wa);
+                    keys4<float>(fa[u + 1], wb);
+                    keys4<float>(fb[u], ua);
+                    keys4<float>(fb[u + 1], ub);
+                    keys4<float>(fc[u], va);
+                    keys4<float>(fc[u + 1], vb);
+                    f32x2 w0[4], w1[4], w2[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        w0[i] = pk2(wa[i], wb[i]);
+                        w1[i] = pk2(ua[i], ub[i]);
+                        w2[i] = pk2(va[i], vb[i]);
+                    }
+                    const f32x2 d2 = stencil_dot3_pair(w0, w1, w2, zl);
+                    const float rv0 = lo2(d2) + vsig * qv[u], rv1 = hi2(d2) + vsig * qv[u + 1];
+                    if (pb + u < p1) {
+                        r[pb + u] = (V)rv0;
+                        alpha += (double)(vsc * qv[u]) * (double)(V)rv0;
+                    }
+                    if (pb + u + 1 < p1) {
+                        r[pb + u + 1] = (V)rv1;
+                        alpha += (double)(vsc * qv[u + 1]) * (double)(V)rv1;
+                    }
+                }
+            } else {
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) {
                 A w0[4], w1[4], w2[4];
@@ -238,6 +319,7 @@ __global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
                     r[pb + u] = rv;
                     alpha += (double)(vsc * qv[u]) * (double)rv;
                 }
+            }
             }
         }
     }

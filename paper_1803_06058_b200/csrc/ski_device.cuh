@@ -101,6 +101,59 @@ __device__ __forceinline__ void stencil_accum(A acc[Slots<D>::value], A v, const
     }
 }
 
+// ---- packed fp32 pairs (Blackwell FFMA2: fma.rn.f32x2).  A pair lives in one 64-bit
+// register; a scalar operand packed as {x, x} is folded by ptxas into a broadcast operand.
+// Per lane the result is the scalar FMA's, bit for bit.
+using f32x2 = unsigned long long;
+__device__ __forceinline__ f32x2 pk2(float a, float b) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float lo2(f32x2 v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a;
+}
+__device__ __forceinline__ float hi2(f32x2 v) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return b;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+// w^T z over the 64-node stencil for TWO points of the same cell (the 3-D fp32 gather):
+// the same FMA sequence as stencil_dot<float, 3> per point, two points per instruction
+__device__ __forceinline__ f32x2 stencil_dot3_pair(const f32x2 w0[4], const f32x2 w1[4], const f32x2 w2[4],
+                                                   const float zl[64]) {
+    f32x2 acc = 0ull;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        f32x2 ta = 0ull;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            f32x2 tb = 0ull;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const float zv = zl[(a * 4 + b) * 4 + cc];
+                tb = fma2(w2[cc], pk2(zv, zv), tb);
+            }
+            ta = fma2(w1[b], tb, ta);
+        }
+        acc = fma2(w0[a], ta, acc);
+    }
+    return acc;
+}
+
 // (W v)[i] = sum over slots l of the moments M[l][item] of the items of cell i - l + 1
 template <int D>
 __device__ __forceinline__ double node_pull(const GridDev& g, int64_t n_items, const int* __restrict__ cis,
