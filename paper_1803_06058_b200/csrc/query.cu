@@ -12,6 +12,11 @@
 #include <cstdlib>
 
 #include "love_internal.h"
+#include "ski_device.cuh"
+
+#ifndef LOVE_PAIRED_Q3
+#define LOVE_PAIRED_Q3 1
+#endif
 
 namespace love {
 
@@ -420,6 +425,40 @@ template <typename V>
 __device__ __forceinline__ double sorted3_chunk(const Stencil& A, const V* rows, int k_pad, int ch) {
     constexpr int W = QV<V>::W;
     using VT = typename QV<V>::T;
+#if LOVE_PAIRED_Q3
+    if constexpr (W == 4) {
+        // fp32: the four k values as two FFMA2 pairs, the weights broadcast (same FMA per k)
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            f32x2 ra01 = 0ull, ra23 = 0ull;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                f32x2 rb01 = 0ull, rb23 = 0ull;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const float4 v = *reinterpret_cast<const float4*>(rows + (a * 16 + b * 4 + cc) * k_pad + ch * 4);
+                    const float w = (float)A.w[2][cc];
+                    const f32x2 ww = pk2(w, w);
+                    rb01 = fma2(ww, pk2(v.x, v.y), rb01);
+                    rb23 = fma2(ww, pk2(v.z, v.w), rb23);
+                }
+                const float w1b = (float)A.w[1][b];
+                const f32x2 w1 = pk2(w1b, w1b);
+                ra01 = fma2(w1, rb01, ra01);
+                ra23 = fma2(w1, rb23, ra23);
+            }
+            acc[0] += A.w[0][a] * (double)lo2(ra01);
+            acc[1] += A.w[0][a] * (double)hi2(ra01);
+            acc[2] += A.w[0][a] * (double)lo2(ra23);
+            acc[3] += A.w[0][a] * (double)hi2(ra23);
+        }
+        double dot = 0.0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dot += acc[e] * acc[e];
+        return dot;
+    }
+#endif
     double acc[W];
 #pragma unroll
     for (int e = 0; e < W; ++e) acc[e] = 0.0;
