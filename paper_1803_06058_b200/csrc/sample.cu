@@ -12,10 +12,13 @@
 //   G = W_{X*}^T S (t x k'),  mu = W_{X*}^T a,  F = mu 1^T + G zeta    (Eq. 11)
 //   zeta from the caller (shared-draw parity) or Philox4x32-10 + Box-Muller (reading A24).
 #include <cuda_runtime.h>
+#include <type_traits>
+#include <cstdlib>
 
 #include <cmath>
 
 #include "love_internal.h"
+#include "ski_device.cuh"
 
 namespace love {
 
@@ -360,52 +363,78 @@ __global__ void zeta_convert_kernel(const double* __restrict__ in, int ks, int k
     }
 }
 
-// F[i + j*t] = mu[i] + sum_c G[i*ks_pad + c] zeta[j*ks_pad + c]    (FP32 FMA tiles, no tensor cores)
-// CTA tile: 64 points x 64 samples, 256 threads each computing 4 x 4; K staged 16 at a time.
+// F[i + j*t] = mu[i] + sum_c G[i*ks_pad + c] zeta[j*ks_pad + c], register-blocked: CTA tile
+// 128 points x 128 samples, 256 threads of 8 x 8 (two runs of 4 consecutive points x two runs
+// of 4 samples, read from shared memory as 16-byte vectors), FFMA2 pairs along the points with
+// the sample value broadcast; threads run along the points, so a warp's stores of one sample
+// column are 256 contiguous bytes.
+constexpr int kSgT = 128, kSgS = 128, kSgK = 16;
+
 template <typename V>
-__global__ void __launch_bounds__(256) sample_gemm_kernel(const float* __restrict__ G, const float* __restrict__ Z,
-                                                          const float* __restrict__ mu, int ks_pad, int64_t t,
-                                                          int64_t s, V* __restrict__ F) {
-    __shared__ float Gs[16][64 + 4];
-    __shared__ float Zs[16][64 + 4];
-    const int64_t i0 = (int64_t)blockIdx.x * 64, j0 = (int64_t)blockIdx.y * 64;
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;      // 16 x 16 threads
-    float acc[4][4];
+__global__ void __launch_bounds__(256) sample_gemm2_kernel(const float* __restrict__ G, const float* __restrict__ Z,
+                                                           const float* __restrict__ mu, int ks_pad, int64_t t,
+                                                           int64_t s, V* __restrict__ F) {
+    __shared__ __align__(16) float Gs[kSgK][kSgT + 4];
+    __shared__ __align__(16) float Zs[kSgK][kSgS + 4];
+    const int64_t i0 = (int64_t)blockIdx.x * kSgT, j0 = (int64_t)blockIdx.y * kSgS;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    f32x2 acc[4][8];                            // [point pair][sample]
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-    for (int k0 = 0; k0 < ks_pad; k0 += 16) {
-        for (int e = threadIdx.x; e < 16 * 64; e += 256) {
-            const int r = e / 16, kk = e % 16;                  // coalesced along k
+        for (int b = 0; b < 8; ++b) acc[a][b] = 0ull;
+    for (int k0 = 0; k0 < ks_pad; k0 += kSgK) {
+        for (int e = threadIdx.x; e < kSgK * kSgT; e += 256) {
+            const int r = e / kSgK, kk = e - r * kSgK;          // coalesced along k
             const int64_t gi = i0 + r, zj = j0 + r;
             Gs[kk][r] = (gi < t && k0 + kk < ks_pad) ? G[gi * ks_pad + k0 + kk] : 0.f;
             Zs[kk][r] = (zj < s && k0 + kk < ks_pad) ? Z[zj * ks_pad + k0 + kk] : 0.f;
         }
         __syncthreads();
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) {
-            float ga[4], zb[4];
+        for (int kk = 0; kk < kSgK; ++kk) {
+            const float4 g0 = *reinterpret_cast<const float4*>(&Gs[kk][tx * 4]);
+            const float4 g1 = *reinterpret_cast<const float4*>(&Gs[kk][64 + tx * 4]);
+            const float4 z0 = *reinterpret_cast<const float4*>(&Zs[kk][ty * 4]);
+            const float4 z1 = *reinterpret_cast<const float4*>(&Zs[kk][64 + ty * 4]);
+            const f32x2 gp[4] = {pk2(g0.x, g0.y), pk2(g0.z, g0.w), pk2(g1.x, g1.y), pk2(g1.z, g1.w)};
+            const float zv[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
 #pragma unroll
-            for (int a = 0; a < 4; ++a) ga[a] = Gs[kk][ty + 16 * a];
+            for (int b = 0; b < 8; ++b) {
+                const f32x2 zz = pk2(zv[b], zv[b]);
 #pragma unroll
-            for (int b = 0; b < 4; ++b) zb[b] = Zs[kk][tx + 16 * b];
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) acc[a][b] += ga[a] * zb[b];
+                for (int a = 0; a < 4; ++a) acc[a][b] = fma2(gp[a], zz, acc[a][b]);
+            }
         }
         __syncthreads();
     }
+    // rows: i0 + tx*4 + {0..3} (pairs 0, 1) and i0 + 64 + tx*4 + {0..3} (pairs 2, 3)
+    float m4[8];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int64_t gi = i0 + ty + 16 * a;
-        if (gi >= t) continue;
-        const float m0 = mu[gi];
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int64_t zj = j0 + tx + 16 * b;
-            if (zj < s) F[zj * t + gi] = (V)(m0 + acc[a][b]);
+        for (int e = 0; e < 4; ++e) {
+            const int64_t gi = i0 + h * 64 + tx * 4 + e;
+            m4[h * 4 + e] = gi < t ? mu[gi] : 0.f;
+        }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int64_t zj = j0 + (b < 4 ? ty * 4 + b : 64 + ty * 4 + (b - 4));
+        if (zj >= s) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t gi = i0 + h * 64 + tx * 4;
+            const float v0 = m4[h * 4 + 0] + lo2(acc[2 * h][b]), v1 = m4[h * 4 + 1] + hi2(acc[2 * h][b]);
+            const float v2 = m4[h * 4 + 2] + lo2(acc[2 * h + 1][b]), v3 = m4[h * 4 + 3] + hi2(acc[2 * h + 1][b]);
+            V* dst = F + zj * t + gi;
+            if (std::is_same<V, float>::value && gi + 3 < t && ((zj * t + gi) & 3) == 0) {
+                *reinterpret_cast<float4*>(dst) = make_float4(v0, v1, v2, v3);
+            } else {
+                if (gi < t) dst[0] = (V)v0;
+                if (gi + 1 < t) dst[1] = (V)v1;
+                if (gi + 2 < t) dst[2] = (V)v2;
+                if (gi + 3 < t) dst[3] = (V)v3;
+            }
         }
     }
 }
@@ -557,8 +586,8 @@ void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns, uint
         LOVE_LAUNCH(philox_normal_kernel, (int)std::min<int64_t>(ceil_div(ns * ks, 1024), 4096), 256, 0, s, seed, ks, kp,
                     ns, Z);
     }
-    dim3 grid((unsigned)ceil_div(t, 64), (unsigned)ceil_div(ns, 64));
-    LOVE_LAUNCH(sample_gemm_kernel<V>, grid, 256, 0, s, G, Z, mu, kp, t, ns, out);
+    const dim3 grid((unsigned)ceil_div(t, kSgT), (unsigned)ceil_div(ns, kSgS));
+    LOVE_LAUNCH(sample_gemm2_kernel<V>, grid, 256, 0, s, G, Z, mu, kp, t, ns, out);
     cuda_check(cudaFreeAsync(G, s), "sample free");
     cuda_check(cudaFreeAsync(mu, s), "sample free");
     cuda_check(cudaFreeAsync(Z, s), "sample free");
