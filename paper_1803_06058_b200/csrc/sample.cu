@@ -6,7 +6,7 @@
 //   breakdown rule of reading A12  ->  Q' (m x k'), T' (k' x k'); the steps run on the grid
 //   Lanczos machinery (device step index, CUDA-graph replay, the fp64 reorthogonalisation
 //   kernels of lanczos.cu) with this operator and without the Cholesky of T
-//   T' = V diag(lambda) V^T (cyclic Jacobi, one CTA), T'^{1/2} = V diag(sqrt(max(lambda, 0))) V^T
+//   T' = V diag(lambda) V^T (multisection + twisted factorisation, one CTA), T'^{1/2} = V diag(sqrt(max(lambda, 0))) V^T
 //   S = Q' T'^{1/2}  (reading A15: the unique PSD root replaces the Cholesky factor of P:351)
 // Draws (love_sample):
 //   G = W_{X*}^T S (t x k'),  mu = W_{X*}^T a,  F = mu 1^T + G zeta    (Eq. 11)
@@ -52,6 +52,215 @@ __global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ A,
 
 
 
+
+// ---- eigen-decomposition of the symmetric tridiagonal T' (n <= kMaxKs) in one CTA of 512
+// threads, all stages parallel over the eigenvalues:
+//   1. eigenvalue i by multisection (8 threads, 9 sub-intervals per round, 19 rounds from the
+//      Gershgorin interval: 9^-19 ~ 2^-60 of it) on the Sturm count of T' - x I;
+//   2. its eigenvector by a twisted factorisation: pivots of the top-down and bottom-up LDL^T
+//      of T' - lambda I, twist index r = argmin |gamma_r|, x_r = 1 and the two one-sided
+//      recurrences (accurate for isolated eigenvalues);
+//   3. classical Gram-Schmidt, twice, inside clusters (gaps < ctol ||T'||_1, default 1e-9,
+//      LOVE_EIG_CTOL) for orthogonality;
+//   4. W = V diag(sqrt(max(lambda, 0))) V^T.
+// LOVE_JACOBI=1 switches to the cyclic Jacobi kernel below (4.4x slower at k' = 100, kept as a
+// cross-check: tests/test_gpu_sampling.py compares the two roots).
+// 1 / x to fp64 accuracy without the division subroutine: MUFU reciprocal + two Newton steps
+// (|x| >= 1e-290 here: the pivots are floored at pivmin)
+__device__ __forceinline__ double rcp64(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(fma(-x, r, 1.0), r, r);
+    r = fma(fma(-x, r, 1.0), r, r);
+    return r;
+}
+
+// number of eigenvalues of T' below x: sign changes of the continuants
+// p_k = (a_k - x) p_{k-1} - b_{k-1}^2 p_{k-2} (p_{-1} = 1), i.e. the negative pivots of the
+// LDL^T of T' - x I, without divisions (rescaled every 8 terms); a zero counts as negative
+__device__ __forceinline__ int sturm_count(const double* a, const double* b2, int n, double x) {
+    double pm = 1.0, pc = a[0] - x;
+    if (pc == 0.0) pc = -1e-300;                 // a zero pivot is taken as -tiny (negative)
+    int cnt = pc < 0.0;
+    for (int k = 1; k < n; ++k) {
+        double pn = (a[k] - x) * pc - b2[k - 1] * pm;
+        if (pn == 0.0) pn = -1e-300 * pc;        // pivot p_k / p_{k-1} = -tiny
+        cnt += (pn > 0.0) != (pc > 0.0);
+        pm = pc;
+        pc = pn;
+        if ((k & 7) == 0) {
+            const double sc = rcp64(fabs(pc) + fabs(pm));
+            pc *= sc;
+            pm *= sc;
+        }
+    }
+    return cnt;
+}
+
+__global__ void __launch_bounds__(512) tridiag_root_kernel(const double* __restrict__ alpha,
+                                                           const double* __restrict__ beta, int n,
+                                                           double* __restrict__ Wout, double* __restrict__ evals,
+                                                           double ctol) {
+    __shared__ double a[kMaxKs], b[kMaxKs], b2[kMaxKs], lam[kMaxKs], sl[kMaxKs];
+    extern __shared__ double Vsm[];                      // [n][n + 1], column i = eigenvector i
+    const int LV = n + 1 + (n & 1 ? 1 : 0);     // odd: column sweeps spread over the banks
+    __shared__ double s_lo, s_hi, s_norm1, s_b2max;
+    __shared__ int cstart[kMaxKs];
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += blockDim.x) {
+        a[i] = alpha[i];
+        b[i] = i + 1 < n ? beta[i] : 0.0;
+        b2[i] = b[i] * b[i];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double lo = 1e300, hi = -1e300, nrm = 0.0, bm = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + fabs(b[i]);
+            lo = fmin(lo, a[i] - r);
+            hi = fmax(hi, a[i] + r);
+            nrm = fmax(nrm, fabs(a[i]) + r);
+            bm = fmax(bm, b2[i]);
+        }
+        const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300;
+        s_lo = lo - pad;
+        s_hi = hi + pad;
+        s_norm1 = nrm;
+        s_b2max = bm;
+    }
+    __syncthreads();
+    const double pivmin = 1e-290 * fmax(1.0, s_b2max);
+    // 1. multisection: 8 threads (sub) per eigenvalue i = tid / 8, 9 sub-intervals per round,
+    // 19 rounds: 9^-19 ~ 2^-60 of the Gershgorin interval
+    for (int i0 = 0; i0 < n; i0 += 64) {
+        const int i = i0 + (tid >> 3), sub = tid & 7;
+        double lo = s_lo, hi = s_hi;
+        for (int it = 0; it < 19; ++it) {
+            const double x = lo + (hi - lo) * (double)(sub + 1) * (1.0 / 9.0);
+            const int cnt = i < n ? sturm_count(a, b2, n, x) : 0;
+            // new interval: between the last x with cnt <= i and the first x with cnt > i
+            double nlo = lo, nhi = hi;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const double xt = __shfl_sync(0xffffffffu, x, (tid & 31 & ~7) + t);
+                const int ct = __shfl_sync(0xffffffffu, cnt, (tid & 31 & ~7) + t);
+                if (ct <= i) nlo = fmax(nlo, xt);
+                else nhi = fmin(nhi, xt);
+            }
+            lo = nlo;
+            hi = nhi;
+        }
+        if (i < n && sub == 0) lam[i] = 0.5 * (lo + hi);
+    }
+    __syncthreads();
+    // 2. twisted factorisation per eigenvalue (thread i)
+    if (tid < n) {
+        const int i = tid;
+        const double l = lam[i];
+        double dp[kMaxKs], dm[kMaxKs];
+        dp[0] = a[0] - l;
+        if (fabs(dp[0]) < pivmin) dp[0] = pivmin;
+        for (int k = 1; k < n; ++k) {
+            double d = (a[k] - l) - b2[k - 1] * rcp64(dp[k - 1]);
+            if (fabs(d) < pivmin) d = pivmin;
+            dp[k] = d;
+        }
+        dm[n - 1] = a[n - 1] - l;
+        if (fabs(dm[n - 1]) < pivmin) dm[n - 1] = pivmin;
+        for (int k = n - 2; k >= 0; --k) {
+            double d = (a[k] - l) - b2[k] * rcp64(dm[k + 1]);
+            if (fabs(d) < pivmin) d = pivmin;
+            dm[k] = d;
+        }
+        int r = 0;
+        double gmin = 1e300;
+        for (int k = 0; k < n; ++k) {
+            const double g = fabs(dp[k] + dm[k] - (a[k] - l));
+            if (g < gmin) {
+                gmin = g;
+                r = k;
+            }
+        }
+        double x = 1.0, nrm = 1.0;
+        Vsm[(r) * LV + (i)] = 1.0;
+        for (int k = r - 1; k >= 0; --k) {          // dp_k x_k + b_k x_{k+1} = 0
+            x = -b[k] * x * rcp64(dp[k]);
+            Vsm[(k) * LV + (i)] = x;
+            nrm += x * x;
+        }
+        x = 1.0;
+        for (int k = r + 1; k < n; ++k) {           // b_{k-1} x_{k-1} + dm_k x_k = 0
+            x = -b[k - 1] * x * rcp64(dm[k]);
+            Vsm[(k) * LV + (i)] = x;
+            nrm += x * x;
+        }
+        const double inv = 1.0 / sqrt(nrm);
+        for (int k = 0; k < n; ++k) Vsm[(k) * LV + (i)] *= inv;
+    }
+    __syncthreads();
+    // 3. clusters (consecutive eigenvalues closer than ctol ||T'||_1): CGS twice per vector.
+    // Twisted-factorisation vectors of eigenvalues a gap g apart are orthogonal to ~eps ||T'|| / g,
+    // so ctol = 1e-9 leaves <= ~1e-7 non-orthogonality outside clusters
+    if (tid == 0) {
+        const double tol = ctol * s_norm1;
+        int c0 = 0;
+        for (int i = 0; i < n; ++i) {
+            if (i > 0 && lam[i] - lam[i - 1] >= tol) c0 = i;
+            cstart[i] = c0;
+        }
+    }
+    __syncthreads();
+    // one warp per cluster (clusters are independent): classical Gram-Schmidt, twice, of each
+    // member against the earlier members, lanes over the n components
+    const int lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+    {
+        int cl = 0;                                  // cluster ordinal of this warp's work
+        for (int c0 = 0; c0 < n;) {
+            int c1 = c0 + 1;
+            while (c1 < n && cstart[c1] == c0) ++c1;
+            if (c1 - c0 > 1 && (cl % nw) == wid) {
+                for (int i = c0 + 1; i < c1; ++i)
+                    for (int pass = 0; pass < 2; ++pass) {
+                        for (int jj = c0; jj < i; ++jj) {
+                            double d = 0.0;
+                            for (int k = lane; k < n; k += 32) d += Vsm[k * LV + jj] * Vsm[k * LV + i];
+                            d = warp_sum(d);
+                            for (int k = lane; k < n; k += 32) Vsm[k * LV + i] -= d * Vsm[k * LV + jj];
+                        }
+                        double nn = 0.0;
+                        for (int k = lane; k < n; k += 32) nn += Vsm[k * LV + i] * Vsm[k * LV + i];
+                        nn = warp_sum(nn);
+                        const double inv = 1.0 / sqrt(nn);
+                        for (int k = lane; k < n; k += 32) Vsm[k * LV + i] *= inv;
+                        __syncwarp();
+                    }
+            }
+            if (c1 - c0 > 1) ++cl;
+            c0 = c1;
+        }
+    }
+    __syncthreads();
+    // 4. W = V diag(sqrt(max(lambda, 0))) V^T
+    for (int i = tid; i < n; i += blockDim.x) {
+        evals[i] = lam[i];
+        sl[i] = sqrt(fmax(lam[i], 0.0));
+    }
+    __syncthreads();
+    double* U = Vsm + (size_t)n * LV;                    // U = V diag(sqrt(max(lambda, 0)))^(1/2)...
+    for (int e = tid; e < n * n; e += blockDim.x) {
+        const int r = e / n, i = e - r * n;
+        U[r * LV + i] = Vsm[r * LV + i] * sqrt(sl[i]);
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += blockDim.x) {      // W = U U^T = V diag(sqrt(lambda)) V^T
+        const int r = e / n, c = e - r * n;
+        const double* ur = U + r * LV;
+        const double* uc = U + c * LV;
+        double acc = 0.0;
+        for (int i = 0; i < n; ++i) acc += ur[i] * uc[i];
+        Wout[e] = acc;
+    }
+}
 
 // ---- cyclic Jacobi eigensolver of the symmetric tridiagonal T' (n <= kMaxKs), one CTA.
 // Parallel round-robin ordering: in each round the n/2 disjoint pairs (p, q) are rotated
@@ -541,8 +750,17 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     double* ev = (double*)dalloc(c, sizeof(double) * ke, s);
     const int N = ke + (ke & 1);
     const size_t smj = sizeof(double) * (2 * (size_t)N * (N + 1) + N) + sizeof(int) * N;
-    ensure_smem((const void*)jacobi_root_kernel, smj);
-    LOVE_LAUNCH(jacobi_root_kernel, 1, 512, smj, s, st.alpha, st.beta, ke, W, ev);
+    if (std::getenv("LOVE_JACOBI") != nullptr) {
+        ensure_smem((const void*)jacobi_root_kernel, smj);
+        LOVE_LAUNCH(jacobi_root_kernel, 1, 512, smj, s, st.alpha, st.beta, ke, W, ev);
+    } else {
+        const size_t smv = sizeof(double) * 2 * (size_t)ke * (ke + 2);
+        // the opt-in limit counts static + dynamic shared memory (the kernel's static arrays
+        // are ~6 KB): request it whenever the sum passes 48 KB
+        ensure_smem((const void*)tridiag_root_kernel, smv + 8192);
+        LOVE_LAUNCH(tridiag_root_kernel, 1, 512, smv, s, st.alpha, st.beta, ke, W, ev,
+                    std::getenv("LOVE_EIG_CTOL") ? std::atof(std::getenv("LOVE_EIG_CTOL")) : 1e-9);
+    }
     c.S = dalloc(c, c.vsize * (size_t)m * c.ks_pad, s);
     const size_t smr = sizeof(double) * ke * ke;
     if (c.precision == LOVE_FP64) {

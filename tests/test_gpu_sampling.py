@@ -128,3 +128,19 @@ def test_cfg5_full_size_monte_carlo():
     chat = (dev[ia] * dev[ib]).sum(1) / (s - 1)
     se = np.sqrt((var[ia] * var[ib] + cov ** 2) / (s - 1))
     assert np.all(np.abs(chat - cov) <= 6.5 * se + 1e-6)
+
+
+def test_tridiag_root_matches_jacobi_root(monkeypatch):
+    """The sampling root's eigensolver (multisection + twisted factorisation + CGS2 in
+    clusters) against the cyclic Jacobi kernel (LOVE_JACOBI=1) on the same fp64 build, past
+    breakdown so T' carries its cluster of ~0 eigenvalues: S S^T agrees to 1e-9 of its max."""
+    p, inp = tiny_problem("1d_n200")
+    S = {}
+    for jac in (False, True):
+        if jac:
+            monkeypatch.setenv("LOVE_JACOBI", "1")
+        c = _build(p, inp, precision="fp64", k_sample=60)
+        ke = c.info()["k_sample_eff"]
+        Sx = c.export("S").cpu().numpy().reshape(p.m_total, -1)[:, :ke]
+        S[jac] = Sx @ Sx.T
+    assert np.abs(S[False] - S[True]).max() <= 1e-9 * np.abs(S[True]).max()
