@@ -620,10 +620,8 @@ __global__ void twiddle_table_kernel(C* __restrict__ tw, int L, int den) {
 
 __global__ void embed_kernel(const double* __restrict__ c, int m, int N, double* __restrict__ col) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-        double v = 0.0;
-        if (i < m) v = c[i];
-        else if (i > N - m) v = c[N - i];
-        col[i] = v;
+        const int a = min(i, N - i);            // circulant distance (N >= 2m - 1: i < m or i > N - m)
+        col[i] = a < m ? c[a] : 0.0;
     }
 }
 
@@ -779,8 +777,19 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     }
     // d = 1: circulant embedding and its eigenvalues, stored * s^2 / N
     const int m = g.m[0];
+    // Embedding length (reading A25b): the circulant of length N agrees with the
+    // Toeplitz T(c) wherever the grid distance delta <= N/2; at delta > N/2 it holds c_{N-delta}
+    // instead of c_delta.  N >= 2m - 1 makes that set empty.  When the RBF column
+    // falls below 1e-30 c_0 from b = ceil(ls/h sqrt(2 ln 1e30)) on and b < m, N >= m + b is
+    // enough: both c_{N-delta} (N - delta > b) and c_delta (delta > (m+b)/2 > b) are < 1e-30 c_0,
+    // 14 orders below the fp64 rounding of the product.  cfg2: N = 2^17 instead of 2^18.
+    int64_t need = 2 * (int64_t)m - 1;
+    if (std::getenv("LOVE_FULL_EMBED") == nullptr) {
+        const double b = std::ceil(std::sqrt(2.0 * std::log(1e30)) * c.rbf.lengthscale[0] / g.h[0]);
+        if (b < (double)m) need = std::min<int64_t>(need, (int64_t)m + (int64_t)b);
+    }
     int N = 8;
-    while (N < 2 * m - 1) N *= 2;
+    while (N < need) N *= 2;
     if (N > (1 << 22)) throw LoveError{LOVE_ERR_ARG, "1-D grid too long (m <= 2^21)"};
     c.fft_N = N;
     if (N <= kSmallFFT) {
@@ -808,9 +817,10 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     fft_run(c, col, nullptr, N, nullptr, (C*)c.fft_buf, X, 1, s);
     LOVE_LAUNCH(lambda_store_kernel, (int)std::min<int64_t>(ceil_div(N, 256), 4096), 256, 0, s, X, N, c.fft_N1,
                 c.fft_N2, c.fft_N1 != 0, c.rbf.outputscale / (double)N, (double*)c.lam);
-    // measured: the half-length real path wins from N = 2^18 (cfg2) but not at 2^15 (cfg5),
-    // where the passes are latency-bound and half as many CTAs hide less of it
-    if (c.fft_N1 != 0 && N >= (1 << 17) && std::getenv("LOVE_NO_RFFT") == nullptr) {
+    // measured: the half-length real path wins at N = 2^18 but not at 2^17 (cfg2 with the
+    // shortened embedding: 11.2 vs 11.4 ms per build) or 2^15: the passes are latency-bound and
+    // half as many CTAs hide less of it
+    if (c.fft_N1 != 0 && N >= (1 << 18) && std::getenv("LOVE_NO_RFFT") == nullptr) {
         // real-input path: N' = N/2 = R1 * R2 (R1 = 2^floor(lg N'/2)), tables and lambda[0..N']
         const int Np = N / 2, lgp = ilog2(Np);
         c.rfft_N1 = 1 << (lgp / 2);

@@ -21,10 +21,10 @@
 #ifndef LOVE_SWEEP_NB
 #define LOVE_SWEEP_NB 1
 #endif
-#ifndef LOVE_UPD_U
-#define LOVE_UPD_U 7
+#ifndef LOVE_UPD_B
+#define LOVE_UPD_B 8
 #endif
-namespace love { constexpr int kUpdU = LOVE_UPD_U; constexpr int kCondSteps = 2; }
+namespace love { constexpr int kUpdB = LOVE_UPD_B; constexpr int kCondSteps = 2; }
 
 namespace love {
 
@@ -355,7 +355,8 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
                                                             const int* __restrict__ gate) {
     pdl_wait();
     constexpr int W = VecT<V>::W;
-    extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i]
+    extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i], as V
+    V* __restrict__ cfv = reinterpret_cast<V*>(cf);
     __shared__ double red[32];
     const int j = *st.jdev;
     // the last pass's update is the last kernel of step j: its last CTA to finish advances
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
             ci = 0.0;
             for (int rp = 0; rp < st.crep; ++rp) ci += c_in[rp * cst + i];
         }
-        cf[i] = ci * st.qscale[i];
+        cfv[i] = (V)(ci * st.qscale[i]);       // rounded to V once per CTA, not per column
     }
     __syncthreads();
     const double sj = st.qscale[j];
@@ -400,13 +401,29 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         // columns are swept LAST to first: the dots pass streamed Q~ from column 0 up, so its
         // last columns are the ones still in L2; the next step's dots pass starts at column
         // 0, the one this pass reads last.
-#pragma unroll kUpdU
-        for (int i = ncols - 1; i >= 0; --i) {
+        // batches of kUpdB columns: all kUpdB 16-byte loads are issued before the first FMA
+        // (same summation order as one column at a time)
+        const V* col = Q + (int64_t)(ncols - 1) * ldq + p;
+        int i = ncols - 1;
+        for (; i >= kUpdB - 1; i -= kUpdB) {
+            V a[kUpdB][W];
+#pragma unroll
+            for (int u = 0; u < kUpdB; ++u) vload<V>(col - (int64_t)u * ldq, a[u]);
+#pragma unroll
+            for (int u = 0; u < kUpdB; ++u) {
+                const V ci = cfv[i - u];
+#pragma unroll
+                for (int e = 0; e < W; ++e) acc[e] += ci * a[u][e];
+            }
+            col -= (int64_t)kUpdB * ldq;
+        }
+        for (; i >= 0; --i) {
             V a[W];
-            vload<V>(Q + (int64_t)i * ldq + p, a);
-            const V ci = (V)cf[i];
+            vload<V>(col, a);
+            const V ci = cfv[i];
 #pragma unroll
             for (int e = 0; e < W; ++e) acc[e] += ci * a[e];
+            col -= ldq;
         }
         V o[W];
 #pragma unroll

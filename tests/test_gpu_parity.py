@@ -55,6 +55,9 @@ def _rel2(a, b):
     ("cfg2m", 2, None, "fp32"), ("cfg3m", 3, None, "fp32"), ("cfg4m", 4, None, "fp32"),
     ("1d_4096", 1, (4096,), "fp32"), ("1d_2049_fp64", 1, (2049,), "fp64"), ("3d_odd", 4, (9, 10, 11), "fp64"),
     ("1d_65537_fp64", 1, (65537,), "fp64"), ("1d_70001", 1, (70001,), "fp32"),   # real-input half-length FFT
+    # shortened circulant embedding (reading A25b: N >= m + b, c_b < 1e-30 c_0): cfg2's grid at
+    # N = 2^17 instead of 2^18, cfg5's at 2^14 instead of 2^15, m = 2200 on the one-CTA 4096 path
+    ("cfg2m_fp64", 2, None, "fp64"), ("cfg5m_fp64", 5, None, "fp64"), ("1d_2200_fp64", 1, (2200,), "fp64"),
 ])
 def test_kuu_mvm(case):
     name, ci, m, prec = case
