@@ -648,6 +648,24 @@ constexpr int kSmallFFT = 4096;
 constexpr int kLinesPerCta = 2;
 
 // convolution (mode 0) of u (m entries) or forward FFT (mode 1) of u (N entries)
+// complex four-step passes with G lines per CTA (mode 0: convolution, mode 1: forward only)
+template <int G>
+static void fft_four_step(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc,
+                          int mode, cudaStream_t s) {
+    const int N1 = c.fft_N1, N2 = c.fft_N2;
+    const C* tw1 = (const C*)c.tw1;
+    const C* tw2 = (const C*)c.tw2;
+    const C* twF = (const C*)c.twF;
+    const double* lam = (const double*)c.lam;
+    const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
+    ensure_smem((const void*)fft_passA_kernel<G>, smA);
+    ensure_smem((const void*)fft_passB_kernel<G>, smB);
+    ensure_smem((const void*)fft_passC_kernel<G>, smA);
+    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
+    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode, t_done);
+    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
+}
+
 void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc, int mode,
              cudaStream_t s) {
     const int N = c.fft_N, N1 = c.fft_N1, N2 = c.fft_N2;
@@ -677,13 +695,10 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
         LOVE_LAUNCH(rfft_passC_kernel<G>, R1 / G, G * R2 / 8, sA, s, (const C*)work, m, R1, R2, r2, z, t_done);
         return;
     }
-    const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
-    ensure_smem((const void*)fft_passA_kernel<G>, smA);
-    ensure_smem((const void*)fft_passB_kernel<G>, smB);
-    ensure_smem((const void*)fft_passC_kernel<G>, smA);
-    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
-    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode, t_done);
-    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
+    // measured: 4 lines per CTA (16-byte loads in 64-byte runs) win at N <= 2^15 (cfg5 build
+    // 6.11 -> 5.97 ms), 2 lines (twice the CTAs) at 2^17; 1 line loses everywhere
+    if (N <= (1 << 15)) fft_four_step<4>(c, u, Mc, m, z, work, outc, mode, s);
+    else fft_four_step<G>(c, u, Mc, m, z, work, outc, mode, s);
 }
 
 void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
