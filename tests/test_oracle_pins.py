@@ -436,3 +436,30 @@ def test_additive_love_equals_dense_gp_at_full_krylov():
     var = O.predict_var(model, cache, inp.Xs)
     np.testing.assert_allclose(var, var_d, rtol=1e-8, atol=1e-12)
     np.testing.assert_allclose(O.predict_mean(model, cache, inp.Xs), mean_d, rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("m,ls,span", [(100_000, 0.01, 1.1), (10_000, 0.05, 1.1), (2200, 0.05, 1.1), (300, 0.5, 1.1)])
+def test_shortened_circulant_embedding_reading_A25b(m, ls, span):
+    """Reading A25b: with b = ceil(ls/h sqrt(2 ln 1e30)) < m, the circulant of
+    the smallest power-of-two length N >= m + b reproduces the Toeplitz product to fp64
+    rounding.  Checked against the oracle's A25 embedding (N >= 2m - 1) and, at m = 300,
+    against the dense Toeplitz matrix; at m = 300 with ls = 0.5 the band is wider than m and
+    the rule keeps N >= 2m - 1."""
+    h = span / (m - 1)
+    c = O.rbf_column(m, h, ls)
+    b = int(np.ceil(np.sqrt(2.0 * np.log(1e30)) * ls / h))
+    need = min(2 * m - 1, m + b) if b < m else 2 * m - 1
+    N = 8
+    while N < need:
+        N *= 2
+    if m == 100_000:
+        assert N == 1 << 17                      # cfg2: half of A25's 2^18
+    a = np.minimum(np.arange(N), N - np.arange(N))
+    col = np.where(a < m, c[np.minimum(a, m - 1)], 0.0)
+    if b < m:                                    # b is where the column falls below 1e-30 c_0
+        assert c[b] < 1e-30 * c[0] <= c[b - 1]
+    u = np.random.default_rng(3).normal(size=(m, 2))
+    got = np.fft.ifft(np.fft.fft(col)[:, None] * np.fft.fft(np.vstack([u, np.zeros((N - m, 2))]), axis=0),
+                      axis=0)[:m].real
+    want = O.toeplitz_matvec_dense(c, u) if m <= 2200 else O.toeplitz_matvec_fft(c, u)
+    assert np.abs(got - want).max() <= 1e-13 * np.abs(want).max()
