@@ -668,10 +668,8 @@ static void fft_four_step(const Cache& c, const double* u, const double* Mc, int
 
 void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc, int mode,
              cudaStream_t s) {
-    const int N = c.fft_N, N1 = c.fft_N1, N2 = c.fft_N2;
+    const int N = c.fft_N, N1 = c.fft_N1;
     const C* tw1 = (const C*)c.tw1;
-    const C* tw2 = (const C*)c.tw2;
-    const C* twF = (const C*)c.twF;
     const double* lam = (const double*)c.lam;
     if (N1 == 0) {
         const size_t sm = sizeof(C) * (padded(N) + N);
