@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LOVE_ABI_VERSION 3
+#define LOVE_ABI_VERSION 4
 
 typedef struct love_cache love_cache;   /* opaque */
 
@@ -97,8 +97,25 @@ typedef struct {
                                LOVE_VAR_BLOCKS_OFF (1): variances from the Rc rows */
     double reorth_tol;      /* LOVE_LANCZOS_PARTIAL only: reorthogonalise when the estimated loss of
                                orthogonality max_i |q_{j+1}^T q_i| exceeds it; 0 => sqrt(eps) of V */
+    int32_t cache_fp64;     /* precision == LOVE_FP32 only (SURVEY §8(c) reading A21, DESIGN reading A12b):
+                               LOVE_CACHE_FP64_ON: the cache is built in fp64 (Lanczos vectors, CGS2,
+                               breakdown tau 1e-10, Rc, the sampling root: the LOVE_FP64 build) while every
+                               query / sample OUTPUT stays V = float.
+                               LOVE_CACHE_FP64_AUTO (0, default): the fp32 build runs; if its Lanczos breaks
+                               down before k (beta_j < 1e-6 ||T||: the problem is converged, var << prior,
+                               and fp32 vectors cannot resolve beta_j below ~1e-7 ||T||, so the late
+                               directions are round-off), the cache is rebuilt as
+                               with LOVE_CACHE_FP64_ON.  Measured at BASELINE config 5: the fp32 build
+                               stops at k_eff = 37 with variances up to 6 % off the oracle at the same k;
+                               the fp64 cache runs to the oracle's k_eff = 49 and matches it to ~6e-8.
+                               LOVE_CACHE_FP64_OFF: the plain fp32 build, whatever k_eff.
+                               love_info.cache_precision reports which build the cache holds; with an fp64
+                               cache love_ski_mvm / love_kuu_mvm vectors and the RC / S exports are fp64.
+                               For precision == LOVE_FP64 only AUTO / OFF are accepted (no effect). */
+    int32_t reserved1;
 } love_opts;
 enum { LOVE_VAR_BLOCKS_AUTO = 0, LOVE_VAR_BLOCKS_OFF = 1 };
+enum { LOVE_CACHE_FP64_AUTO = 0, LOVE_CACHE_FP64_ON = 1, LOVE_CACHE_FP64_OFF = 2 };
 enum { LOVE_LANCZOS_AUTO = 0, LOVE_LANCZOS_TWO_PASS = 1, LOVE_LANCZOS_ONE_READ = 2, LOVE_LANCZOS_PARTIAL = 3 };
 
 /* Data-parallel sharding of the training points.  Every rank calls
@@ -132,7 +149,8 @@ typedef struct {
     int64_t n_out_of_range; /* query points outside the grid (NaN returned) */
     int32_t n_reorth_steps; /* Lanczos steps that ran the reorthogonalisation (all but the last one,
                                except in LOVE_LANCZOS_PARTIAL) */
-    int32_t reserved0;
+    int32_t cache_precision; /* precision of the cache's factors (Q, Rc, S; LOVE_FP64 when built with
+                               opts.cache_fp64); `precision` above is that of the query / sample outputs */
 } love_info;
 
 /* ---------------------------------------------------------------------------------------
@@ -200,6 +218,9 @@ love_status love_predict_covar(const love_cache* cache, const double* Xa, const 
  *   zeta : NULL (draw N(0,1) with Philox4x32-10 keyed by `seed`, reading A24) or
  *          k_sample_eff x s fp64 column-major (sample j = column j), for shared-draw parity.
  *   out  : t x s values of V, column-major (sample j is contiguous: out[j*t + i]).
+ * Arithmetic: the root S is computed in fp64 (reading A16); G = W_{X*}^T S and mu are accumulated
+ * in fp64 and rounded to float, and F = mu 1^T + G zeta runs on the FP32 FMA pipes (SURVEY §8(a)
+ * a13) for every cache precision: draws from an fp64 cache are accurate to fp32 round-off.
  * Requires a cache built with k_sample > 0 (else LOVE_ERR_STATE). */
 love_status love_sample(const love_cache* cache, const double* Xs, int64_t t, int64_t s,
                         uint64_t seed, const double* zeta, void* out, void* stream);
@@ -219,16 +240,18 @@ const char* love_last_error(void);
  * ------------------------------------------------------------------------------------ */
 
 /* out = (W_X^T K_UU W_X + sigma^2 I) v on this rank's points (mvm_K_XX, Alg. 1).
- * v, out : n_local values of V.  Single-rank caches only (else LOVE_ERR_STATE). */
+ * v, out : n_local values of Vc (the cache precision: V, or double with opts.cache_fp64).
+ * Single-rank caches only (else LOVE_ERR_STATE). */
 love_status love_ski_mvm(const love_cache* cache, const void* v, void* out, void* stream);
 
-/* out = K_UU u (Toeplitz / Kronecker-of-Toeplitz MVM).  u, out : m_total of V. */
+/* out = K_UU u (Toeplitz / Kronecker-of-Toeplitz MVM).  u, out : m_total of Vc. */
 love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void* stream);
 
 enum {
-    LOVE_EXPORT_RC = 0,        /* m_total x k_pad of V, row-major: Rc = K_UU W_X Q L^{-T} */
+    LOVE_EXPORT_RC = 0,        /* m_total x k_pad of Vc, row-major: Rc = K_UU W_X Q L^{-T} */
     LOVE_EXPORT_MEAN = 1,      /* m_total fp64: mean cache a */
-    LOVE_EXPORT_S = 2,         /* m_total x k_sample_eff of V, row-major: sampling root */
+    LOVE_EXPORT_S = 2,         /* m_total x ks_pad of Vc, row-major: sampling root (ks_pad = k_sample_eff
+                                  rounded up to a multiple of 4) */
     LOVE_EXPORT_PERM = 3       /* n_local int32: sorted position -> original point index */
 };
 /* Copies an internal array into the caller's DEVICE buffer `dst` of `capacity` bytes.
@@ -265,7 +288,8 @@ enum {
     LOVE_PROF_SAMPLE = 10,       /* sample draws */
     LOVE_PROF_COMM = 11,         /* NCCL all-reduces */
     LOVE_PROF_FUSED_PASS = 12,   /* one-read pass: lagged update + gather + moments + Gram dots */
-    LOVE_PROF_N = 13
+    LOVE_PROF_SAMPLE_GEMM = 13,  /* the draw product F = mu 1^T + G zeta alone (inside LOVE_PROF_SAMPLE) */
+    LOVE_PROF_N = 14
 };
 void love_profile_enable(int32_t on);
 /* ms_out, calls_out: HOST arrays of LOVE_PROF_N entries (either may be NULL); reset != 0

@@ -15,8 +15,9 @@ LOVE_FP32, LOVE_FP64 = 0, 1
 LOVE_PROBE_Y, LOVE_PROBE_AVGCOL = 0, 1
 LOVE_PRIOR_SKI, LOVE_PRIOR_EXACT = 0, 1
 LOVE_EXPORT_RC, LOVE_EXPORT_MEAN, LOVE_EXPORT_S, LOVE_EXPORT_PERM = 0, 1, 2, 3
+LOVE_CACHE_FP64_AUTO, LOVE_CACHE_FP64_ON, LOVE_CACHE_FP64_OFF = 0, 1, 2
 PROF_NAMES = ["setup", "scatter", "kuu", "gather", "reorth_dots", "reorth_update", "scalars_rc",
-              "finish", "query", "sample_cache", "sample", "comm", "fused_pass"]
+              "finish", "query", "sample_cache", "sample", "comm", "fused_pass", "sample_gemm"]
 
 
 class love_grid(ctypes.Structure):
@@ -32,7 +33,7 @@ class love_opts(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("probe", ctypes.c_int32), ("prior", ctypes.c_int32),
                 ("reorth_passes", ctypes.c_int32), ("breakdown_tol", ctypes.c_double),
                 ("k_sample", ctypes.c_int32), ("lanczos_mode", ctypes.c_int32), ("var_blocks", ctypes.c_int32),
-                ("reorth_tol", ctypes.c_double)]
+                ("reorth_tol", ctypes.c_double), ("cache_fp64", ctypes.c_int32), ("reserved1", ctypes.c_int32)]
 
 
 class love_axis(ctypes.Structure):
@@ -52,7 +53,7 @@ class love_info(ctypes.Structure):
                 ("m_total", ctypes.c_int64), ("n_items", ctypes.c_int64),
                 ("b_norm", ctypes.c_double),
                 ("alpha", ctypes.POINTER(ctypes.c_double)), ("beta", ctypes.POINTER(ctypes.c_double)),
-                ("n_negative_var", ctypes.c_int64), ("n_out_of_range", ctypes.c_int64), ("n_reorth_steps", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("n_negative_var", ctypes.c_int64), ("n_out_of_range", ctypes.c_int64), ("n_reorth_steps", ctypes.c_int32), ("cache_precision", ctypes.c_int32)]
 
 
 # name -> (restype, argtypes); every symbol include/love.h declares

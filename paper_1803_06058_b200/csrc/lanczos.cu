@@ -881,4 +881,13 @@ void finish_cache(Cache& c, cudaStream_t s) {
                     (float*)c.Rc);
 }
 
+// fp64 row-major copy of the cache (m x k_pad) from the fp64 streamed Rc: fp32 caches answer
+// covariances from it (love_predict_covar).  `out` holds m * k_pad doubles.
+void launch_rc_rows64(const Cache& c, double* out, cudaStream_t s) {
+    const int m = c.g.m_total;
+    dim3 grid((unsigned)ceil_div(m, 32), (unsigned)ceil_div(c.k_pad, 32));
+    dim3 block(32, 8);
+    LOVE_LAUNCH(rc_transpose_kernel<double>, grid, block, 0, s, (const double*)c.Rc_col, m, c.k_eff, c.k_pad, out);
+}
+
 }  // namespace love

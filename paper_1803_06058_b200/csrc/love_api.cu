@@ -6,8 +6,11 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 
@@ -33,11 +36,14 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 void ensure_smem(const void* fn, size_t bytes) {
+    // the attribute is per device context: cache it per (device, kernel)
     static std::mutex mu;
-    static std::unordered_map<const void*, size_t> done;
+    static std::map<std::pair<int, const void*>, size_t> done;
     if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     std::lock_guard<std::mutex> g(mu);
-    size_t& cur = done[fn];
+    size_t& cur = done[{dev, fn}];
     if (cur >= bytes) return;
     cuda_check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "smem attr");
     cur = bytes;
@@ -116,6 +122,39 @@ void order_after(cudaStream_t waiter, cudaStream_t producer) {
     cuda_check(cudaEventDestroy(e), "event destroy");
 }
 
+// The exception in flight, as a status (every extern "C" entry point catches everything:
+// nothing may unwind through the C ABI).  Host allocation failures map to LOVE_ERR_OOM.
+LoveError current_error() {
+    try {
+        throw;
+    } catch (const LoveError& e) {
+        return e;
+    } catch (const std::bad_alloc&) {
+        return LoveError{LOVE_ERR_OOM, "host allocation failed"};
+    } catch (const std::exception& e) {
+        return LoveError{LOVE_ERR_CUDA, std::string("internal error: ") + e.what()};
+    } catch (...) {
+        return LoveError{LOVE_ERR_CUDA, "internal error: unknown exception"};
+    }
+}
+
+// The fp64 row-major copy of an fp32 cache's Rc, made once per cache (under a lock, finished
+// before it is published: concurrent queries on other streams never see it half written).
+void* rc_rows64(const Cache& cc, cudaStream_t s) {
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    Cache& c = const_cast<Cache&>(cc);
+    if (c.Rc64 == nullptr) {
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, sizeof(double) * (size_t)c.g.m_total * std::max(c.k_pad, 4)), "cudaMalloc(Rc64)");
+        c.allocs.push_back(p);
+        launch_rc_rows64(c, (double*)p, s);
+        cuda_check(cudaStreamSynchronize(s), "Rc64 sync");
+        c.Rc64 = p;
+    }
+    return c.Rc64;
+}
+
 love_status fail(const LoveError& e) {
     set_error(e.msg);
     return e.status;
@@ -160,6 +199,10 @@ love_opts checked_opts(const love_opts* opts) {
     if (o.k_sample < 0 || o.reorth_passes < 0) throw LoveError{LOVE_ERR_ARG, "bad opts"};
     if (o.var_blocks != LOVE_VAR_BLOCKS_AUTO && o.var_blocks != LOVE_VAR_BLOCKS_OFF)
         throw LoveError{LOVE_ERR_ARG, "bad var_blocks"};
+    if (o.cache_fp64 < LOVE_CACHE_FP64_AUTO || o.cache_fp64 > LOVE_CACHE_FP64_OFF)
+        throw LoveError{LOVE_ERR_ARG, "bad cache_fp64"};
+    if (o.cache_fp64 == LOVE_CACHE_FP64_ON && o.precision != LOVE_FP32)
+        throw LoveError{LOVE_ERR_ARG, "cache_fp64 = LOVE_CACHE_FP64_ON applies to precision == LOVE_FP32 only"};
 
     return o;
 }
@@ -173,25 +216,29 @@ Cache* begin_build(const love_opts& o, double sigma2, int64_t n_local, int32_t& 
         cuda_check(cudaGetDevice(&c->device), "cudaGetDevice");
         keep_pool_memory(c->device);
         c->sigma2 = sigma2;
-        c->precision = o.precision;
-        c->vsize = o.precision == LOVE_FP64 ? 8 : 4;
+        // cache_fp64 (reading A12b): the whole build runs as the fp64 build; only the query and
+        // sample outputs keep the caller's precision
+        const int cprec = o.cache_fp64 == LOVE_CACHE_FP64_ON ? LOVE_FP64 : o.precision;
+        c->precision = cprec;
+        c->out_precision = o.precision;
+        c->vsize = cprec == LOVE_FP64 ? 8 : 4;
         c->probe = o.probe;
         c->prior = o.prior;
         if (o.reorth_passes > 2) throw LoveError{LOVE_ERR_ARG, "reorth_passes must be 0, 1 or 2"};
-        c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (o.precision == LOVE_FP64 ? 2 : 1);
+        c->reorth_passes = o.reorth_passes > 0 ? o.reorth_passes : (cprec == LOVE_FP64 ? 2 : 1);
         int mode = o.lanczos_mode;
         if (const char* e = std::getenv("LOVE_LANCZOS_MODE")) mode = std::atoi(e);
         if (mode < 0 || mode > 3) throw LoveError{LOVE_ERR_ARG, "bad lanczos_mode"};
-        if (mode == LOVE_LANCZOS_ONE_READ && o.precision != LOVE_FP32)
+        if (mode == LOVE_LANCZOS_ONE_READ && cprec != LOVE_FP32)
             throw LoveError{LOVE_ERR_ARG, "the one-read Lanczos pass is fp32 only"};
         c->fused = mode == LOVE_LANCZOS_ONE_READ;
         c->partial = mode == LOVE_LANCZOS_PARTIAL;
         if (c->partial && dist && (dist->world > 1 || dist->nccl_unique_id))
             throw LoveError{LOVE_ERR_ARG, "partial reorthogonalisation runs on one GPU"};
-        if (c->partial && o.precision != LOVE_FP32)
+        if (c->partial && cprec != LOVE_FP32)
             throw LoveError{LOVE_ERR_ARG, "partial reorthogonalisation is fp32 only"};
         if (!(o.reorth_tol >= 0.0)) throw LoveError{LOVE_ERR_ARG, "reorth_tol must be >= 0"};
-        c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (o.precision == LOVE_FP64 ? 1e-10 : 1e-6);
+        c->tol = o.breakdown_tol > 0 ? o.breakdown_tol : (cprec == LOVE_FP64 ? 1e-10 : 1e-6);
         c->k_sample_req = o.k_sample;
         c->n = n_local;
         // a communicator is set up whenever a NCCL id is given (world == 1 runs every
@@ -292,6 +339,11 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
     c->k_eff = hfl[1];
     g_launch_count += c->cond_nodes * (hfl[6] / c->cond_steps);   // kernels of the device-terminated step loop
+    // LOVE_CACHE_FP64_AUTO (reading A12b): an fp32 Lanczos that broke down before k is not
+    // finished -- the caller rebuilds the cache with fp64 factors
+    if (o.cache_fp64 == LOVE_CACHE_FP64_AUTO && c->precision == LOVE_FP32 && !c->partial && !c->fused &&
+        c->k_eff < c->k_req)
+        throw LoveError{kRebuildFp64, "fp32 Lanczos broke down before k: rebuild with an fp64 cache"};
     c->b_norm = std::sqrt(bn2);
     c->n_reorth_steps = std::max(c->k_eff - 1, 0);
     if (c->partial) {
@@ -334,9 +386,9 @@ love_status love_nccl_unique_id(void* out) {
     return nccl_get_unique_id(out);
 }
 
-love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
-                             const double* y, int64_t n_local, int32_t k, const love_opts* opts,
-                             const love_dist* dist, void* stream, love_cache** out) {
+static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
+                                   const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                                   const love_dist* dist, void* stream, love_cache** out) {
     Cache* c = nullptr;
     cudaStream_t s = nullptr;
     try {
@@ -417,7 +469,8 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
         finish_build(c, o, k, s);
         *out = reinterpret_cast<love_cache*>(c);
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         if (c) {
             if (s) cudaStreamSynchronize(s);
             release(c);
@@ -426,9 +479,9 @@ love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double 
     }
 }
 
-love_status love_build_cache_additive(const love_axis* axes, int32_t d, double sigma2, const double* X,
-                                      const double* y, int64_t n_local, int32_t k, const love_opts* opts,
-                                      const love_dist* dist, void* stream, love_cache** out) {
+static love_status build_additive_once(const love_axis* axes, int32_t d, double sigma2, const double* X,
+                                       const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                                       const love_dist* dist, void* stream, love_cache** out) {
     Cache* c = nullptr;
     cudaStream_t s = nullptr;
     try {
@@ -516,13 +569,50 @@ love_status love_build_cache_additive(const love_axis* axes, int32_t d, double s
         finish_build(c, o, k, s);
         *out = reinterpret_cast<love_cache*>(c);
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         if (c) {
             if (s) cudaStreamSynchronize(s);
             release(c);
         }
         return fail(e);
     }
+}
+
+// LOVE_CACHE_FP64_AUTO (reading A12b): an fp32 Lanczos that breaks down before k has reached
+// the point where its fp32 vectors no longer resolve beta_j (tau = 1e-6 ~ 16 eps_32 of ||T||):
+// the problem is converged (var << prior) and the late fp32 directions are round-off.  The fp32
+// build stops right after its Lanczos loop (finish_build throws kRebuildFp64) and the cache is
+// rebuilt with fp64 factors (the outputs stay fp32), which runs to the fp64 breakdown the
+// oracle sees.  Every rank sees the same k_eff, so they all take the same branch.
+
+static love_opts with_fp64_cache(const love_opts* opts) {
+    love_opts o{};
+    if (opts) o = *opts;
+    o.cache_fp64 = LOVE_CACHE_FP64_ON;
+    return o;
+}
+
+love_status love_build_cache(const love_grid* grid, const love_rbf* rbf, double sigma2, const double* X,
+                             const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                             const love_dist* dist, void* stream, love_cache** out) {
+    love_status st = build_grid_once(grid, rbf, sigma2, X, y, n_local, k, opts, dist, stream, out);
+    if (st == kRebuildFp64) {
+        const love_opts o = with_fp64_cache(opts);
+        st = build_grid_once(grid, rbf, sigma2, X, y, n_local, k, &o, dist, stream, out);
+    }
+    return st;
+}
+
+love_status love_build_cache_additive(const love_axis* axes, int32_t d, double sigma2, const double* X,
+                                      const double* y, int64_t n_local, int32_t k, const love_opts* opts,
+                                      const love_dist* dist, void* stream, love_cache** out) {
+    love_status st = build_additive_once(axes, d, sigma2, X, y, n_local, k, opts, dist, stream, out);
+    if (st == kRebuildFp64) {
+        const love_opts o = with_fp64_cache(opts);
+        st = build_additive_once(axes, d, sigma2, X, y, n_local, k, &o, dist, stream, out);
+    }
+    return st;
 }
 
 void love_free(love_cache* cache) { release(reinterpret_cast<Cache*>(cache)); }
@@ -539,7 +629,8 @@ love_status love_cache_info(const love_cache* cache, love_info* info) {
         info->n_reorth_steps = c->n_reorth_steps;
         info->k_pad = c->k_pad;
         info->k_sample_eff = c->k_sample_eff;
-        info->precision = c->precision;
+        info->precision = c->out_precision;
+        info->cache_precision = c->precision;
         info->n_local = c->n;
         info->n_global = c->n_global;
         info->m_total = c->g.m_total;
@@ -550,7 +641,8 @@ love_status love_cache_info(const love_cache* cache, love_info* info) {
         info->n_negative_var = (int64_t)cnt[0];
         info->n_out_of_range = (int64_t)cnt[1];
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -561,13 +653,23 @@ love_status love_predict_var(const love_cache* cache, const double* Xs, int64_t 
         if (!cache || (t > 0 && (!Xs || !var_out)) || t < 0) throw LoveError{LOVE_ERR_ARG, "bad arguments"};
         const Cache* c = reinterpret_cast<const Cache*>(cache);
         cudaStream_t s = (cudaStream_t)stream;
-        if (c->precision == LOVE_FP64)
+        if (c->precision == LOVE_FP64 && c->out_precision == LOVE_FP32) {
+            // fp64 cache, fp32 outputs (opts.cache_fp64): fp64 results rounded once
+            TempPool tmp(s);
+            double* v64 = (double*)tmp.get(sizeof(double) * t);
+            double* m64 = mean_out ? (double*)tmp.get(sizeof(double) * t) : nullptr;
+            launch_predict<double>(*c, Xs, nullptr, t, v64, m64, s);
+            launch_convert<double, float>(v64, (float*)var_out, t, s);
+            if (mean_out) launch_convert<double, float>(m64, (float*)mean_out, t, s);
+        } else if (c->precision == LOVE_FP64) {
             launch_predict<double>(*c, Xs, nullptr, t, (double*)var_out, (double*)mean_out, s);
-        else
+        } else {
             launch_predict<float>(*c, Xs, nullptr, t, (float*)var_out, (float*)mean_out, s);
+        }
         cuda_check(cudaGetLastError(), "predict_var launch");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -578,13 +680,28 @@ love_status love_predict_covar(const love_cache* cache, const double* Xa, const 
         if (!cache || (t > 0 && (!Xa || !Xb || !cov_out)) || t < 0) throw LoveError{LOVE_ERR_ARG, "bad arguments"};
         const Cache* c = reinterpret_cast<const Cache*>(cache);
         cudaStream_t s = (cudaStream_t)stream;
-        if (c->precision == LOVE_FP64)
+        if (c->precision == LOVE_FP64 && c->out_precision == LOVE_FP64) {
             launch_predict<double>(*c, Xa, Xb, t, (double*)cov_out, nullptr, s);
-        else
-            launch_predict<float>(*c, Xa, Xb, t, (float*)cov_out, nullptr, s);
+        } else if (t > 0) {
+            // fp32 outputs: the pair products (Rc^T w_a) . (Rc^T w_b) ~ prior cancel against the
+            // prior, so they are formed from fp64 rows (an fp64 cache, or the fp64 row copy of
+            // an fp32 cache's Rc) and the fp64 covariance is rounded once
+            Cache w = *c;
+            w.allocs.clear();
+            if (c->precision == LOVE_FP32) {
+                w.Rc = rc_rows64(*c, s);
+                w.precision = LOVE_FP64;
+                w.vsize = 8;
+            }
+            TempPool tmp(s);
+            double* c64 = (double*)tmp.get(sizeof(double) * t);
+            launch_predict<double>(w, Xa, Xb, t, c64, nullptr, s);
+            launch_convert<double, float>(c64, (float*)cov_out, t, s);
+        }
         cuda_check(cudaGetLastError(), "predict_covar launch");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -598,11 +715,12 @@ love_status love_sample(const love_cache* cache, const double* Xs, int64_t t, in
         if (c->k_sample_eff <= 0 || c->S == nullptr)
             throw LoveError{LOVE_ERR_STATE, "cache was built without a sampling root (k_sample = 0)"};
         cudaStream_t s = (cudaStream_t)stream;
-        if (c->precision == LOVE_FP64) launch_sample<double>(*c, Xs, t, ns, seed, zeta, (double*)out, s);
+        if (c->out_precision == LOVE_FP64) launch_sample<double>(*c, Xs, t, ns, seed, zeta, (double*)out, s);
         else launch_sample<float>(*c, Xs, t, ns, seed, zeta, (float*)out, s);
         cuda_check(cudaGetLastError(), "sample launch");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -644,7 +762,8 @@ love_status love_ski_mvm(const love_cache* cache, const void* v, void* out, void
         }
         cuda_check(cudaGetLastError(), "ski_mvm launch");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -673,7 +792,8 @@ love_status love_kuu_mvm(const love_cache* cache, const void* u, void* out, void
         }
         cuda_check(cudaGetLastError(), "kuu_mvm launch");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }
@@ -698,7 +818,8 @@ love_status love_cache_export(const love_cache* cache, int32_t what, void* dst, 
         if (!src || nb == 0) return LOVE_OK;
         cuda_check(cudaMemcpyAsync(dst, src, nb, cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "export copy");
         return LOVE_OK;
-    } catch (const LoveError& e) {
+    } catch (...) {
+        const LoveError e = current_error();
         return fail(e);
     }
 }

@@ -106,7 +106,8 @@ struct Cache {
     GridDev g;
     love_rbf rbf;
     double sigma2 = 0;
-    int precision = LOVE_FP32;
+    int precision = LOVE_FP32;          // of the cache's factors (LOVE_FP64 with opts.cache_fp64)
+    int out_precision = LOVE_FP32;      // of the query / sample outputs (love_opts.precision)
     int probe = LOVE_PROBE_Y, prior = LOVE_PRIOR_SKI, reorth_passes = 1;
     double tol = 0;
     int k_req = 0, k_sample_req = 0;
@@ -178,6 +179,8 @@ struct Cache {
     double* U64 = nullptr;               // [3][m] u~_{j-1}, u~_j, u~_{j+1} (rolling, fp64)
     float* U32 = nullptr;                // [k+1][m] every u~_i in fp32 (reorth correction)
     void* Rc = nullptr;                  // V[m * k_pad] row-major
+    void* Rc64 = nullptr;                // fp32 caches: double[m * k_pad] row-major, made by the first
+                                         // love_predict_covar (covariances from fp64 rows)
     void* a = nullptr;                   // double[m] mean cache
     void* vblk = nullptr;                // d <= 2: double[m][4^d(4^d+1)/2] per-cell variance blocks
     bool var_blocks_off = false;
@@ -207,6 +210,9 @@ struct LoveError {
     love_status status;
     std::string msg;
 };
+// internal status (never returned through the ABI): the fp32 build broke down before k under
+// LOVE_CACHE_FP64_AUTO and must be rebuilt with an fp64 cache (love_api.cu)
+constexpr love_status kRebuildFp64 = (love_status)100;
 void cuda_check(cudaError_t e, const char* what);
 // raises a kernel's dynamic shared-memory limit once (cudaFuncSetAttribute is a host call)
 void ensure_smem(const void* fn, size_t bytes);
@@ -264,6 +270,7 @@ void launch_init_q0(const LanczosState& st, cudaStream_t s);
 void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu
 void setup_fused(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
+void launch_rc_rows64(const Cache& c, double* out, cudaStream_t s);   // fp64 row-major Rc (m x k_pad)
 void avgcol_probe(Cache& c, cudaStream_t s);    // Q~[:, 0] = (1/m) W^T K_UU 1   (probe avg)
 void mean_cache_eq4(Cache& c, cudaStream_t s);  // a = Rc L^{-1} Q^T y after the Lanczos loop
 // query.cu

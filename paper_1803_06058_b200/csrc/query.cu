@@ -618,6 +618,26 @@ __global__ void nan_fill_kernel(const int* __restrict__ qstart, int m, const int
     }
 }
 
+// opt-in shared memory per block of the current device, and the static shared memory of the
+// sorted d = 3 kernel (both host queries, cached)
+size_t optin_smem() {
+    int dev = 0, v = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "smem optin");
+    return (size_t)v;
+}
+
+template <typename V>
+size_t sorted3_static_smem() {
+    static size_t bytes = 0;
+    if (bytes == 0) {
+        cudaFuncAttributes a{};
+        cuda_check(cudaFuncGetAttributes(&a, (const void*)predict_sorted3_kernel<V>), "func attributes");
+        bytes = a.sharedSizeBytes + 1;
+    }
+    return bytes - 1;
+}
+
 void build_var_blocks(Cache& c, cudaStream_t s) {
     if (c.additive || c.g.d > 2 || c.var_blocks_off || c.k_eff < 1) return;
     ProfScope ps(LOVE_PROF_FINISH, s);
@@ -653,28 +673,37 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
                         c.prior, (const double*)c.vblk, (const double*)c.a, Xa, t, out, mean_out, c.counters);
         return;
     }
-    if (Xb == nullptr && c.g.d == 3 && t >= 65536 && std::getenv("LOVE_NO_SORTED_QUERIES") == nullptr) {
+    // d = 3 cell-sorted path: the 64 stencil rows of a cell (64 k_pad values) must fit in one
+    // CTA's shared memory next to the kernel's static arrays; larger k takes the per-query path
+    const size_t sm3 = sizeof(V) * 64 * (size_t)c.k_pad;
+    if (Xb == nullptr && c.g.d == 3 && t >= 65536 && std::getenv("LOVE_NO_SORTED_QUERIES") == nullptr &&
+        sm3 + sorted3_static_smem<V>() <= optin_smem()) {
         const int m = c.g.m_total;
-        int *key = nullptr, *perm = nullptr, *qstart = nullptr;
-        cuda_check(cudaMallocAsync((void**)&key, sizeof(int) * t, s), "query sort alloc");
-        cuda_check(cudaMallocAsync((void**)&perm, sizeof(int) * t, s), "query sort alloc");
-        cuda_check(cudaMallocAsync((void**)&qstart, sizeof(int) * (m + 2), s), "query sort alloc");
+        struct Tmp {                                    // freed on every exit (stream-ordered)
+            cudaStream_t s;
+            int *key = nullptr, *perm = nullptr, *qstart = nullptr;
+            ~Tmp() {
+                if (key) cudaFreeAsync(key, s);
+                if (perm) cudaFreeAsync(perm, s);
+                if (qstart) cudaFreeAsync(qstart, s);
+            }
+        } tm{s};
+        cuda_check(cudaMallocAsync((void**)&tm.key, sizeof(int) * t, s), "query sort alloc");
+        cuda_check(cudaMallocAsync((void**)&tm.perm, sizeof(int) * t, s), "query sort alloc");
+        cuda_check(cudaMallocAsync((void**)&tm.qstart, sizeof(int) * (m + 2), s), "query sort alloc");
         LOVE_LAUNCH(query_cell3_kernel, (int)std::min<int64_t>(ceil_div(t, 256), 148 * 16), 256, 0, s, c.g, Xa, t,
-                    key);
-        counting_sort_keys(key, t, m + 1, qstart, perm, s);
+                    tm.key);
+        counting_sort_keys(tm.key, t, m + 1, tm.qstart, tm.perm, s);
         C4 c4{};
         for (int d = 0; d < 3; ++d)
             for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
         const int cpc = 8;
-        const size_t sm = sizeof(V) * 64 * (size_t)c.k_pad;
-        ensure_smem((const void*)predict_sorted3_kernel<V>, sm);
-        LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm, s, c.g, c4, c.rbf.outputscale,
+        ensure_smem((const void*)predict_sorted3_kernel<V>, sm3);
+        LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm3, s, c.g, c4, c.rbf.outputscale,
                     c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                    c.k_pad, (const double*)c.a, Xa, qstart, perm, cpc, out, mean_out, c.counters, kLanePerQuery);
-        LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, qstart, m, perm, out, mean_out, c.counters);
-        cuda_check(cudaFreeAsync(key, s), "query sort free");
-        cuda_check(cudaFreeAsync(perm, s), "query sort free");
-        cuda_check(cudaFreeAsync(qstart, s), "query sort free");
+                    c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
+                    kLanePerQuery);
+        LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, tm.qstart, m, tm.perm, out, mean_out, c.counters);
         return;
     }
     constexpr int G = 8;

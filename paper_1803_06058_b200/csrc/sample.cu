@@ -777,6 +777,19 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     cuda_check(cudaStreamSynchronize(s), "sampling sync");
 }
 
+template <typename VS>
+void launch_sample_gather(const Cache& c, const double* Xs, int64_t t, float* G, float* mu, int gb, cudaStream_t s) {
+    const int ks = c.k_sample_eff, kp = c.ks_pad;
+    switch (c.g.d) {
+        case 1: LOVE_LAUNCH((sample_gather_kernel<VS, 1>), gb, 256, 0, s, c.g, (const VS*)c.S, kp, ks,
+                            (const double*)c.a, Xs, t, G, mu, c.counters); break;
+        case 2: LOVE_LAUNCH((sample_gather_kernel<VS, 2>), gb, 256, 0, s, c.g, (const VS*)c.S, kp, ks,
+                            (const double*)c.a, Xs, t, G, mu, c.counters); break;
+        default: LOVE_LAUNCH((sample_gather_kernel<VS, 3>), gb, 256, 0, s, c.g, (const VS*)c.S, kp, ks,
+                             (const double*)c.a, Xs, t, G, mu, c.counters); break;
+    }
+}
+
 template <typename V>
 void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns, uint64_t seed, const double* zeta,
                    V* out, cudaStream_t s) {
@@ -788,14 +801,9 @@ void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns, uint
     cuda_check(cudaMallocAsync((void**)&mu, sizeof(float) * t, s), "sample alloc");
     cuda_check(cudaMallocAsync((void**)&Z, sizeof(float) * ns * kp, s), "sample alloc");
     const int gb = (int)ceil_div(t * 32, 256);
-    switch (c.g.d) {
-        case 1: LOVE_LAUNCH((sample_gather_kernel<V, 1>), gb, 256, 0, s, c.g, (const V*)c.S, kp, ks, (const double*)c.a,
-                            Xs, t, G, mu, c.counters); break;
-        case 2: LOVE_LAUNCH((sample_gather_kernel<V, 2>), gb, 256, 0, s, c.g, (const V*)c.S, kp, ks, (const double*)c.a,
-                            Xs, t, G, mu, c.counters); break;
-        default: LOVE_LAUNCH((sample_gather_kernel<V, 3>), gb, 256, 0, s, c.g, (const V*)c.S, kp, ks, (const double*)c.a,
-                             Xs, t, G, mu, c.counters); break;
-    }
+    // S is stored in the cache precision (double for LOVE_FP64 and opts.cache_fp64 caches)
+    if (c.precision == LOVE_FP64) launch_sample_gather<double>(c, Xs, t, G, mu, gb, s);
+    else launch_sample_gather<float>(c, Xs, t, G, mu, gb, s);
     if (zeta) {
         LOVE_LAUNCH(zeta_convert_kernel, (int)std::min<int64_t>(ceil_div(ns * kp, 256), 4096), 256, 0, s, zeta, ks, kp,
                     ns, Z);
@@ -805,7 +813,9 @@ void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns, uint
                     ns, Z);
     }
     const dim3 grid((unsigned)ceil_div(t, kSgT), (unsigned)ceil_div(ns, kSgS));
+    prof_begin(LOVE_PROF_SAMPLE_GEMM, s);
     LOVE_LAUNCH(sample_gemm2_kernel<V>, grid, 256, 0, s, G, Z, mu, kp, t, ns, out);
+    prof_end(LOVE_PROF_SAMPLE_GEMM, s);
     cuda_check(cudaFreeAsync(G, s), "sample free");
     cuda_check(cudaFreeAsync(mu, s), "sample free");
     cuda_check(cudaFreeAsync(Z, s), "sample free");

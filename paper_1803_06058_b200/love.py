@@ -51,6 +51,17 @@ def _ptr(t: Optional[torch.Tensor]):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 
+def _cache_fp64_mode(v) -> int:
+    # love_opts.cache_fp64: "auto" (fp64 rebuild after an fp32 breakdown), True / "on", False / "off"
+    if v is None or v == "auto":
+        return _abi.LOVE_CACHE_FP64_AUTO
+    if v is True or v == "on":
+        return _abi.LOVE_CACHE_FP64_ON
+    if v is False or v == "off":
+        return _abi.LOVE_CACHE_FP64_OFF
+    raise ValueError(f"cache_fp64: {v!r}")
+
+
 def nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib().love_nccl_unique_id(buf))
@@ -64,12 +75,16 @@ def launch_count() -> int:
 class LoveCache:
     """A built LOVE cache (Algorithm 1 pre-computation) on the current device."""
 
-    def __init__(self, handle: int, precision: int, d: int, m_total: int):
+    def __init__(self, handle: int, precision: int, d: int, m_total: int, cache_precision: Optional[int] = None):
         self._h = ctypes.c_void_p(handle)
         self.precision = precision
+        self.cache_precision = precision if cache_precision is None else cache_precision
         self.d = d
         self.m_total = m_total
+        # outputs of predict_var / predict_covar / sample
         self.vdtype = torch.float64 if precision == _abi.LOVE_FP64 else torch.float32
+        # the cache's factors (Rc, S exports) and the operator vectors (ski_mvm, kuu_mvm)
+        self.cdtype = torch.float64 if self.cache_precision == _abi.LOVE_FP64 else torch.float32
 
     # ------------------------------------------------------------------ build
     @classmethod
@@ -77,7 +92,7 @@ class LoveCache:
               lengthscale: Sequence[float], outputscale: float, sigma2: float, k: int,
               precision: str = "fp32", prior: str = "ski", k_sample: int = 0, probe: str = "y",
               reorth_passes: int = 0, breakdown_tol: float = 0.0, lanczos_mode: str = "auto",
-              var_blocks: str = "auto", reorth_tol: float = 0.0,
+              var_blocks: str = "auto", reorth_tol: float = 0.0, cache_fp64="auto",
               rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
               stream=None) -> "LoveCache":
         d = len(m)
@@ -101,6 +116,7 @@ class LoveCache:
         o.lanczos_mode = {"auto": 0, "two_pass": 1, "one_read": 2, "partial": 3}[lanczos_mode]
         o.reorth_tol = float(reorth_tol)
         o.var_blocks = {"auto": 0, "off": 1}[var_blocks]
+        o.cache_fp64 = _cache_fp64_mode(cache_fp64)
         dist = None
         idbuf = None
         if world > 1 or nccl_id is not None:
@@ -111,13 +127,13 @@ class LoveCache:
                                        int(Xd.shape[0]), int(k), ctypes.byref(o),
                                        ctypes.byref(dist) if dist is not None else None,
                                        ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
-        return cls(out.value, o.precision, d, int(np.prod(m)))
+        return cls._made(out.value, o.precision, d, int(np.prod(m)))
 
     @classmethod
     def build_additive(cls, X, y, m: Sequence[int], lo: Sequence[float], h: Sequence[float],
                        lengthscale: Sequence[float], outputscale, sigma2: float, k: int,
                        precision: str = "fp32", prior: str = "ski", probe: str = "y",
-                       reorth_passes: int = 0, breakdown_tol: float = 0.0,
+                       reorth_passes: int = 0, breakdown_tol: float = 0.0, cache_fp64="auto",
                        rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                        stream=None) -> "LoveCache":
         """Additive composition of len(m) 1-D RBF components (Eq. 16, P:406-441);
@@ -136,6 +152,7 @@ class LoveCache:
         o.prior = _abi.LOVE_PRIOR_EXACT if prior == "exact" else _abi.LOVE_PRIOR_SKI
         o.reorth_passes = int(reorth_passes)
         o.breakdown_tol = float(breakdown_tol)
+        o.cache_fp64 = _cache_fp64_mode(cache_fp64)
         dist = None
         idbuf = None
         if world > 1 or nccl_id is not None:
@@ -146,7 +163,16 @@ class LoveCache:
                                                 int(k), ctypes.byref(o),
                                                 ctypes.byref(dist) if dist is not None else None,
                                                 ctypes.c_void_p(_stream(stream)), ctypes.byref(out)))
-        return cls(out.value, o.precision, d, int(sum(m)))
+        return cls._made(out.value, o.precision, d, int(sum(m)))
+
+    @classmethod
+    def _made(cls, handle: int, precision: int, d: int, m_total: int) -> "LoveCache":
+        c = cls(handle, precision, d, m_total)
+        inf = _abi.love_info()
+        _check(_lib().love_cache_info(c._h, ctypes.byref(inf)))
+        c.cache_precision = inf.cache_precision
+        c.cdtype = torch.float64 if inf.cache_precision == _abi.LOVE_FP64 else torch.float32
+        return c
 
     # ------------------------------------------------------------------ queries
     def predict_var(self, Xs, return_mean: bool = False, stream=None):
@@ -179,13 +205,13 @@ class LoveCache:
 
     # ------------------------------------------------------------------ operators
     def ski_mvm(self, v, stream=None):
-        vd = _dev(v, self.vdtype)
+        vd = _dev(v, self.cdtype)
         out = torch.empty_like(vd)
         _check(_lib().love_ski_mvm(self._h, _ptr(vd), _ptr(out), ctypes.c_void_p(_stream(stream))))
         return out
 
     def kuu_mvm(self, u, stream=None):
-        ud = _dev(u, self.vdtype)
+        ud = _dev(u, self.cdtype)
         out = torch.empty_like(ud)
         _check(_lib().love_kuu_mvm(self._h, _ptr(ud), _ptr(out), ctypes.c_void_p(_stream(stream))))
         return out
@@ -201,14 +227,14 @@ class LoveCache:
             alpha=np.array([inf.alpha[i] for i in range(k)]),
             beta=np.array([inf.beta[i] for i in range(max(k - 1, 0))]),
             n_negative_var=inf.n_negative_var, n_out_of_range=inf.n_out_of_range,
-            n_reorth_steps=inf.n_reorth_steps)
+            n_reorth_steps=inf.n_reorth_steps, precision=inf.precision, cache_precision=inf.cache_precision)
 
     def export(self, what: str, stream=None) -> torch.Tensor:
         code = {"rc": _abi.LOVE_EXPORT_RC, "mean": _abi.LOVE_EXPORT_MEAN, "S": _abi.LOVE_EXPORT_S,
                 "perm": _abi.LOVE_EXPORT_PERM}[what]
         nb = ctypes.c_int64()
         _check(_lib().love_cache_export(self._h, code, None, 0, ctypes.byref(nb), None))
-        dtype = {"rc": self.vdtype, "S": self.vdtype, "mean": torch.float64, "perm": torch.int32}[what]
+        dtype = {"rc": self.cdtype, "S": self.cdtype, "mean": torch.float64, "perm": torch.int32}[what]
         esize = torch.empty(0, dtype=dtype).element_size()
         out = torch.empty(nb.value // esize, dtype=dtype, device="cuda")
         _check(_lib().love_cache_export(self._h, code, _ptr(out), nb.value, None,

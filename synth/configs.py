@@ -30,6 +30,9 @@ class Problem:
     s: int = 0                   # samples drawn (config 5)
     seed: int = 0
     kind: str = "product"        # "product" (Kronecker grid) | "additive" (Eq. 16)
+    # fp32 outputs from an fp64-built cache (love_opts.cache_fp64, reading A12b): config 5 is
+    # converged (var << prior) and an fp32 Lanczos breaks down before the fp64 oracle does
+    cache_fp64: bool = False
 
     @property
     def h(self) -> Tuple[float, ...]:
@@ -55,7 +58,7 @@ CONFIGS = {
     4: Problem("cfg4_3d_kron", 3, 2_000_000, (64, 64, 64), (-3.3, -3.3, -3.3), (3.3, 3.3, 3.3),
                (0.5, 0.5, 0.5), 1.0, 0.1 ** 2, 100, 4_000_000, "fp32", "rsinr3d", 0.1),
     5: Problem("cfg5_sampling", 1, 100_000, (10_000,), (-0.05,), (1.05,), (0.05,), 1.0, 0.01,
-               100, 10_000, "fp32", "sin6pi", 0.1, k_sample=100, s=1000),
+               100, 10_000, "fp32", "sin6pi", 0.1, k_sample=100, s=1000, cache_fp64=True),
     # SURVEY 8(f) NEXT #2 (not a BASELINE config): additive composition of 10 1-D RBF kernels
     # with m = 100 inducing points each, the paper's Styblinski-Tang model;
     # x ~ U(-5, 5)^10, grid [-5.5, 5.5] per axis (reading A5), y a scaled Styblinski-Tang
@@ -72,9 +75,10 @@ def get_config(i: int) -> Problem:
 def scaled_config(i: int, n: Optional[int] = None, m: Optional[Tuple[int, ...]] = None,
                   k: Optional[int] = None, t: Optional[int] = None,
                   precision: Optional[str] = None, k_sample: Optional[int] = None,
-                  s: Optional[int] = None) -> Problem:
+                  s: Optional[int] = None, cache_fp64: bool = False) -> Problem:
     """A smaller problem with the same data distribution, kernel and grid bounds as config i
-    (used for parity at sizes the oracle finishes in seconds)."""
+    (used for parity at sizes the oracle finishes in seconds).  cache_fp64 is not inherited:
+    a scaled problem runs the precision path it names."""
     p = CONFIGS[i]
     return dataclasses.replace(
         p,
@@ -86,4 +90,5 @@ def scaled_config(i: int, n: Optional[int] = None, m: Optional[Tuple[int, ...]] 
         precision=p.precision if precision is None else precision,
         k_sample=p.k_sample if k_sample is None else k_sample,
         s=p.s if s is None else s,
+        cache_fp64=cache_fp64,
     )

@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_no_gpu_calls_are_safe():
     _abi, lib = _lib()
-    assert lib.love_abi_version() == 3
+    assert lib.love_abi_version() == 4
     assert lib.love_launch_count() >= 0
     # argument validation happens before any device work
     out = ctypes.c_void_p()

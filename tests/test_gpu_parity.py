@@ -58,6 +58,9 @@ def _rel2(a, b):
     # shortened circulant embedding (reading A25b: N >= m + b, c_b < 1e-30 c_0): cfg2's grid at
     # N = 2^17 instead of 2^18, cfg5's at 2^14 instead of 2^15, m = 2200 on the one-CTA 4096 path
     ("cfg2m_fp64", 2, None, "fp64"), ("cfg5m_fp64", 5, None, "fp64"), ("1d_2200_fp64", 1, (2200,), "fp64"),
+    # N = 2^18 and 2^19: the real-input half-length passes (rfft_passA/B/C, N >= 2^18)
+    ("1d_200000", 2, (200_000,), "fp32"), ("1d_200000_fp64", 2, (200_000,), "fp64"),
+    ("1d_300007_fp64", 2, (300_007,), "fp64"),
 ])
 def test_kuu_mvm(case):
     name, ci, m, prec = case
@@ -121,6 +124,61 @@ def test_cfg1_fp64_end_to_end():
     _assert_var(var.cpu().numpy(), ov, _prior(model, inp.Xs), fp64=True)
     om = O.predict_mean(model, oc, inp.Xs)
     np.testing.assert_allclose(mean.cpu().numpy(), om, atol=1e-9 * np.abs(om).max())
+    # covariances of pairs (both priors): fp64 bound relative to sqrt(var_a var_b)
+    Xb = inp.Xs[np.random.default_rng(2).permutation(p.t)]
+    for prior in ("ski",):
+        cov = c.predict_covar(inp.Xs, Xb).cpu().numpy()
+        ocov = O.predict_covar(model, oc, inp.Xs, Xb, prior=prior)
+        scale = np.sqrt(ov * O.predict_var(model, oc, Xb))
+        _assert_cov(cov, ocov, scale, np.sqrt(_prior(model, inp.Xs) * _prior(model, Xb)), fp64=True)
+
+
+def _assert_cov(got, want, scale, prior_scale, fp64):
+    """Covariances: the A21 variance bound with |v_or| replaced by the covariance's own scale
+    sqrt(var_a var_b) (>= |cov|) and P(x*) by sqrt(P_a P_b):
+    fp64 1e-9 sqrt(v_a v_b) + 1e-13 sqrt(P_a P_b), fp32 1e-3 sqrt(v_a v_b) + 1e-6 sqrt(P_a P_b)."""
+    a, b = (1e-9, 1e-13) if fp64 else (1e-3, 1e-6)
+    r = np.abs(got - want) / (a * scale + b * prior_scale)
+    assert r.max() <= 1.0, (r.max(), np.argmax(r))
+
+
+@pytest.mark.parametrize("kind,prec", [("cfg1", "fp64"), ("cfg1", "fp32"), ("2d", "fp64"), ("3d", "fp64"),
+                                       ("3d", "fp32")])
+def test_prior_exact_covariances_distinct_points(kind, prec):
+    """EXACT-prior mode (Eq. 10 with k(x*_i, x*_j), reading A8) on pairs of DISTINCT
+    test points, product grids in 1-3-D, against the oracle's predict_covar(prior="exact") (its
+    prior_exact is pinned to scikit-learn's RBF kernel in test_oracle_pins)."""
+    if kind == "cfg1":
+        # k = 30: config 1 converges (var << prior) and its fp32 Lanczos would stop before the
+        # fp64 oracle's breakdown step (reading A12b)
+        p = scaled_config(1, k=30, precision=prec)
+        inp = make_inputs(p)
+    else:
+        import dataclasses as dc
+        pt, inp = tiny_problem(kind)
+        p = dc.replace(pt, k=60, precision=prec)
+    c = _build(p, inp, prior="exact")
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    assert c.info()["k_eff"] == oc.lanczos.k_eff
+    rng = np.random.default_rng(9)
+    a, b = rng.integers(0, p.t, 3000), rng.integers(0, p.t, 3000)
+    a, b = a[a != b], b[a != b]
+    cov = c.predict_covar(inp.Xs[a], inp.Xs[b]).cpu().numpy().astype(np.float64)
+    ocov = O.predict_covar(model, oc, inp.Xs[a], inp.Xs[b], prior="exact")
+    va = O.predict_var(model, oc, inp.Xs[a], prior="exact")
+    vb = O.predict_var(model, oc, inp.Xs[b], prior="exact")
+    # EXACT-mode variances can be slightly negative where the SKI kernel's interpolation error
+    # exceeds the variance (reading A8): the covariance scale uses |var|
+    scale = np.sqrt(np.abs(va) * np.abs(vb))
+    _assert_cov(cov, ocov, scale, np.full(len(a), p.outputscale), fp64=prec == "fp64")
+    # the exact prior really is used: the result differs from the SKI-prior covariance by
+    # k(x_a, x_b) - w_a^T K_UU w_b
+    ia, wa = O.interp(inp.Xs[a], p.m, p.lo, p.h)
+    ib, wb = O.interp(inp.Xs[b], p.m, p.lo, p.h)
+    diff = O.prior_exact(model, inp.Xs[a], inp.Xs[b]) - O.prior_ski(model, ia, wa, ib, wb)
+    cs = _build(p, inp).predict_covar(inp.Xs[a], inp.Xs[b]).cpu().numpy().astype(np.float64)
+    np.testing.assert_allclose(cov - cs, diff, atol=(1e-12 if prec == "fp64" else 1e-6) * p.outputscale)
 
 
 @pytest.mark.parametrize("prec", ["fp64"])
@@ -187,9 +245,9 @@ def test_scaled_fp32_variances_and_covariances(ci, n, m, k, t, mode):
     cov = c.predict_covar(inp.Xs, Xb).cpu().numpy().astype(np.float64)
     ocov = O.predict_covar(model, oc, inp.Xs, Xb)
     scale = np.sqrt(prior * _prior(model, Xb))
-    # covariances of distant pairs are ~0: the absolute floor is fp32 round-off of O(prior)
-    # terms (4^d stencil rows x k products), 1e-5 of the prior scale
-    ratio = np.abs(cov - ocov) / (1e-3 * np.abs(ocov) + 1e-5 * scale)
+    # fp32 caches form the pair products from fp64 rows of Rc, so the variance
+    # bound's floor holds for covariances too: 1e-3 |cov| + 1e-6 sqrt(P_a P_b)
+    ratio = np.abs(cov - ocov) / (1e-3 * np.abs(ocov) + 1e-6 * scale)
     assert ratio.max() <= 1.0, ratio.max()
     # symmetry cov(a,b) == cov(b,a)
     cov2 = c.predict_covar(Xb, inp.Xs).cpu().numpy().astype(np.float64)

@@ -8,6 +8,7 @@ mistake (dropped term, wrong sign/index, transposed operand) fails at least one 
 import json
 import math
 import os
+import types
 
 import numpy as np
 import pytest
@@ -329,6 +330,78 @@ def test_prior_ski_closed_form():
     K = O.kuu_dense(model.cols, model.outputscale)
     np.testing.assert_allclose(O.prior_ski(model, ia, wa, ia, wa),
                                np.einsum("it,ij,jt->t", Ws, K, Ws), rtol=1e-13)
+
+
+def test_prior_exact_vs_library_rbf_and_closed_values():
+    """prior_exact (Eq. 10's k(x*_i, x*_j)) at DISTINCT points, pinned three ways
+    that share nothing with its own formula:
+      * scikit-learn's RBF kernel (exp(-0.5 ||(x - x')/l||^2), anisotropic l) times a
+        ConstantKernel(s^2), on random 1-D, 2-D and 3-D pairs;
+      * hand values: |x - x'| = l sqrt(2 ln 2) gives s^2 / 2 exactly per dimension (1/8 for three
+        such offsets), |x - x'| = l gives s^2 e^{-1/2}; l != 1 so an l-vs-l^2 slip fails;
+      * on grid nodes the SKI interpolation is exact, so prior_exact == prior_ski there (the
+        latter pinned by K_UU's closed-form entries above)."""
+    from sklearn.gaussian_process.kernels import RBF, ConstantKernel
+    rng = np.random.default_rng(21)
+    for d, ls, s2 in [(1, (0.05,), 1.0), (2, (0.1, 0.3), 2.5), (3, (0.5, 0.7, 1.3), 0.7)]:
+        model = types.SimpleNamespace(kind="product", lengthscale=tuple(ls), outputscale=s2)
+        Xi = rng.uniform(-1, 1, (200, d))
+        Xj = Xi + rng.normal(0, 1, (200, d)) * np.array(ls)          # distinct, O(l) apart
+        ref = (ConstantKernel(s2) * RBF(length_scale=np.array(ls)))
+        want = np.array([ref(Xi[r:r + 1], Xj[r:r + 1])[0, 0] for r in range(200)])
+        np.testing.assert_allclose(O.prior_exact(model, Xi, Xj), want, rtol=1e-13)
+        half = np.array(ls) * math.sqrt(2.0 * math.log(2.0))
+        got = O.prior_exact(model, np.zeros((1, d)), half[None, :])[0]
+        assert abs(got - s2 * 0.5 ** d) < 1e-14 * s2
+        one = np.zeros((1, d))
+        one[0, 0] = ls[0]
+        assert abs(O.prior_exact(model, np.zeros((1, d)), one)[0] - s2 * math.exp(-0.5)) < 1e-14 * s2
+    # on grid nodes: exact prior == SKI prior, for distinct node pairs
+    p, inp = tiny_problem("2d")
+    model = _model(p, inp)
+    ni = rng.integers(2, 13, (50, 2))
+    nj = rng.integers(2, 13, (50, 2))
+    lo, h = np.array(p.lo), np.array(p.h)
+    Xi, Xj = lo + ni * h, lo + nj * h
+    ia, wa = O.interp(Xi, p.m, p.lo, p.h)
+    ib, wb = O.interp(Xj, p.m, p.lo, p.h)
+    np.testing.assert_allclose(O.prior_exact(model, Xi, Xj), O.prior_ski(model, ia, wa, ib, wb),
+                               rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("kind", ["1d_n200", "2d", "3d"])
+def test_predict_covar_offdiagonal_equals_dense_gp(kind):
+    """Off-diagonal covariances (Eq. 10) at full Krylov dimension equal the dense
+    SKI-GP covariance of Eq. 2, K** - K*X K_hat^{-1} KX*, formed here from the densified W, the
+    dense K_UU and a Cholesky solve (no Lanczos), on 400 random pairs of distinct test points;
+    the EXACT-prior mode differs from it by exactly k(x_a, x_b) - w_a^T K_UU w_b."""
+    p, inp = tiny_problem(kind)
+    model = _model(p, inp)
+    cache = O.love_precompute(model, p.k)
+    assert cache.lanczos.k_eff < p.k
+    rng = np.random.default_rng(4)
+    a, b = rng.integers(0, p.t, 400), rng.integers(0, p.t, 400)
+    keep = a != b
+    a, b = a[keep], b[keep]
+    Xa, Xb = inp.Xs[a], inp.Xs[b]
+    W = O.dense_W(model.idx, model.w, p.m_total)
+    Kuu = O.kuu_dense(model.cols, model.outputscale)
+    Khat = W.T @ Kuu @ W + p.sigma2 * np.eye(p.n)
+    L = np.linalg.cholesky(Khat)
+    ia, wa = O.interp(Xa, p.m, p.lo, p.h)
+    ib, wb = O.interp(Xb, p.m, p.lo, p.h)
+    Wa, Wb = O.dense_W(ia, wa, p.m_total), O.dense_W(ib, wb, p.m_total)
+    Ka, Kb = np.linalg.solve(L, W.T @ Kuu @ Wa), np.linalg.solve(L, W.T @ Kuu @ Wb)
+    dense = np.einsum("it,ij,jt->t", Wa, Kuu, Wb) - (Ka * Kb).sum(0)
+    got = O.predict_covar(model, cache, Xa, Xb)
+    scale = np.sqrt(np.abs(O.predict_var(model, cache, Xa) * O.predict_var(model, cache, Xb)))
+    assert np.max(np.abs(got - dense) / scale) < 1e-8
+    assert np.max(np.abs(O.predict_covar(model, cache, Xb, Xa) - got) / scale) < 1e-10     # symmetry
+    ex = O.predict_covar(model, cache, Xa, Xb, prior="exact")
+    from sklearn.gaussian_process.kernels import RBF, ConstantKernel
+    kab = (ConstantKernel(p.outputscale) * RBF(length_scale=np.array(p.lengthscale)))
+    kx = np.array([kab(Xa[r:r + 1], Xb[r:r + 1])[0, 0] for r in range(len(a))])
+    np.testing.assert_allclose(ex - got, kx - np.einsum("it,ij,jt->t", Wa, Kuu, Wb), rtol=1e-9, atol=1e-12)
 
 
 # ---------------------------------------------------------------- sampling (P:308-362)
