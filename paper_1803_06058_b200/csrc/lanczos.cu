@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <memory>
 
 #include "love_internal.h"
 
@@ -24,7 +25,7 @@
 #ifndef LOVE_UPD_B
 #define LOVE_UPD_B 8
 #endif
-namespace love { constexpr int kUpdB = LOVE_UPD_B; constexpr int kCondSteps = 2; }
+namespace love { constexpr int kUpdB = LOVE_UPD_B; constexpr int kCondSteps = 2; int update_grid(int64_t nchunks); }
 
 namespace love {
 
@@ -332,6 +333,10 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
         if (fin) {
             st.alpha_cur[0] = 0.0;
             st.beta2_cur[0] = 0.0;
+        }
+        if (st.hdone != nullptr && st.flags[0]) {    // tell the host to stop replaying
+            *(volatile int*)st.hdone = 1;
+            __threadfence_system();
         }
         st.step_ctr[0] = 0;
         st.jdev[0] = j + 1;
@@ -658,7 +663,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
                      pl.mean_y};
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
-    pl.gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(c.ldq / VecT<V>::W, 256), 148 * 8));
+    pl.gu = update_grid(c.ldq / VecT<V>::W);
     pl.smu = sizeof(double) * (pl.k + 1);
     ensure_smem((const void*)reorth_dots_sweep_kernel<V, 1>, sizeof(double) * 8 * (pl.k + 1));
     ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
@@ -678,6 +683,14 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     }
     // the step graph is also captured on several GPUs: its all-reduces have fixed addresses
     const bool graph = !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
+    // one GPU: early stop of the replays at breakdown (the device sets a mapped host flag; on
+    // several GPUs every rank must issue the same collectives, so they replay to k)
+    std::unique_ptr<ReplayThrottle> thr;
+    if (graph && c.comm == nullptr && pl.fold) {
+        thr.reset(new ReplayThrottle(c.device));
+        c.st.hdone = thr->d;
+        pl.rs.st = c.st;
+    }
     // every kernel of a step starts with pdl_wait(): its launch can overlap the previous
     // kernel's drain (programmatic dependent launch)
     PdlScope pdl(std::getenv("LOVE_NO_PDL") == nullptr);
@@ -739,16 +752,25 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
         const int64_t nodes = g_launch_count.load() - before;
         g_launch_count -= nodes;
-        for (int j = 0; j + 1 < pl.k; j += 2) {
+        // replays past a breakdown would only run early-exiting kernels: the host stops as soon
+        // as the mapped done flag is set, keeping a window of replays in flight (no stream sync)
+        bool stop = false;
+        for (int j = 0, i = 0; j + 1 < pl.k; j += 2, ++i) {
+            if (thr != nullptr && !thr->admit(i)) {
+                stop = true;
+                break;
+            }
             cuda_check(cudaGraphLaunch(ge, s), "graph launch");
             g_launch_count += nodes;
+            if (thr != nullptr) thr->launched(i, s);
         }
-        if (pl.k & 1) enqueue_step<V>(pl, pl.k - 1, s);
+        if ((pl.k & 1) && !stop) enqueue_step<V>(pl, pl.k - 1, s);
         cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
         cuda_check(cudaGraphDestroy(g), "graph destroy");
     } else {
         for (int j = 0; j < pl.k; ++j) enqueue_step<V>(pl, j, s);
     }
+    c.st.hdone = nullptr;
     if (pl.fold) {   // the last streamed column (its scalars were finalised by the last update)
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(stream_rc_kernel, pl.gm, 256, 0, s, pl.rs);
@@ -840,7 +862,7 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
     ensure_smem((const void*)reorth_dots_sweep_kernel<double, 1>, smd);
     LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), dots_grid(ldq, 2, k), 256, smd, s, (const double*)Q, ldq,
                 k, pass, r, st, (const int*)nullptr);
-    const int gu = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(ldq / 2, 256), 148 * 8));
+    const int gu = update_grid(ldq / 2);
     const size_t smu = sizeof(double) * (k + 1);
     ensure_smem((const void*)reorth_update_kernel<double>, smu);
     LOVE_LAUNCH(reorth_update_kernel<double>, gu, 256, smu, s, Q, ldq, n, k, pass,
@@ -848,6 +870,48 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
 }
 
 void launch_init_q0(const LanczosState& st, cudaStream_t s) { LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st); }
+
+// CTAs of the reorthogonalisation update for nchunks 16-byte chunks (one per thread)
+int update_grid(int64_t nchunks) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nchunks, 256), 148 * 8));
+}
+
+// ---- ReplayThrottle (love_internal.h).  Per (thread, device): one mapped host int and a ring
+// of kReplayWindow events, created once.
+constexpr int kReplayWindow = 3;
+ReplayThrottle::ReplayThrottle(int device) {
+    struct Slot {
+        int* h = nullptr;
+        int* d = nullptr;
+        cudaEvent_t ev[kReplayWindow] = {};
+    };
+    thread_local Slot slots[64];
+    if (device < 0 || device >= 64) throw LoveError{LOVE_ERR_CUDA, "device index out of range"};
+    Slot& sl = slots[device];
+    if (sl.h == nullptr) {
+        cuda_check(cudaHostAlloc((void**)&sl.h, 64, cudaHostAllocMapped), "cudaHostAlloc(done flag)");
+        cuda_check(cudaHostGetDevicePointer((void**)&sl.d, sl.h, 0), "cudaHostGetDevicePointer");
+        for (int i = 0; i < kReplayWindow; ++i)
+            cuda_check(cudaEventCreateWithFlags(&sl.ev[i], cudaEventDisableTiming), "event create");
+    }
+    *(volatile int*)sl.h = 0;
+    h = sl.h;
+    d = sl.d;
+    ev = sl.ev;
+}
+
+bool ReplayThrottle::admit(int i) {
+    if (stopped()) return false;
+    if (i >= kReplayWindow) {
+        cuda_check(cudaEventSynchronize(ev[i % kReplayWindow]), "replay window");
+        if (stopped()) return false;
+    }
+    return true;
+}
+
+void ReplayThrottle::launched(int i, cudaStream_t s) {
+    cuda_check(cudaEventRecord(ev[i % kReplayWindow], s), "replay event");
+}
 
 void run_lanczos(Cache& c, cudaStream_t s) {
     if (c.precision == LOVE_FP64) lanczos_impl<double>(c, s);

@@ -67,6 +67,8 @@ struct LanczosState {
     int* flags;            // [4]        done, k_eff, notpd, zero_probe
     int* jdev;             // [1]        current step index j
     int* step_ctr;         // [1]        CTAs done in the step's last kernel (advance_step)
+    int* hdone = nullptr;  // mapped host memory: set to 1 with flags[0] (done), so the host stops
+                           // replaying the step graph without a stream synchronisation
     int chol = 1;          // finalise the Cholesky row of T too (0: sampling Lanczos on M, reading A15)
     // device-terminated step loop (a CUDA graph WHILE node, one GPU): the step's last CTA
     // clears the loop condition once the Lanczos is done or the step index reaches cond_limit;
@@ -264,6 +266,19 @@ void setup_kuu(Cache& c, cudaStream_t s);
 void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
+// Host side of the early stop of step-graph replays (ReplayThrottle in lanczos.cu): a mapped
+// host flag the device sets at breakdown, and at most kReplayWindow replays in flight beyond the
+// last one the host has seen complete.
+struct ReplayThrottle {
+    volatile int* h = nullptr;     // host view of the done flag
+    int* d = nullptr;              // device view (LanczosState::hdone)
+    cudaEvent_t* ev = nullptr;
+    explicit ReplayThrottle(int device);
+    bool stopped() const { return *h != 0; }
+    // before replay i: wait until replay i - kReplayWindow has completed; false once done
+    bool admit(int i);
+    void launched(int i, cudaStream_t s);
+};
 void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int64_t n, int k, int pass,
                             int last_pass, const double* r, double tol, cudaStream_t s);
 void launch_init_q0(const LanczosState& st, cudaStream_t s);

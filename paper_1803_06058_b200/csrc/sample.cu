@@ -31,6 +31,7 @@ constexpr int kDotRows = 128;       // rows per CTA tile of dots_kernel (~m/128 
 __global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ A, int64_t lda, int nrow, int ncol,
                                                    const double* __restrict__ x, double* __restrict__ out,
                                                    const int* __restrict__ stop) {
+    pdl_wait();
     if (stop && *stop) return;
     __shared__ double xs[kDotRows];
     const int r0 = blockIdx.x * kDotRows;
@@ -410,6 +411,7 @@ __global__ void __launch_bounds__(256) root_kernel(const double* __restrict__ Qp
 // q_j into the fixed MVM input buffer (the K_UU kernels read a fixed pointer); zero t
 __global__ void samp_qcur_kernel(LanczosState st, const double* __restrict__ Q, int64_t ld, int m,
                                  double* __restrict__ qcur, double* __restrict__ t, int kt) {
+    pdl_wait();
     if (st.flags[0]) return;
     const int j = *st.jdev;
     const double sc = st.qscale[j];
@@ -426,6 +428,7 @@ __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ 
                                                      LanczosState st) {
     extern __shared__ double ts[];               // [k_eff]
     __shared__ double red[32];
+    pdl_wait();
     if (st.flags[0]) return;
     for (int i = threadIdx.x; i < k_eff; i += blockDim.x) ts[i] = t[i];
     __syncthreads();
@@ -711,28 +714,35 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 1, 1, v, tol, s);
     };
     const bool graph = !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr && ks >= 4;
+    ReplayThrottle thr(c.device);
+    if (graph) st.hdone = thr.d;
     if (graph) {
         cudaGraph_t gph = nullptr;
         cudaGraphExec_t ge = nullptr;
         const int64_t before = g_launch_count.load();
-        cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "sampling capture");
-        step();
-        step();
-        cuda_check(cudaStreamEndCapture(s, &gph), "sampling capture end");
+        {   // every step kernel starts with pdl_wait(): programmatic dependent launch
+            PdlScope pdl(std::getenv("LOVE_NO_PDL") == nullptr);
+            cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "sampling capture");
+            step();
+            step();
+            cuda_check(cudaStreamEndCapture(s, &gph), "sampling capture end");
+        }
         cuda_check(cudaGraphInstantiate(&ge, gph, 0), "sampling graph instantiate");
         const int64_t nodes = g_launch_count.load() - before;
         g_launch_count -= nodes;
-        int hflag = 0;                              // stop replaying after breakdown (polled)
-        for (int j = 0; j + 1 < ks; j += 2) {
-            if (j > 0 && (j % 16) == 0) {
-                cuda_check(cudaMemcpyAsync(&hflag, st.flags, sizeof(int), cudaMemcpyDeviceToHost, s), "flag poll");
-                cuda_check(cudaStreamSynchronize(s), "flag poll");
-                if (hflag) break;
+        // stop replaying after breakdown: the device sets the mapped host flag (ReplayThrottle),
+        // a window of replays stays in flight, the stream is never drained to poll
+        bool stop = false;
+        for (int j = 0, i = 0; j + 1 < ks; j += 2, ++i) {
+            if (!thr.admit(i)) {
+                stop = true;
+                break;
             }
             cuda_check(cudaGraphLaunch(ge, s), "sampling graph launch");
             g_launch_count += nodes;
+            thr.launched(i, s);
         }
-        if (ks & 1) step();
+        if ((ks & 1) && !stop) step();
         cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
         cuda_check(cudaGraphDestroy(gph), "graph destroy");
     } else {

@@ -112,3 +112,43 @@ def sharded_lanczos(rank: int, world: int, port: int, kind: str, passes: int) ->
                                    rtol=1e-8, atol=1e-10)
     finally:
         dist.destroy_process_group()
+
+
+def liblove_host_plumbing(rank: int, world: int, port: int) -> None:
+    """liblove's own host side of the N > 1 path, over gloo: rank 0 makes the NCCL unique id
+    with love_nccl_unique_id (liblove.so dlopens NCCL; no GPU needed) and the caller's process
+    group broadcasts it (dist.nccl_id_for_group's default); bench.py's strong-scaling shards of
+    one global draw tile the training and test sets exactly, its weak-scaling shards are
+    distinct draws, and both arms' `config` records agree."""
+    import bench
+    from paper_1803_06058_b200 import dist as D
+    from synth import get_config, make_inputs
+    _init(rank, world, port)
+    try:
+        ident = D.nccl_id_for_group()                       # love_nccl_unique_id on rank 0
+        allid = [None] * world
+        dist.all_gather_object(allid, ident)
+        assert len(ident) == 128 and all(x == ident for x in allid) and any(ident)
+        p = dataclass_replace(get_config(4), n=10_007, t=5_003)
+        g = make_inputs(p)
+        sh = bench.shard_inputs(p, rank, world, "strong")
+        parts = [None] * world
+        dist.all_gather_object(parts, (sh.X, sh.y, sh.Xs))
+        np.testing.assert_array_equal(np.concatenate([q[0] for q in parts]), g.X)
+        np.testing.assert_array_equal(np.concatenate([q[1] for q in parts]), g.y)
+        np.testing.assert_array_equal(np.concatenate([q[2] for q in parts]), g.Xs)
+        w = bench.shard_inputs(p, rank, world, "weak")
+        assert len(w.X) == p.n and len(w.Xs) == p.t
+        allw = [None] * world
+        dist.all_gather_object(allw, w.y[:8])
+        assert not np.allclose(allw[0], allw[1])             # independent shards per rank
+        assert bench.config_record(p, world, "strong")["n"] == p.n
+        assert bench.config_record(p, world, "weak")["n"] == world * p.n
+        assert D.sum_over_ranks(float(len(sh.Xs))) == p.t
+    finally:
+        dist.destroy_process_group()
+
+
+def dataclass_replace(p, **kw):
+    import dataclasses
+    return dataclasses.replace(p, **kw)

@@ -22,3 +22,7 @@ def test_host_plumbing_world2():
 @pytest.mark.parametrize("kind,passes", [("cfg1", 2), ("1d_n200", 1), ("2d", 2), ("3d", 2)])
 def test_sharded_lanczos_matches_oracle_world2(kind, passes):
     mp.spawn(W.sharded_lanczos, args=(2, _port(), kind, passes), nprocs=2, join=True)
+
+
+def test_liblove_host_plumbing_world2():
+    mp.spawn(W.liblove_host_plumbing, args=(2, _port()), nprocs=2, join=True)

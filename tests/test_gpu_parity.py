@@ -461,3 +461,27 @@ def test_device_terminated_step_loop(monkeypatch, G):
     oc = O.love_precompute(model, p.k)
     assert oc.lanczos.k_eff == i1["k_eff"]
     _assert_var(v1, O.predict_var(model, oc, inp.Xs), prior, fp64=True)
+
+
+def test_sorted_queries_d3_large_k_falls_back(monkeypatch):
+    """d = 3, t >= 65536 and a cache whose 64 stencil rows do not fit one CTA's shared memory
+    (64 k_pad 8 B > 227 KB once k_pad > 443 in fp64): love_predict_var takes the per-query path
+    instead of failing, and matches the oracle (query.cu smem cap)."""
+    import dataclasses as dc
+    p = dc.replace(scaled_config(4, n=6_007, m=(14, 14, 14), k=1024, t=70_001, precision="fp64"),
+                   lo=(-4.5,) * 3, hi=(4.5,) * 3, lengthscale=(0.3, 0.3, 0.3))
+    inp = make_inputs(p)
+    c = _build(p, inp)
+    k_eff = c.info()["k_eff"]
+    assert k_eff > 443, k_eff
+    v, mu = c.predict_var(inp.Xs, return_mean=True)
+    monkeypatch.setenv("LOVE_NO_SORTED_QUERIES", "1")
+    vu, muu = c.predict_var(inp.Xs, return_mean=True)
+    np.testing.assert_array_equal(v.cpu().numpy(), vu.cpu().numpy())
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    # both run to breakdown; the step where beta_j crosses tau is set by round-off (+-3 steps
+    # of directions that carry nothing)
+    assert abs(oc.lanczos.k_eff - k_eff) <= 3
+    sel = np.arange(0, p.t, 37)
+    _assert_var(v.cpu().numpy()[sel], O.predict_var(model, oc, inp.Xs[sel]), _prior(model, inp.Xs[sel]), fp64=True)

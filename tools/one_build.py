@@ -37,6 +37,8 @@ def main():
         kw["lanczos_mode"] = a.lanczos_mode
     if p.k_sample:
         kw["k_sample"] = p.k_sample
+    if p.cache_fp64:
+        kw["cache_fp64"] = True
     for it in range(2):
         if it == 1:
             torch.cuda.synchronize()

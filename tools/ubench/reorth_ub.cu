@@ -1,0 +1,387 @@
+// Microbenchmark of the reorthogonalisation update's memory pattern (lanczos.cu
+// reorth_update_kernel): out = (r - a q_j - b q_{j-1}) - sum_{i<=j} c_i Q[:, i], beta^2 += ||out||^2,
+// n = 1e6 fp32 rows, column-major Q, j = J.  Variants of the launch shape / load pipelining,
+// each timed alone with CUDA events (best of 20) after an L2 flush, and after a forward read
+// of the columns (the dots pass's L2 state).  Prints one line per variant:
+//   variant  us_cold  GBps_cold  us_warm  GBps_warm   (algorithmic bytes (J+4) n 4)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench/reorth_ub tools/ubench/reorth_ub.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+#include <cuda_pipeline.h>
+
+constexpr int64_t N = 1000000;
+constexpr int KMAX = 128;
+
+__constant__ float c_coef[KMAX];
+
+__device__ double g_beta2;
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ void block_beta(double b2) {
+    __shared__ double red[32];
+    b2 = warp_sum(b2);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = b2;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) atomicAdd(&g_beta2, v);
+    }
+}
+
+// V0: the production structure: one float4 chunk per thread (grid-stride), columns last to
+// first in batches of B whose loads are issued before the first FMA, fp64 three-term source
+template <int B, int MINB>
+__global__ void __launch_bounds__(256, MINB) upd_batched(float* __restrict__ Q, int64_t ldq, int j,
+                                                        const float* __restrict__ r, double a, double b) {
+    const int ncols = j + 1;
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nch; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = q * 4;
+        const float4 rv = *reinterpret_cast<const float4*>(r + p);
+        const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+        const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+        double v[4] = {rv.x - a * qa.x - b * qb.x, rv.y - a * qa.y - b * qb.y, rv.z - a * qa.z - b * qb.z,
+                       rv.w - a * qa.w - b * qb.w};
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const float* col = Q + (int64_t)(ncols - 1) * ldq + p;
+        int i = ncols - 1;
+        for (; i >= B - 1; i -= B) {
+            float4 x[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) x[u] = *reinterpret_cast<const float4*>(col - (int64_t)u * ldq);
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const float ci = c_coef[i - u];
+                acc[0] += ci * x[u].x; acc[1] += ci * x[u].y; acc[2] += ci * x[u].z; acc[3] += ci * x[u].w;
+            }
+            col -= (int64_t)B * ldq;
+        }
+        for (; i >= 0; --i) {
+            const float4 x = *reinterpret_cast<const float4*>(col);
+            const float ci = c_coef[i];
+            acc[0] += ci * x.x; acc[1] += ci * x.y; acc[2] += ci * x.z; acc[3] += ci * x.w;
+            col -= ldq;
+        }
+        float4 o;
+        o.x = (float)(v[0] - acc[0]); o.y = (float)(v[1] - acc[1]); o.z = (float)(v[2] - acc[2]); o.w = (float)(v[3] - acc[3]);
+        b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+        *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+    }
+    block_beta(b2);
+}
+
+// V2: columns split across the two halves of the CTA: thread t < 128 sweeps the upper half of
+// the columns, t >= 128 the lower half, for the same 128 chunks; partial sums meet in smem.
+template <int B>
+__global__ void __launch_bounds__(256) upd_split2(float* __restrict__ Q, int64_t ldq, int j,
+                                                  const float* __restrict__ r, double a, double b) {
+    __shared__ float4 part[128];
+    const int ncols = j + 1;
+    const int half = threadIdx.x >> 7, t = threadIdx.x & 127;
+    const int mid = ncols / 2;
+    const int cbeg = half ? 0 : mid, cend = half ? mid : ncols;
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    for (int64_t q0 = (int64_t)blockIdx.x * 128; q0 < nch; q0 += (int64_t)gridDim.x * 128) {
+        const int64_t q = q0 + t;
+        const bool live = q < nch;
+        const int64_t p = q * 4;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (live) {
+            const float* col = Q + (int64_t)(cend - 1) * ldq + p;
+            int i = cend - 1;
+            for (; i >= cbeg + B - 1; i -= B) {
+                float4 x[B];
+#pragma unroll
+                for (int u = 0; u < B; ++u) x[u] = *reinterpret_cast<const float4*>(col - (int64_t)u * ldq);
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const float ci = c_coef[i - u];
+                    acc[0] += ci * x[u].x; acc[1] += ci * x[u].y; acc[2] += ci * x[u].z; acc[3] += ci * x[u].w;
+                }
+                col -= (int64_t)B * ldq;
+            }
+            for (; i >= cbeg; --i) {
+                const float4 x = *reinterpret_cast<const float4*>(col);
+                const float ci = c_coef[i];
+                acc[0] += ci * x.x; acc[1] += ci * x.y; acc[2] += ci * x.z; acc[3] += ci * x.w;
+                col -= ldq;
+            }
+        }
+        if (half == 1) part[t] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        __syncthreads();
+        if (half == 0 && live) {
+            const float4 o2 = part[t];
+            const float4 rv = *reinterpret_cast<const float4*>(r + p);
+            const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+            const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+            float4 o;
+            o.x = (float)(rv.x - a * qa.x - b * qb.x - (double)(acc[0] + o2.x));
+            o.y = (float)(rv.y - a * qa.y - b * qb.y - (double)(acc[1] + o2.y));
+            o.z = (float)(rv.z - a * qa.z - b * qb.z - (double)(acc[2] + o2.z));
+            o.w = (float)(rv.w - a * qa.w - b * qb.w - (double)(acc[3] + o2.w));
+            b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+            *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+        }
+        __syncthreads();
+    }
+    block_beta(b2);
+}
+
+// V3: cp.async pipeline: each thread streams its chunk's columns through a ring of S stages of
+// B columns in shared memory (16 B per column per thread), so the bytes in flight do not
+// occupy registers
+template <int B, int S>
+__global__ void __launch_bounds__(256) upd_cpasync(float* __restrict__ Q, int64_t ldq, int j,
+                                                   const float* __restrict__ r, double a, double b) {
+    extern __shared__ float4 ring[];                 // [S][B][256]
+    const int ncols = j + 1;
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    const int nst = (ncols + B - 1) / B;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nch; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = q * 4;
+        auto issue = [&](int st) {
+            if (st < nst) {
+                float4* dst = ring + (size_t)(st % S) * B * 256 + threadIdx.x;
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const int ci = ncols - 1 - (st * B + u);
+                    if (ci >= 0) __pipeline_memcpy_async(dst + u * 256, Q + (int64_t)ci * ldq + p, 16);
+                }
+            }
+            __pipeline_commit();
+        };
+#pragma unroll
+        for (int st = 0; st < S - 1; ++st) issue(st);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int st = 0; st < nst; ++st) {
+            issue(st + S - 1);
+            __pipeline_wait_prior(S - 1);
+            const float4* src = ring + (size_t)(st % S) * B * 256 + threadIdx.x;
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int ci = ncols - 1 - (st * B + u);
+                if (ci >= 0) {
+                    const float4 x = src[u * 256];
+                    const float c = c_coef[ci];
+                    acc[0] += c * x.x; acc[1] += c * x.y; acc[2] += c * x.z; acc[3] += c * x.w;
+                }
+            }
+        }
+        __pipeline_wait_prior(0);
+        const float4 rv = *reinterpret_cast<const float4*>(r + p);
+        const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+        const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+        float4 o;
+        o.x = (float)(rv.x - a * qa.x - b * qb.x - (double)acc[0]);
+        o.y = (float)(rv.y - a * qa.y - b * qb.y - (double)acc[1]);
+        o.z = (float)(rv.z - a * qa.z - b * qb.z - (double)acc[2]);
+        o.w = (float)(rv.w - a * qa.w - b * qb.w - (double)acc[3]);
+        b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+        *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+    }
+    block_beta(b2);
+}
+
+
+// V4: V0 with the column tail as one predicated batch (no dependent single loads) and the
+// three-term source loaded after the sweep
+template <int B>
+__global__ void __launch_bounds__(256) upd_pred(float* __restrict__ Q, int64_t ldq, int j,
+                                               const float* __restrict__ r, double a, double b) {
+    const int ncols = j + 1;
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nch; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = q * 4;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int i0 = ncols - 1; i0 >= 0; i0 -= B) {
+            float4 x[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u)
+                x[u] = i0 - u >= 0 ? *reinterpret_cast<const float4*>(Q + (int64_t)(i0 - u) * ldq + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const float ci = i0 - u >= 0 ? c_coef[i0 - u] : 0.f;
+                acc[0] += ci * x[u].x; acc[1] += ci * x[u].y; acc[2] += ci * x[u].z; acc[3] += ci * x[u].w;
+            }
+        }
+        const float4 rv = *reinterpret_cast<const float4*>(r + p);
+        const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+        const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+        float4 o;
+        o.x = (float)(rv.x - a * qa.x - b * qb.x - (double)acc[0]);
+        o.y = (float)(rv.y - a * qa.y - b * qb.y - (double)acc[1]);
+        o.z = (float)(rv.z - a * qa.z - b * qb.z - (double)acc[2]);
+        o.w = (float)(rv.w - a * qa.w - b * qb.w - (double)acc[3]);
+        b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+        *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+    }
+    block_beta(b2);
+}
+
+// V5: columns split G ways inside the CTA (256 / G threads per chunk group), predicated
+// batches, partial sums combined in shared memory by the first group
+template <int B, int G>
+__global__ void __launch_bounds__(256) upd_splitG(float* __restrict__ Q, int64_t ldq, int j,
+                                                 const float* __restrict__ r, double a, double b) {
+    constexpr int T = 256 / G;
+    __shared__ float4 part[G - 1][T];
+    const int ncols = j + 1;
+    const int g = threadIdx.x / T, t = threadIdx.x % T;
+    const int per = (ncols + G - 1) / G;
+    const int cbeg = min(ncols, g * per), cend = min(ncols, cbeg + per);
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    for (int64_t q0 = (int64_t)blockIdx.x * T; q0 < nch; q0 += (int64_t)gridDim.x * T) {
+        const int64_t q = q0 + t;
+        const bool live = q < nch;
+        const int64_t p = q * 4;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (live) {
+            for (int i0 = cend - 1; i0 >= cbeg; i0 -= B) {
+                float4 x[B];
+#pragma unroll
+                for (int u = 0; u < B; ++u)
+                    x[u] = i0 - u >= cbeg ? *reinterpret_cast<const float4*>(Q + (int64_t)(i0 - u) * ldq + p) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < B; ++u) {
+                    const float ci = i0 - u >= cbeg ? c_coef[i0 - u] : 0.f;
+                    acc[0] += ci * x[u].x; acc[1] += ci * x[u].y; acc[2] += ci * x[u].z; acc[3] += ci * x[u].w;
+                }
+            }
+        }
+        if (g > 0) part[g - 1][t] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        __syncthreads();
+        if (g == 0 && live) {
+#pragma unroll
+            for (int h = 0; h < G - 1; ++h) {
+                const float4 o2 = part[h][t];
+                acc[0] += o2.x; acc[1] += o2.y; acc[2] += o2.z; acc[3] += o2.w;
+            }
+            const float4 rv = *reinterpret_cast<const float4*>(r + p);
+            const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+            const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+            float4 o;
+            o.x = (float)(rv.x - a * qa.x - b * qb.x - (double)acc[0]);
+            o.y = (float)(rv.y - a * qa.y - b * qb.y - (double)acc[1]);
+            o.z = (float)(rv.z - a * qa.z - b * qb.z - (double)acc[2]);
+            o.w = (float)(rv.w - a * qa.w - b * qb.w - (double)acc[3]);
+            b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+            *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+        }
+        __syncthreads();
+    }
+    block_beta(b2);
+}
+
+// reference: the dots pass's pattern without the reduction (sum of all columns, forward)
+__global__ void __launch_bounds__(256) read_cols(const float* __restrict__ Q, int64_t ldq, int ncols, float* out) {
+    const int64_t nch = ldq / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nch; q += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int i = 0; i < ncols; i += 8) {
+            float4 x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = i + u < ncols ? *reinterpret_cast<const float4*>(Q + (int64_t)(i + u) * ldq + q * 4) : make_float4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += x[u].x + x[u].y + x[u].z + x[u].w;
+        }
+        if (s == 1234.5f) out[0] = s;
+    }
+}
+
+__global__ void flush_kernel(float* buf, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) buf[i] = 0.f;
+}
+
+struct Ctx {
+    float *Q, *r, *flush, *out;
+    int j;
+    cudaEvent_t e0, e1;
+};
+
+template <typename F>
+void timeit(const char* name, Ctx& c, F launch) {
+    const double bytes = (double)(c.j + 1 + 3) * N * 4 + N * 4;
+    float best[2] = {1e30f, 1e30f};
+    for (int mode = 0; mode < 2; ++mode) {
+        for (int rep = 0; rep < 20; ++rep) {
+            flush_kernel<<<148 * 8, 256>>>(c.flush, 64ll * 1024 * 1024);
+            if (mode == 1) read_cols<<<148 * 8, 256>>>(c.Q, N, c.j + 1, c.out);
+            cudaEventRecord(c.e0);
+            launch();
+            cudaEventRecord(c.e1);
+            cudaEventSynchronize(c.e1);
+            float ms;
+            cudaEventElapsedTime(&ms, c.e0, c.e1);
+            if (ms < best[mode]) best[mode] = ms;
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    printf("%-28s cold %7.2f us %6.0f GB/s   warm %7.2f us %6.0f GB/s %s\n", name, best[0] * 1e3,
+           bytes / (best[0] * 1e-3) / 1e9, best[1] * 1e3, bytes / (best[1] * 1e-3) / 1e9,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main(int argc, char** argv) {
+    const int J = argc > 1 ? atoi(argv[1]) : 49;
+    Ctx c;
+    c.j = J;
+    cudaMalloc(&c.Q, sizeof(float) * N * (J + 2));
+    cudaMalloc(&c.r, sizeof(float) * N);
+    cudaMalloc(&c.flush, sizeof(float) * 64ll * 1024 * 1024);
+    cudaMalloc(&c.out, 64);
+    cudaMemset(c.Q, 0, sizeof(float) * N * (J + 2));
+    cudaMemset(c.r, 0, sizeof(float) * N);
+    float h[KMAX];
+    for (int i = 0; i < KMAX; ++i) h[i] = 1e-3f * (i + 1);
+    cudaMemcpyToSymbol(c_coef, h, sizeof(h));
+    cudaEventCreate(&c.e0);
+    cudaEventCreate(&c.e1);
+    const int64_t nch = N / 4;
+    const int g977 = (int)((nch + 255) / 256);
+    printf("j = %d, n = %lld, algorithmic bytes %.1f MB\n", J, (long long)N, ((J + 4.0) * N * 4 + N * 4) / 1e6);
+    timeit("read_cols (dots pattern)", c, [&] { read_cols<<<g977, 256>>>(c.Q, N, J + 1, c.out); });
+    timeit("V0 batch8 grid977", c, [&] { upd_batched<8, 1><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V0 batch8 grid592", c, [&] { upd_batched<8, 1><<<592, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V0 batch4 minB8 grid977", c, [&] { upd_batched<4, 8><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V0 batch4 minB8 grid1184", c, [&] { upd_batched<4, 8><<<1184, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V0 batch16 grid977", c, [&] { upd_batched<16, 1><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V4 pred batch8 grid977", c, [&] { upd_pred<8><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V4 pred batch8 grid592", c, [&] { upd_pred<8><<<592, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V4 pred batch4 grid977", c, [&] { upd_pred<4><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V5 split2 pred B8", c, [&] { upd_splitG<8, 2><<<(int)((nch + 127) / 128), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V5 split2 pred B4", c, [&] { upd_splitG<4, 2><<<(int)((nch + 127) / 128), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V5 split4 pred B8", c, [&] { upd_splitG<8, 4><<<(int)((nch + 63) / 64), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V5 split4 pred B4", c, [&] { upd_splitG<4, 4><<<(int)((nch + 63) / 64), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V5 split2 pred B8 grid/2", c, [&] { upd_splitG<8, 2><<<(int)((nch + 255) / 256), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V2 split2 batch8", c, [&] { upd_split2<8><<<(int)((nch + 127) / 128), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V2 split2 batch4", c, [&] { upd_split2<4><<<(int)((nch + 127) / 128), 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    {
+        auto k = upd_cpasync<8, 3>;
+        const size_t sm = sizeof(float4) * 8 * 3 * 256;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        timeit("V3 cp.async B8 S3", c, [&] { k<<<g977, 256, sm>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    }
+    {
+        auto k = upd_cpasync<4, 4>;
+        const size_t sm = sizeof(float4) * 4 * 4 * 256;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        timeit("V3 cp.async B4 S4", c, [&] { k<<<g977, 256, sm>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    }
+    {
+        auto k = upd_cpasync<8, 2>;
+        const size_t sm = sizeof(float4) * 8 * 2 * 256;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        timeit("V3 cp.async B8 S2", c, [&] { k<<<g977, 256, sm>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    }
+    return 0;
+}
