@@ -298,6 +298,83 @@ __global__ void __launch_bounds__(256) var_blocks2_kernel(GridDev g, int k_eff, 
     }
 }
 
+// d = 2 blocks from node-pair products.  B_c[a][b] (a <= b, row-major over the 4x4 stencil
+// of cell c) only depends on the node pair (n_a, n_b) = (n_a, n_a + off) with off = (di, dj)
+// in the half neighbourhood H = {di = 0, 0 <= dj <= 3} u {1 <= di <= 3, |dj| <= 3} (25
+// offsets): B_c[a][b] = K_UU[n_a][n_b] - P[off][n_a], P[off][n] = sum_i Rc[n, i] Rc[n + off, i].
+// A node pair is shared by up to 16 cells, so the products are formed once per pair (25 m k
+// FMAs instead of 136 m k), tile by tile from shared memory; the assembly is a gather.
+constexpr int kPairOffs = 25;
+__host__ __device__ __forceinline__ void pair_off(int o, int& di, int& dj) {
+    if (o < 4) { di = 0; dj = o; }
+    else { di = 1 + (o - 4) / 7; dj = (o - 4) % 7 - 3; }
+}
+__host__ __device__ __forceinline__ int pair_index(int di, int dj) {   // inverse of pair_off
+    return di == 0 ? dj : 4 + (di - 1) * 7 + (dj + 3);
+}
+constexpr int kPTI = 8, kPTJ = 32, kPB = 8;   // node tile (rows x cols) and Rc columns per stage
+
+__global__ void __launch_bounds__(kPTI * kPTJ) pair_products2_kernel(GridDev g, int k_eff,
+                                                                      const double* __restrict__ Rc,
+                                                                      double* __restrict__ P) {
+    constexpr int HI = kPTI + 3, HJ = kPTJ + 6;         // halo: +3 rows, -3..+3 columns
+    __shared__ double tile[kPB][HI][HJ];
+    const int m = g.m_total, m0 = g.m[0], m1 = g.m[1];
+    const int ti = threadIdx.x / kPTJ, tj = threadIdx.x % kPTJ;
+    const int i0 = blockIdx.y * kPTI, j0 = blockIdx.x * kPTJ;
+    const int ni = i0 + ti, nj = j0 + tj;
+    double acc[kPairOffs];
+#pragma unroll
+    for (int o = 0; o < kPairOffs; ++o) acc[o] = 0.0;
+    for (int c0 = 0; c0 < k_eff; c0 += kPB) {
+        for (int e = threadIdx.x; e < kPB * HI * HJ; e += blockDim.x) {
+            const int b = e / (HI * HJ), r = (e / HJ) % HI, q = e % HJ;
+            const int gi = i0 + r, gj = j0 + q - 3, col = c0 + b;
+            tile[b][r][q] = (col < k_eff && gi < m0 && gj >= 0 && gj < m1) ? Rc[(int64_t)col * m + gi * m1 + gj] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int b = 0; b < kPB; ++b) {
+            const double x = tile[b][ti][tj + 3];
+#pragma unroll
+            for (int o = 0; o < kPairOffs; ++o) {
+                int di, dj;
+                pair_off(o, di, dj);
+                acc[o] += x * tile[b][ti + di][tj + 3 + dj];
+            }
+        }
+        __syncthreads();
+    }
+    if (ni < m0 && nj < m1) {
+#pragma unroll
+        for (int o = 0; o < kPairOffs; ++o) P[(int64_t)o * m + ni * m1 + nj] = acc[o];
+    }
+}
+
+// thread per block entry: B_c[p] = s^2 c0[|di|] c1[|dj|] - P[off][n_a] (0 for cells whose
+// stencil leaves the grid)
+__global__ void __launch_bounds__(256) assemble_blocks2_kernel(GridDev g, const double* __restrict__ P,
+                                                               const double* __restrict__ cols, double s2,
+                                                               double* __restrict__ blk) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int m = g.m_total;
+    if (e >= (int64_t)m * 136) return;
+    const int c = (int)(e / 136), p0 = (int)(e - (int64_t)c * 136);
+    const int ci = c / g.m[1], cj = c - ci * g.m[1];
+    const bool ok = ci >= 1 && ci <= g.m[0] - 3 && cj >= 1 && cj <= g.m[1] - 3;
+    if (!ok) {
+        blk[e] = 0.0;
+        return;
+    }
+    int p = p0, a = 0;
+    while (p >= 16 - a) { p -= 16 - a; ++a; }
+    const int b = a + p;
+    const int di = (b >> 2) - (a >> 2), dj = (b & 3) - (a & 3);
+    const int na = (ci - 1 + (a >> 2)) * g.m[1] + (cj - 1 + (a & 3));
+    const double kuu = s2 * cols[di] * cols[g.m[0] + (dj < 0 ? -dj : dj)];
+    blk[e] = kuu - P[(int64_t)pair_index(di, dj) * m + na];
+}
+
 // variance (and mean) of one query from its cell block (fp64)
 template <typename V, int D>
 __device__ __forceinline__ void block_query(const GridDev& g, const C4& c4, double s2, int prior_mode,
@@ -646,9 +723,18 @@ void build_var_blocks(Cache& c, cudaStream_t s) {
     if (c.g.d == 1)
         LOVE_LAUNCH(var_blocks1_kernel, (int)ceil_div(m, 256), 256, 0, s, m, c.k_eff, (const double*)c.Rc_col,
                     (const double*)c.cols64, c.rbf.outputscale, (double*)c.vblk);
-    else
+    else if (std::getenv("LOVE_VAR_BLOCKS2_WARP") != nullptr)   // the warp-per-cell kernel (cross-check)
         LOVE_LAUNCH(var_blocks2_kernel, (int)ceil_div((int64_t)m * 32, 256), 256, 0, s, c.g, c.k_eff,
                     (const double*)c.Rc_col, (const double*)c.cols64, c.rbf.outputscale, (double*)c.vblk);
+    else {
+        double* P = nullptr;
+        cuda_check(cudaMallocAsync((void**)&P, sizeof(double) * kPairOffs * (size_t)m, s), "pair products");
+        const dim3 grid((unsigned)ceil_div(c.g.m[1], kPTJ), (unsigned)ceil_div(c.g.m[0], kPTI));
+        LOVE_LAUNCH(pair_products2_kernel, grid, kPTI * kPTJ, 0, s, c.g, c.k_eff, (const double*)c.Rc_col, P);
+        LOVE_LAUNCH(assemble_blocks2_kernel, (int)ceil_div((int64_t)m * 136, 256), 256, 0, s, c.g, (const double*)P,
+                    (const double*)c.cols64, c.rbf.outputscale, (double*)c.vblk);
+        cuda_check(cudaFreeAsync(P, s), "pair products free");
+    }
 }
 
 template <typename V>

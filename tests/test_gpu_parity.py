@@ -485,3 +485,21 @@ def test_sorted_queries_d3_large_k_falls_back(monkeypatch):
     assert abs(oc.lanczos.k_eff - k_eff) <= 3
     sel = np.arange(0, p.t, 37)
     _assert_var(v.cpu().numpy()[sel], O.predict_var(model, oc, inp.Xs[sel]), _prior(model, inp.Xs[sel]), fp64=True)
+
+
+def test_var_blocks2_pair_products_equal_warp_kernel(monkeypatch):
+    """d = 2 variance blocks from node-pair products (query.cu pair_products2 + assembly) equal
+    the warp-per-cell kernel's (LOVE_VAR_BLOCKS2_WARP=1): the same fp64 sums over the Rc
+    columns, regrouped by node pair; both priors, with cells on the grid edge."""
+    p = scaled_config(3, n=30_007, m=(48, 40), k=40, t=4001)
+    inp = make_inputs(p)
+    for prior in ("ski", "exact"):
+        c = _build(p, inp, prior=prior)
+        v = c.predict_var(inp.Xs).cpu().numpy().astype(np.float64)
+        monkeypatch.setenv("LOVE_VAR_BLOCKS2_WARP", "1")
+        cw = _build(p, inp, prior=prior)
+        monkeypatch.delenv("LOVE_VAR_BLOCKS2_WARP")
+        vw = cw.predict_var(inp.Xs).cpu().numpy().astype(np.float64)
+        # the two builds differ only by fp64 atomic order in the Lanczos; the block algebra is
+        # exact: fp32 outputs agree to round-off
+        np.testing.assert_allclose(v, vw, rtol=2e-6, atol=1e-9)

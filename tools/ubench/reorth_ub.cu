@@ -282,6 +282,66 @@ __global__ void __launch_bounds__(256) upd_splitG(float* __restrict__ Q, int64_t
     block_beta(b2);
 }
 
+
+__device__ unsigned g_ctr;
+__device__ int g_step;
+// V6: V0 with switches: BETA = 0 drops the beta^2 block reduction + atomic, ADV = 1 adds the
+// production last-CTA-done step advance (__threadfence + same-address atomic per CTA)
+template <int BETA, int ADV>
+__global__ void __launch_bounds__(256) upd_sw(float* __restrict__ Q, int64_t ldq, int j,
+                                             const float* __restrict__ r, double a, double b) {
+    constexpr int B = 8;
+    const int ncols = j + 1;
+    double b2 = 0.0;
+    const int64_t nch = ldq / 4;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nch; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = q * 4;
+        const float4 rv = *reinterpret_cast<const float4*>(r + p);
+        const float4 qa = *reinterpret_cast<const float4*>(Q + (int64_t)j * ldq + p);
+        const float4 qb = *reinterpret_cast<const float4*>(Q + (int64_t)(j - 1) * ldq + p);
+        double v[4] = {rv.x - a * qa.x - b * qb.x, rv.y - a * qa.y - b * qb.y, rv.z - a * qa.z - b * qb.z,
+                       rv.w - a * qa.w - b * qb.w};
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        const float* col = Q + (int64_t)(ncols - 1) * ldq + p;
+        int i = ncols - 1;
+        for (; i >= B - 1; i -= B) {
+            float4 x[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) x[u] = *reinterpret_cast<const float4*>(col - (int64_t)u * ldq);
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const float ci = c_coef[i - u];
+                acc[0] += ci * x[u].x; acc[1] += ci * x[u].y; acc[2] += ci * x[u].z; acc[3] += ci * x[u].w;
+            }
+            col -= (int64_t)B * ldq;
+        }
+        for (; i >= 0; --i) {
+            const float4 x = *reinterpret_cast<const float4*>(col);
+            const float ci = c_coef[i];
+            acc[0] += ci * x.x; acc[1] += ci * x.y; acc[2] += ci * x.z; acc[3] += ci * x.w;
+            col -= ldq;
+        }
+        float4 o;
+        o.x = (float)(v[0] - acc[0]); o.y = (float)(v[1] - acc[1]); o.z = (float)(v[2] - acc[2]); o.w = (float)(v[3] - acc[3]);
+        b2 += (double)o.x * o.x + (double)o.y * o.y + (double)o.z * o.z + (double)o.w * o.w;
+        *reinterpret_cast<float4*>(Q + (int64_t)(j + 1) * ldq + p) = o;
+    }
+    if (BETA) block_beta(b2);
+    else if (b2 == 1234.5) g_beta2 = b2;
+    if (ADV) {
+        __shared__ int last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const unsigned prev = atomicAdd(&g_ctr, 1u);
+            last = prev == gridDim.x - 1;
+            if (last) __threadfence();
+        }
+        __syncthreads();
+        if (last && threadIdx.x == 0) { g_ctr = 0; g_step += 1; __threadfence(); }
+    }
+}
+
 // reference: the dots pass's pattern without the reduction (sum of all columns, forward)
 __global__ void __launch_bounds__(256) read_cols(const float* __restrict__ Q, int64_t ldq, int ncols, float* out) {
     const int64_t nch = ldq / 4;
@@ -355,6 +415,10 @@ int main(int argc, char** argv) {
     timeit("V0 batch4 minB8 grid977", c, [&] { upd_batched<4, 8><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
     timeit("V0 batch4 minB8 grid1184", c, [&] { upd_batched<4, 8><<<1184, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
     timeit("V0 batch16 grid977", c, [&] { upd_batched<16, 1><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V6 beta0 adv0", c, [&] { upd_sw<0, 0><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V6 beta1 adv0", c, [&] { upd_sw<1, 0><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V6 beta1 adv1", c, [&] { upd_sw<1, 1><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
+    timeit("V6 beta0 adv0 nostore", c, [&] { upd_sw<0, 0><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
     timeit("V4 pred batch8 grid977", c, [&] { upd_pred<8><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
     timeit("V4 pred batch8 grid592", c, [&] { upd_pred<8><<<592, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
     timeit("V4 pred batch4 grid977", c, [&] { upd_pred<4><<<g977, 256>>>(c.Q, N, J, c.r, 0.5, 0.25); });
