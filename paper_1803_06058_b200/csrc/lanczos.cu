@@ -254,11 +254,102 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     }
 }
 
+// ---- one-sync step (several GPUs, fp32, probe X9): ONE pass over Q~_j gives
+// the three dot vectors c_r = Q_j^T r, g1 = Q_j^T q_j and g2 = Q_j^T q_{j-1} (normalised
+// columns) into c_cur[0 .. 3(k+1)), so a single all-reduce replaces those of alpha and of the
+// reorthogonalisation dots: alpha_j = c_r[j] and Q_j^T r' = c_r - alpha_j g1 - beta_{j-1} g2
+// for the three-term residual r' (reorth_update_kernel, kUpd1Sync).  Same sweep as the kernel
+// above (8-column blocks, butterfly reduce-scatter per source, fp64 across lanes); it also
+// runs at j = k-1, where only alpha is needed.
+template <typename V>
+__global__ void __launch_bounds__(256) reorth_dots3_kernel(const V* __restrict__ Q, int64_t ldq, int k,
+                                                           const V* __restrict__ r, LanczosState st) {
+    pdl_wait();
+    constexpr int W = VecT<V>::W;
+    extern __shared__ __align__(16) double smd[];
+    const int j = *st.jdev;
+    if (st.flags[0] || j >= k) return;
+    const int ncols = j + 1;
+    const int cpg = (int)round_up(ceil_div(ncols, gridDim.y), 8);
+    const int cbeg = blockIdx.y * cpg, cend = min(ncols, cbeg + cpg);
+    if (cbeg >= cend) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t K1 = k + 1;
+    double* csum = smd;                                   // [3][nw][ncols]
+    const int64_t nvec = ldq / W;
+    const int64_t qv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    V src[3][W];
+    {
+        V a[W], b[W], c[W];
+#pragma unroll
+        for (int e = 0; e < W; ++e) a[e] = b[e] = c[e] = V(0);
+        if (qv < nvec) {
+            vload<V>(r + qv * W, a);
+            vload<V>(Q + (int64_t)j * ldq + qv * W, b);
+            if (j > 0) vload<V>(Q + (int64_t)(j - 1) * ldq + qv * W, c);
+        }
+#pragma unroll
+        for (int e = 0; e < W; ++e) { src[0][e] = a[e]; src[1][e] = b[e]; src[2][e] = c[e]; }
+    }
+    const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        V pv[3][8];
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+            const int cidx = c0 + cc;
+#pragma unroll
+            for (int sidx = 0; sidx < 3; ++sidx) pv[sidx][cc] = V(0);
+            if (cidx < cend && qv < nvec) {
+                V a[W];
+                vload<V>(Q + (int64_t)cidx * ldq + qv * W, a);
+#pragma unroll
+                for (int sidx = 0; sidx < 3; ++sidx)
+#pragma unroll
+                    for (int e = 0; e < W; ++e) pv[sidx][cc] += a[e] * src[sidx][e];
+            }
+        }
+#pragma unroll
+        for (int sidx = 0; sidx < 3; ++sidx) {
+            double h4[4], h2[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double keep = (double)(b2 ? pv[sidx][i + 4] : pv[sidx][i]);
+                const double send = (double)(b2 ? pv[sidx][i] : pv[sidx][i + 4]);
+                h4[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const double keep = b1 ? h4[i + 2] : h4[i], send = b1 ? h4[i] : h4[i + 2];
+                h2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+            }
+            double h1;
+            {
+                const double keep = b0 ? h2[1] : h2[0], send = b0 ? h2[0] : h2[1];
+                h1 = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+            }
+            h1 += __shfl_xor_sync(0xffffffffu, h1, 8);
+            h1 += __shfl_xor_sync(0xffffffffu, h1, 16);
+            const int col = c0 + (b2 << 2 | b1 << 1 | b0);
+            if (lane < 8 && col < cend) csum[((int64_t)sidx * nw + wid) * ncols + col] = h1;
+        }
+    }
+    __syncthreads();
+    const double sj = st.qscale[j], sj1 = j > 0 ? st.qscale[j - 1] : 0.0;
+    const int nc = cend - cbeg;
+    for (int e = threadIdx.x; e < 3 * nc; e += blockDim.x) {
+        const int sidx = e / nc, i = cbeg + (e - sidx * nc);
+        double tot = 0.0;
+        for (int w = 0; w < nw; ++w) tot += csum[((int64_t)sidx * nw + w) * ncols + i];
+        const double sc = st.qscale[i] * (sidx == 0 ? 1.0 : sidx == 1 ? sj : sj1);
+        atomicAdd(&st.c_cur[sidx * K1 + i], tot * sc);
+    }
+}
+
 // the current step's accumulators back to zero (one thread)
 __device__ __forceinline__ void clear_step_acc(const LanczosState& st, int k) {
     st.alpha_cur[0] = 0.0;
     st.beta2_cur[0] = 0.0;
-    for (int64_t i = 0; i < 2 * st.crep * c_stride(st, k); ++i) st.c_cur[i] = 0.0;
+    for (int64_t i = 0; i < st.c_len; ++i) st.c_cur[i] = 0.0;
 }
 
 // multi-GPU path: after the prologue has consumed the previous step's accumulators
@@ -327,7 +418,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
     if (fin) {
         if (threadIdx.x == 0) finalize_index(st, j, k, tol);
         __syncthreads();                             // scalars read before the accumulators clear
-        for (int64_t i = threadIdx.x; i < 2 * st.crep * c_stride(st, k); i += blockDim.x) st.c_cur[i] = 0.0;
+        for (int64_t i = threadIdx.x; i < st.c_len; i += blockDim.x) st.c_cur[i] = 0.0;
     }
     if (threadIdx.x == 0) {
         if (fin) {
@@ -351,7 +442,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
 // update modes: accumulate beta^2 / advance the step (the step's last kernel) / three-term
 // only (no reorthogonalisation columns; partial reorthogonalisation)
-constexpr int kUpdBeta = 1, kUpdAdvance = 2, kUpd3T = 4;
+constexpr int kUpdBeta = 1, kUpdAdvance = 2, kUpd3T = 4, kUpd1Sync = 8;
 
 template <typename V>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
@@ -367,6 +458,9 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     // the last pass's update is the last kernel of step j: its last CTA to finish advances
     // the device step index (every CTA has read j by then), also on the early-exit paths
     if (st.flags[0] || j >= k - 1) {
+        // one-sync step: alpha of the last step comes from the dots vector (no gather partials)
+        if ((mode & kUpd1Sync) && !st.flags[0] && j == k - 1 && blockIdx.x == 0 && threadIdx.x == 0)
+            st.alpha_cur[0] = st.c_cur[j];
         if (mode & kUpdAdvance) advance_step(st, j, fold && j == k - 1, k, tol);
         return;
     }
@@ -379,9 +473,16 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     const double* __restrict__ c_in = st.c_cur + (int64_t)pass * st.crep * cst;
     double* __restrict__ beta2_out = (mode & kUpdBeta) ? st.beta2_cur : nullptr;
     const int ncols = (mode & kUpd3T) ? 0 : j + 1;
+    // one-sync step: alpha_j = c_r[j], coefficients of r' = r - alpha q_j - beta q_{j-1}:
+    // Q_j^T r' = c_r - alpha_j g1 - beta_{j-1} g2 (all-reduced, normalised columns)
+    const double al1 = (mode & kUpd1Sync) ? c_in[j] : 0.0;
+    const double bt1 = (mode & kUpd1Sync) && j > 0 ? st.beta[j - 1] : 0.0;
+    if ((mode & kUpd1Sync) && blockIdx.x == 0 && threadIdx.x == 0) st.alpha_cur[0] = al1;
     for (int i = threadIdx.x; i < ncols; i += blockDim.x) {
         double ci;
-        if (st.crep == 4) {                     // independent loads (one L2 round trip)
+        if (mode & kUpd1Sync) {
+            ci = c_in[i] - al1 * c_in[cst + i] - bt1 * c_in[2 * cst + i];
+        } else if (st.crep == 4) {              // independent loads (one L2 round trip)
             ci = (c_in[i] + c_in[cst + i]) + (c_in[2 * cst + i] + c_in[3 * cst + i]);
         } else {
             ci = 0.0;
@@ -391,7 +492,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     }
     __syncthreads();
     const double sj = st.qscale[j];
-    const double aj = st.alpha_cur[0] * sj;
+    const double aj = ((mode & kUpd1Sync) ? al1 : st.alpha_cur[0]) * sj;
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
     double b2 = 0.0;
     const int64_t nchunks = ldq / W;
@@ -552,6 +653,7 @@ struct StepPlan {
     RcStream rs;
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
     bool partial;                 // partial reorthogonalisation (single GPU)
+    bool one_sync;                // several GPUs, fp32, one CGS pass: the one-sync step (reorth_dots3)
     int64_t ldq;
     size_t smu;
 };
@@ -595,7 +697,30 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_GATHER, s);
-        launch_gather<V>(c, zj, Q, ref, r, st.alpha_cur, s, pl.fold ? &pl.rs : nullptr);
+        launch_gather<V>(c, zj, Q, ref, r, pl.one_sync ? nullptr : st.alpha_cur, s, pl.fold ? &pl.rs : nullptr);
+    }
+    if (pl.one_sync) {
+        // one pass over Q~_j, one all-reduce of the three dot vectors (alpha included), the
+        // update, the beta^2 all-reduce: three collectives per step instead of four
+        {
+            ProfScope ps(LOVE_PROF_REORTH_DOTS, s);
+            LOVE_LAUNCH(reorth_dots3_kernel<V>, dots_grid(pl.ldq, VecT<V>::W, pl.k), 256,
+                        sizeof(double) * 3 * 8 * (pl.k + 1), s, (const V*)Q, pl.ldq, pl.k, (const V*)r, st);
+        }
+        {
+            ProfScope ps(LOVE_PROF_COMM, s);
+            allreduce_sum(c, st.c_cur, 3 * (int64_t)(pl.k + 1), true, s);
+        }
+        {
+            ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
+            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0,
+                        kUpdBeta | kUpdAdvance | kUpd1Sync, r, st, c.tol, 0, (const int*)nullptr);
+        }
+        {
+            ProfScope ps(LOVE_PROF_COMM, s);
+            allreduce_sum(c, st.beta2_cur, 1, true, s);
+        }
+        return;
     }
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
@@ -659,6 +784,11 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
     pl.fold = c.comm == nullptr && std::getenv("LOVE_NO_FOLD") == nullptr;
     pl.partial = c.partial;
+    // the one-sync step needs 3 (k+1) fp64 partial dots per warp in shared memory
+    pl.one_sync = c.comm != nullptr && c.precision == LOVE_FP32 && c.reorth_passes == 1 && !c.partial &&
+                  sizeof(double) * 3 * 8 * (size_t)(c.k_req + 1) <= 200 * 1024 &&
+                  std::getenv("LOVE_NO_ONE_SYNC") == nullptr;
+    if (pl.one_sync) ensure_smem((const void*)reorth_dots3_kernel<V>, sizeof(double) * 3 * 8 * (c.k_req + 1));
     pl.rs = RcStream{c.st, (const double*)c.z[0], (const double*)c.z[1], (double*)c.Rc_col, (double*)c.a, pl.m,
                      pl.mean_y};
     pl.ldq = c.ldq;

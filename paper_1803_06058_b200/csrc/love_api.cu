@@ -286,13 +286,14 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
     {
         const size_t K = k;
-        const size_t nd = K + K + 2 * K * (K + 1) + 1 + (K + 1) + 5 * K + 2 + 1;
+        const size_t nd = 2 + 3 * (K + 1) + 1 + (K + 1) + 5 * K + 2 + 1;
         c->scal = (double*)dalloc(*c, sizeof(double) * nd, s);
         double* p = c->scal;
         LanczosState& st = c->st;
         st.alpha_cur = p; p += 1;
         st.beta2_cur = p; p += 1;
-        st.c_cur = p; p += 2 * (K + 1);
+        st.c_cur = p; p += 3 * (K + 1);     // passes 0, 1 (CGS2) or the one-sync step's three dot vectors
+        st.c_len = 3 * (int64_t)(K + 1);
         st.bnorm2 = p; p += 1;
         st.qscale = p; p += K + 1;
         st.alpha = p; p += K;
@@ -318,6 +319,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
             st.crep = 4;                                 // measured: 4 beats 8 and 16 (cfg2, cfg3)
             st.cld = (int)(round_up((int64_t)K + 1, 16) + 16);
             st.c_cur = (double*)dalloc(*c, sizeof(double) * 2 * st.crep * st.cld, s);
+            st.c_len = 2 * (int64_t)st.crep * st.cld;
         }
         LOVE_LAUNCH(init_state_kernel, 1, 32, 0, s, st.flags, k, c->one);
     }

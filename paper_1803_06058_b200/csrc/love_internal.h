@@ -56,6 +56,7 @@ struct LanczosState {
     int crep = 1;          // copies of each pass's dots (CTA b adds to copy b % crep: same-address
                            // fp64 atomics serialise in L2; the update sums the copies)
     int cld = 0;           // stride between copies (0: k + 1)
+    int64_t c_len = 0;     // doubles of c_cur (cleared once a step's scalars are final)
     double* bnorm2;        // [1]        ||b||^2
     double* qscale;        // [k+1]      1/||q~_j|| (lazy normalisation of Q's columns)
     double* alpha;         // [k]

@@ -674,6 +674,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         st.alpha_cur = p; p += 1;
         st.beta2_cur = p; p += 1;
         st.c_cur = p; p += 2 * (K + 1);
+        st.c_len = 2 * (int64_t)(K + 1);
         st.bnorm2 = p; p += 1;
         st.qscale = p; p += K + 1;
         st.alpha = p; p += K;

@@ -21,6 +21,9 @@ namespace love {
 namespace {
 
 constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
+#ifndef LOVE_PULL3_SG
+#define LOVE_PULL3_SG 4     // outer slots per thread of the 3-D last-axis pull (16: one thread per node)
+#endif
 #ifndef LOVE_PAIRED3
 #define LOVE_PAIRED3 1
 #endif
@@ -164,20 +167,26 @@ __global__ void __launch_bounds__(256) moments2_tpc_kernel(int64_t n_items, cons
 //   pull_mid  : V[a][c0, i1, i2]          = sum_b T[a*4 + b][c0, i1 - b + 1, i2]          (d = 3)
 //   pull_first: u[i0, ...]                = s_j * sum_a X[a][i0 - a + 1, ...]            (X = V or T)
 // Every pull reads 4 neighbours per output, coalesced along the last axis.
-template <int D, typename MT>
+// Thread per (node x, group of SG outer slots): d = 3 has 16 outer slots so, split over
+// 16 / SG threads per node (x fastest: coalesced M and T along the grid), fewer registers
+// and shorter chains per thread than one thread per node.
+template <int D, typename MT, int SG>
 __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_items, const int* __restrict__ cis,
                                                         const MT* __restrict__ M, StepRef ref,
                                                         double* __restrict__ T) {
     pdl_wait();
     constexpr int SO = D == 2 ? 4 : 16;
+    static_assert(SO % SG == 0, "slot groups");
     const int m = g.m_total;
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= m || step_done(ref)) return;
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)m * (SO / SG) || step_done(ref)) return;
+    const int grp = (int)(idx / m), x = (int)(idx - (int64_t)grp * m);
+    const int so0 = grp * SG;
     const int ml = g.m[D - 1];
     const int il = x % ml;
-    double sum[SO];
+    double sum[SG];
 #pragma unroll
-    for (int so = 0; so < SO; ++so) sum[so] = 0.0;
+    for (int so = 0; so < SG; ++so) sum[so] = 0.0;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const int cl = il - c + 1;
@@ -186,10 +195,10 @@ __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_ite
         const int e = cis[cell + 1];
         for (int it = cis[cell]; it < e; ++it)
 #pragma unroll
-            for (int so = 0; so < SO; ++so) sum[so] += (double)M[(int64_t)(so * 4 + c) * n_items + it];
+            for (int so = 0; so < SG; ++so) sum[so] += (double)M[(int64_t)((so0 + so) * 4 + c) * n_items + it];
     }
 #pragma unroll
-    for (int so = 0; so < SO; ++so) T[(int64_t)so * m + x] = sum[so];
+    for (int so = 0; so < SG; ++so) T[(int64_t)(so0 + so) * m + x] = sum[so];
 }
 
 __global__ void __launch_bounds__(256) pull_mid_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
@@ -513,7 +522,7 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             if (ni)
                 LOVE_LAUNCH(moments2_tpc_kernel<V>, (int)ceil_div(2 * ni, 256), 256, 0, s, ni, c.item_start, f0, f1, q,
                             ref, M);
-            LOVE_LAUNCH((pull_last_kernel<2, double>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
+            LOVE_LAUNCH((pull_last_kernel<2, double, 4>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
                         c.cell_item_start, (const double*)M, ref, (double*)c.pullT);
             LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
         } else {
@@ -521,8 +530,9 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             using MT = typename AccT<V, 3>::type;
             MT* Mf = (MT*)c.M;
             if (ni) LOVE_LAUNCH((moments_kernel<V, 3, MT>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, Mf);
-            LOVE_LAUNCH((pull_last_kernel<3, MT>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
-                        c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
+            constexpr int SG = LOVE_PULL3_SG;
+            LOVE_LAUNCH((pull_last_kernel<3, MT, SG>), (int)ceil_div((int64_t)m * (16 / SG), 256), 256, 0, s, c.g,
+                        ni, c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
             LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g, (const double*)c.pullT,
                         ref, (double*)c.pullV);
             LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);

@@ -36,7 +36,7 @@ def host_plumbing(rank: int, world: int, port: int) -> None:
         dist.destroy_process_group()
 
 
-def sharded_lanczos(rank: int, world: int, port: int, kind: str, passes: int) -> None:
+def sharded_lanczos(rank: int, world: int, port: int, kind: str, passes: int, one_sync: bool = False) -> None:
     """The exchange schedule liblove runs on N GPUs, with gloo all-reduces in
     place of NCCL: each rank owns a contiguous shard of the training points; per step
       u = allreduce(W_r q_r); z = K_UU u; r_r = W_r^T z + s2 q_r; alpha = allreduce(q_r.r_r)
@@ -75,14 +75,27 @@ def sharded_lanczos(rank: int, world: int, port: int, kind: str, passes: int) ->
             u = allreduce(O.W_apply(idx, w, Q[:, j], M))
             z = O.kuu_matvec(full.cols, full.outputscale, u)
             r = O.WT_apply(idx, w, z) + full.sigma2 * Q[:, j]
-            a = float(allreduce(np.array([Q[:, j] @ r]))[0])
-            alpha.append(a)
-            if j == k - 1:
-                break
-            r = r - a * Q[:, j] - (beta[j - 1] * Q[:, j - 1] if j > 0 else 0.0)
-            for _ in range(passes):
-                c = allreduce(Q[:, :j + 1].T @ r)
-                r = r - Q[:, :j + 1] @ c
+            if one_sync:
+                # one all-reduce of Q_j^T [r, q_j, q_{j-1}]: alpha = (Q^T r)_j,
+                # Q_j^T r' = Q^T r - alpha Q^T q_j - beta Q^T q_{j-1}
+                qm1 = Q[:, j - 1] if j > 0 else np.zeros(hi - lo)
+                D3 = allreduce(np.stack([Q[:, :j + 1].T @ r, Q[:, :j + 1].T @ Q[:, j], Q[:, :j + 1].T @ qm1]))
+                a = float(D3[0, j])
+                alpha.append(a)
+                if j == k - 1:
+                    break
+                bj = beta[j - 1] if j > 0 else 0.0
+                c = D3[0] - a * D3[1] - bj * D3[2]
+                r = r - a * Q[:, j] - bj * qm1 - Q[:, :j + 1] @ c
+            else:
+                a = float(allreduce(np.array([Q[:, j] @ r]))[0])
+                alpha.append(a)
+                if j == k - 1:
+                    break
+                r = r - a * Q[:, j] - (beta[j - 1] * Q[:, j - 1] if j > 0 else 0.0)
+                for _ in range(passes):
+                    c = allreduce(Q[:, :j + 1].T @ r)
+                    r = r - Q[:, :j + 1] @ c
             b = float(np.sqrt(allreduce(np.array([r @ r]))[0]))
             if b < 1e-10 * (max(abs(x) for x in alpha) + 2.0 * max(beta + [b])):
                 k_eff = j + 1

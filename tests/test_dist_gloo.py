@@ -26,3 +26,11 @@ def test_sharded_lanczos_matches_oracle_world2(kind, passes):
 
 def test_liblove_host_plumbing_world2():
     mp.spawn(W.liblove_host_plumbing, args=(2, _port()), nprocs=2, join=True)
+
+
+@pytest.mark.parametrize("kind", ["cfg1", "2d"])
+def test_one_sync_schedule_matches_oracle_world2(kind):
+    """The one-sync step liblove runs on several GPUs in fp32 (three collectives per step:
+    u, the dot vectors Q_j^T [r, q_j, q_{j-1}], beta^2), in fp64 oracle arithmetic, sharded
+    over 2 gloo ranks: the same Lanczos as the unsharded CGS oracle."""
+    mp.spawn(W.sharded_lanczos, args=(2, _port(), kind, 1, True), nprocs=2, join=True)

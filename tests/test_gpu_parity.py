@@ -320,12 +320,18 @@ def test_prior_exact_mode():
     _assert_var(var, ov, np.full(len(ov), p.outputscale), fp64=True)
 
 
+@pytest.mark.parametrize("one_sync", [True, False])
 @pytest.mark.parametrize("ci,n,m,k", [(2, 50_003, (5000,), 30), (4, 40_009, (24, 24, 24), 25)])
-def test_sharded_code_path_one_rank_nccl(ci, n, m, k):
+def test_sharded_code_path_one_rank_nccl(ci, n, m, k, one_sync, monkeypatch):
     """The multi-GPU code path (every all-reduce issued through NCCL, eager step launches)
     with a one-rank communicator must give the single-GPU result: the collectives are
-    identities, so any addressing or ordering bug in the sharded path shows up here."""
+    identities, so any addressing or ordering bug in the sharded path shows up here.  fp32
+    runs the one-sync step by default (one pass over Q~ for Q^T [r, q_j, q_{j-1}], three
+    collectives per step); LOVE_NO_ONE_SYNC=1 the four-collective step.  Both
+    also meet the oracle bound."""
     from paper_1803_06058_b200 import nccl_unique_id
+    if not one_sync:
+        monkeypatch.setenv("LOVE_NO_ONE_SYNC", "1")
     p = scaled_config(ci, n=n, m=m, k=k, t=2001)
     inp = make_inputs(p)
     c1 = _build(p, inp)
@@ -335,7 +341,19 @@ def test_sharded_code_path_one_rank_nccl(ci, n, m, k):
     assert cN.info()["k_eff"] == c1.info()["k_eff"]
     np.testing.assert_allclose(cN.info()["alpha"], c1.info()["alpha"], rtol=1e-6)
     np.testing.assert_allclose(vN.cpu().numpy(), v1.cpu().numpy(), rtol=1e-4, atol=1e-7)
-    np.testing.assert_allclose(mN.cpu().numpy(), m1.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    m1, mN = m1.cpu().numpy().astype(np.float64), mN.cpu().numpy().astype(np.float64)
+    if one_sync:
+        # a different (equally valid) fp32 CGS order: the mean, a Krylov solve (Eq. 3), moves
+        # within the fp32 mean tolerance, measured ~5e-6 of max |mean|
+        assert np.max(np.abs(mN - m1)) <= 1e-4 * np.abs(m1).max()
+    else:
+        np.testing.assert_allclose(mN, m1, rtol=1e-4, atol=1e-6)
+    model = _model(p, inp)
+    oc = O.love_precompute(model, p.k)
+    _assert_var(vN.cpu().numpy().astype(np.float64), O.predict_var(model, oc, inp.Xs), _prior(model, inp.Xs),
+                fp64=False)
+    om = O.predict_mean(model, oc, inp.Xs)
+    assert np.max(np.abs(mN - om)) <= 1e-3 * np.abs(om).max()
 
 
 @pytest.mark.parametrize("ci,n,m,k,prec", [(1, 1000, (256,), 50, "fp64"), (2, 60_001, (6000,), 40, "fp32"),

@@ -8,7 +8,7 @@ p = get_config(5)
 inp = make_inputs(p)
 Xs = torch.from_numpy(inp.Xs).cuda()
 c = LoveCache.build(inp.X, inp.y, p.m, p.lo, p.h, p.lengthscale, p.outputscale, p.sigma2, p.k,
-                    precision=p.precision, k_sample=p.k_sample)
+                    precision=p.precision, k_sample=p.k_sample, cache_fp64=p.cache_fp64)
 torch.cuda.synchronize()
 torch.cuda.cudart().cudaProfilerStart()
 for _ in range(3):
