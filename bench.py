@@ -567,6 +567,15 @@ def main():
                 "achieved": q_ach, "peak": peak, "unit": "GB/s", "frac": q_ach / peak,
                 "bytes_per_query": bq, "kernel_ms": qk_ms,
                 "timing": "CUDA events around the query launches (profiled steps)"}
+    if p.kind != "additive" and p.d <= 2:
+        # the cell-block table (m blocks) is L2-resident: the DRAM floor is each query's x* and
+        # result plus the table once, far below the gathered bytes
+        nb = 4 ** p.d
+        ub = t_loc * (8 * p.d + (8 if p.precision == "fp64" else 4)) + p.m_total * 8 * nb * (nb + 1) // 2
+        query_rf["unique_dram_bytes"] = ub
+        query_rf["unique_dram_frac"] = ub / (qk_ms / 1e3) / 1e9 / peak
+        query_rf["note"] = ("frac counts the block bytes each query gathers (mostly L2 hits: the table is "
+                            f"{p.m_total * 8 * nb * (nb + 1) // 2 / 1e6:.0f} MB); unique_dram_frac the DRAM floor")
     sampling = None
     if p.k_sample:
         smean = float(np.mean(sample_ms))

@@ -452,6 +452,82 @@ __global__ void __launch_bounds__(256) predict_block_kernel(GridDev g, C4 c4, do
     }
 }
 
+// G lanes per query (d = 1: G = 2, d = 2: G = 8): the same w^T B_c w as block_query, with the
+// block's packed entries p read by lane p % G (each group's loads are contiguous: 64 B per load
+// instruction per query instead of one 8-byte load per entry and thread) and the 4^d fp64
+// stencil weights shared through shared memory; the partial sums meet by shuffles.
+template <typename V, int D, int G>
+__global__ void __launch_bounds__(256) predict_block_coop_kernel(GridDev g, C4 c4, double s2, int prior_mode,
+                                                                 const double* __restrict__ blk,
+                                                                 const double* __restrict__ amean,
+                                                                 const double* __restrict__ Xs, int64_t t,
+                                                                 V* __restrict__ out, V* __restrict__ mean_out,
+                                                                 unsigned long long* __restrict__ counters) {
+    constexpr int S = D == 1 ? 4 : 16;
+    constexpr int NB = S * (S + 1) / 2;            // 10 / 136 packed upper-triangular entries
+    constexpr int QPB = 256 / G;                   // queries per CTA
+    __shared__ unsigned char pa[NB], pb[NB];
+    __shared__ double ws[QPB][S];
+    for (int p = threadIdx.x; p < NB; p += blockDim.x) {
+        int a = 0, r = p;
+        while (r >= S - a) { r -= S - a; ++a; }
+        pa[p] = (unsigned char)a;
+        pb[p] = (unsigned char)(a + r);
+    }
+    const int gl = threadIdx.x % G, ql = threadIdx.x / G;
+    const int64_t qi = (int64_t)blockIdx.x * QPB + ql;
+    const bool live = qi < t;
+    const Stencil A = make_stencil<D>(g, Xs + (live ? qi : 0) * D);
+    for (int a = gl; a < S; a += G) ws[ql][a] = D == 1 ? pick4(A.w[0], a) : pick4(A.w[0], a >> 2) * pick4(A.w[1], a & 3);
+    __syncthreads();
+    const bool ok = live && A.ok;
+    double v = 0.0, mu = 0.0;
+    if (ok) {
+        const int cell = D == 1 ? A.j[0] : A.j[0] * g.m[1] + A.j[1];
+        const double* __restrict__ B = blk + (int64_t)cell * blk_size(D);
+#pragma unroll
+        for (int p = gl; p < NB; p += G) {
+            const int a = pa[p], b = pb[p];
+            const double wab = ws[ql][a] * ws[ql][b];
+            v += (a == b ? wab : 2.0 * wab) * __ldg(B + p);
+        }
+        if (mean_out) {
+            for (int a = gl; a < S; a += G) {
+                const int node = D == 1 ? A.base + a : A.base + (a >> 2) * g.stride[0] + (a & 3);
+                mu += ws[ql][a] * __ldg(amean + node);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+        mu += __shfl_xor_sync(0xffffffffu, mu, o);
+    }
+    if (gl != 0 || !live) return;
+    if (!A.ok) {
+        out[qi] = (V)NAN;
+        if (mean_out) mean_out[qi] = (V)NAN;
+        atomicAdd(&counters[1], 1ull);
+        return;
+    }
+    if (prior_mode == LOVE_PRIOR_EXACT) {          // k(x*, x*) - w^T K_UU w + w^T B w  (Eq. 10)
+        double pr = s2;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc += A.w[d][a] * A.w[d][b] * c4.c[d][a > b ? a - b : b - a];
+            pr *= acc;
+        }
+        v += s2 - pr;
+    }
+    out[qi] = (V)v;
+    if (v < 0.0) atomicAdd(&counters[0], 1ull);
+    if (mean_out) mean_out[qi] = (V)mu;
+}
+
 }  // namespace
 
 // ---- d = 3 variance queries grouped by cell (SURVEY 8(f) NEXT #3a): the queries are
@@ -750,6 +826,19 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
         C4 c4{};
         for (int d = 0; d < c.g.d; ++d)
             for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
+        const char* ce = std::getenv("LOVE_QUERY_COOP");
+        const bool coop = ce == nullptr || std::atoi(ce) != 0;
+        if (coop) {                              // G lanes per query (d = 1: 2, d = 2: 8)
+            if (c.g.d == 1)
+                LOVE_LAUNCH((predict_block_coop_kernel<V, 1, 2>), (int)ceil_div(t, 128), 256, 0, s, c.g, c4,
+                            c.rbf.outputscale, c.prior, (const double*)c.vblk, (const double*)c.a, Xa, t, out, mean_out,
+                            c.counters);
+            else
+                LOVE_LAUNCH((predict_block_coop_kernel<V, 2, 8>), (int)ceil_div(t, 32), 256, 0, s, c.g, c4,
+                            c.rbf.outputscale, c.prior, (const double*)c.vblk, (const double*)c.a, Xa, t, out, mean_out,
+                            c.counters);
+            return;
+        }
         // one query per thread (measured: two per thread with interleaved chains is ~8% slower)
         if (c.g.d == 1)
             LOVE_LAUNCH((predict_block_kernel<V, 1, 1>), (int)ceil_div(t, 256), 256, 0, s, c.g, c4, c.rbf.outputscale,

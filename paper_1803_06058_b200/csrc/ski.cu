@@ -21,6 +21,9 @@ namespace love {
 namespace {
 
 constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
+#ifndef LOVE_PULL2_SG
+#define LOVE_PULL2_SG 4     // outer slots per thread of the 2-D last-axis pull (4: one thread per node)
+#endif
 #ifndef LOVE_PULL3_SG
 #define LOVE_PULL3_SG 4     // outer slots per thread of the 3-D last-axis pull (16: one thread per node)
 #endif
@@ -522,8 +525,9 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             if (ni)
                 LOVE_LAUNCH(moments2_tpc_kernel<V>, (int)ceil_div(2 * ni, 256), 256, 0, s, ni, c.item_start, f0, f1, q,
                             ref, M);
-            LOVE_LAUNCH((pull_last_kernel<2, double, 4>), (int)ceil_div(m, 256), 256, 0, s, c.g, ni,
-                        c.cell_item_start, (const double*)M, ref, (double*)c.pullT);
+            constexpr int SG2 = LOVE_PULL2_SG;
+            LOVE_LAUNCH((pull_last_kernel<2, double, SG2>), (int)ceil_div((int64_t)m * (4 / SG2), 256), 256, 0, s,
+                        c.g, ni, c.cell_item_start, (const double*)M, ref, (double*)c.pullT);
             LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
         } else {
             // the 3-D moments are stored in their accumulation type (fp32 in LOVE_FP32 mode)

@@ -521,3 +521,23 @@ def test_var_blocks2_pair_products_equal_warp_kernel(monkeypatch):
         # the two builds differ only by fp64 atomic order in the Lanczos; the block algebra is
         # exact: fp32 outputs agree to round-off
         np.testing.assert_allclose(v, vw, rtol=2e-6, atol=1e-9)
+
+
+@pytest.mark.parametrize("ci,n,m", [(1, 1000, (256,)), (3, 30_007, (48, 40))])
+@pytest.mark.parametrize("prior", ["ski", "exact"])
+def test_block_queries_cooperative_equal_per_thread(ci, n, m, prior, monkeypatch):
+    """d <= 2 variance-block queries with G lanes per query (query.cu predict_block_coop_kernel,
+    the default) equal the one-thread-per-query kernel (LOVE_QUERY_COOP=0) to fp64 summation
+    order, means included, out-of-range points NaN in both (fp64 build)."""
+    p = scaled_config(ci, n=n, m=m, k=30, t=5001, precision="fp64")
+    inp = make_inputs(p)
+    Xs = inp.Xs.copy()
+    Xs[7] = 50.0                                       # outside the grid
+    c = _build(p, inp, prior=prior)
+    v, mu = (x.cpu().numpy() for x in c.predict_var(Xs, return_mean=True))
+    monkeypatch.setenv("LOVE_QUERY_COOP", "0")                      # same cache, other kernel
+    v2, mu2 = (x.cpu().numpy() for x in c.predict_var(Xs, return_mean=True))
+    assert np.isnan(v[7]) and np.isnan(v2[7]) and np.isnan(mu[7])
+    ok = ~np.isnan(v2)
+    np.testing.assert_allclose(v[ok], v2[ok], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(mu[ok], mu2[ok], rtol=1e-10, atol=1e-14)
