@@ -315,6 +315,13 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
             st.pro_eps = eps;
             st.pro_tol = o.reorth_tol > 0.0 ? o.reorth_tol : std::sqrt(eps);
         }
+        // DGKS-gated second CGS pass (fp64 CGS2, one GPU): the second pass runs only when the
+        // first one removed more than 1 - 1/sqrt(2) of the norm (LOVE_NO_DGKS: always)
+        if (c->reorth_passes == 2 && c->comm == nullptr && !c->partial && !c->fused &&
+            std::getenv("LOVE_NO_DGKS") == nullptr) {
+            st.nrm2 = (double*)dalloc(*c, sizeof(double) * 2, s);
+            st.dgks = 1;
+        }
         if (c->comm == nullptr) {                        // one GPU: spread the dot atomics
             st.crep = 4;                                 // measured: 4 beats 8 and 16 (cfg2, cfg3)
             st.cld = (int)(round_up((int64_t)K + 1, 16) + 16);

@@ -57,6 +57,11 @@ struct LanczosState {
                            // fp64 atomics serialise in L2; the update sums the copies)
     int cld = 0;           // stride between copies (0: k + 1)
     int64_t c_len = 0;     // doubles of c_cur (cleared once a step's scalars are final)
+    // DGKS-gated second CGS pass (fp64, one GPU): nrm2[0] = ||r'||^2 (pass-0 source, summed by
+    // the pass-0 dots), nrm2[1] = ||r''||^2 (pass-0 update output); pass 1 runs only when
+    // ||r''||^2 < ||r'||^2 / 2 ("twice is enough")
+    double* nrm2 = nullptr;
+    int dgks = 0;
     double* bnorm2;        // [1]        ||b||^2
     double* qscale;        // [k+1]      1/||q~_j|| (lazy normalisation of Q's columns)
     double* alpha;         // [k]

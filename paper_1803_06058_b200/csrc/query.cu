@@ -395,12 +395,29 @@ __device__ __forceinline__ void block_query(const GridDev& g, const C4& c4, doub
     const double* __restrict__ B = blk + (int64_t)cell * blk_size(D);
     double v = 0.0;
     int p = 0;
+    if constexpr (D == 1) {                      // the 80-byte block as five 16-byte loads
+        double bb[10];
+#pragma unroll
+        for (int h = 0; h < 5; ++h) {
+            const double2 x = __ldg(reinterpret_cast<const double2*>(B) + h);
+            bb[2 * h] = x.x;
+            bb[2 * h + 1] = x.y;
+        }
+#pragma unroll
+        for (int a = 0; a < S; ++a) {
+            double row = 0.5 * w[a] * bb[p++];
+#pragma unroll
+            for (int b = a + 1; b < S; ++b) row += w[b] * bb[p++];
+            v += 2.0 * w[a] * row;
+        }
+    } else {
 #pragma unroll
     for (int a = 0; a < S; ++a) {
         double row = 0.5 * w[a] * __ldg(B + p++);
 #pragma unroll
         for (int b = a + 1; b < S; ++b) row += w[b] * __ldg(B + p++);
         v += 2.0 * w[a] * row;
+    }
     }
     if (prior_mode == LOVE_PRIOR_EXACT) {
         // k(x*, x*) - w^T K_UU w + w^T B w   (the exact prior of Eq. 10)
@@ -828,7 +845,9 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
             for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
         const char* ce = std::getenv("LOVE_QUERY_COOP");
         const bool coop = ce == nullptr || std::atoi(ce) != 0;
-        if (coop) {                              // G lanes per query (d = 1: 2, d = 2: 8)
+        // measured (ncu, 10^6 queries): d = 2 with 8 lanes per query 245 vs 348 us; d = 1 keeps
+        // one thread per query (25 vs 32 us with 2 lanes)
+        if (coop && c.g.d == 2) {                // G lanes per query (d = 2: 8)
             if (c.g.d == 1)
                 LOVE_LAUNCH((predict_block_coop_kernel<V, 1, 2>), (int)ceil_div(t, 128), 256, 0, s, c.g, c4,
                             c.rbf.outputscale, c.prior, (const double*)c.vblk, (const double*)c.a, Xa, t, out, mean_out,

@@ -687,6 +687,10 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         st.jdev = st.flags + 4;
         st.step_ctr = st.flags + 5;
         st.chol = 0;
+        if (std::getenv("LOVE_NO_DGKS") == nullptr) {   // DGKS-gated second CGS pass (lanczos.cu)
+            st.nrm2 = (double*)dalloc(c, sizeof(double) * 2, s);
+            st.dgks = 1;
+        }
         const int f[4] = {0, ks, 0, 0};
         cuda_check(cudaMemcpyAsync(st.flags, f, sizeof(f), cudaMemcpyHostToDevice, s), "sampling flags");
     }
