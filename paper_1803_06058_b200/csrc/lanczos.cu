@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     const int j = *st.jdev;
     if (st.flags[0] || j >= k - 1) return;
     if (gate != nullptr && !*gate) return;
-    if (st.dgks && pass == 1 && !(st.nrm2[1] < 0.5 * st.nrm2[0])) return;   // DGKS: pass 1 not needed
+    if (sizeof(V) == 8 && st.dgks && pass == 1 && !(st.nrm2[1] < 0.5 * st.nrm2[0])) return;   // DGKS: pass 1 not needed
     const int from_r = pass == 0;
     double* __restrict__ c_out = st.c_cur + ((int64_t)pass * st.crep + blockIdx.x % st.crep) * c_stride(st, k);
     const int ncols = j + 1;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
     const int64_t nvec = ldq / W;
     V src[CPT][W];
     int64_t qv[CPT];
-    double s2 = 0.0;                                     // ||r'||^2 partial (DGKS, pass 0)
+    double s2 = 0.0;                                     // ||r'||^2 partial (DGKS, pass 0, fp64 only)
 #pragma unroll
     for (int u = 0; u < CPT; ++u) {
         qv[u] = ((int64_t)blockIdx.x * CPT + u) * blockDim.x + threadIdx.x;
@@ -201,13 +201,15 @@ __global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restr
 #pragma unroll
         for (int e = 0; e < W; ++e) {
             src[u][e] = (V)v[e];
-            s2 += v[e] * v[e];
+            if constexpr (sizeof(V) == 8) s2 += v[e] * v[e];
         }
     }
-    if (st.dgks && pass == 0 && blockIdx.y == 0) {      // one column group counts the rows once
-        __shared__ double red2[32];
-        s2 = block_sum(s2, red2);
-        if (threadIdx.x == 0) atomicAdd(&st.nrm2[0], s2);
+    if constexpr (sizeof(V) == 8) {                     // (the fp32 instantiation keeps 32 registers)
+        if (st.dgks && pass == 0 && blockIdx.y == 0) {  // one column group counts the rows once
+            __shared__ double red2[32];
+            s2 = block_sum(s2, red2);
+            if (threadIdx.x == 0) atomicAdd(&st.nrm2[0], s2);
+        }
     }
     const int b2 = (lane >> 2) & 1, b1 = (lane >> 1) & 1, b0 = lane & 1;
     constexpr int NB = LOVE_SWEEP_NB;                    // 8-column blocks whose loads are issued together
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
         return;
     }
-    if (st.dgks && pass == 1 && !(st.nrm2[1] < 0.5 * st.nrm2[0])) {
+    if (sizeof(V) == 8 && st.dgks && pass == 1 && !(st.nrm2[1] < 0.5 * st.nrm2[0])) {
         // DGKS: the first pass kept ||r''|| >= ||r'|| / sqrt 2, the column stands; beta^2 is its norm
         if (threadIdx.x == 0) st.beta2_cur[0] = st.nrm2[1];
         if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
@@ -492,7 +494,8 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     const int from_r = pass == 0;
     const int64_t cst = c_stride(st, k);
     const double* __restrict__ c_in = st.c_cur + (int64_t)pass * st.crep * cst;
-    double* __restrict__ beta2_out = (mode & kUpdBeta) ? st.beta2_cur : (st.dgks && pass == 0) ? st.nrm2 + 1 : nullptr;
+    double* __restrict__ beta2_out =
+        (mode & kUpdBeta) ? st.beta2_cur : (sizeof(V) == 8 && st.dgks && pass == 0) ? st.nrm2 + 1 : nullptr;
     const int ncols = (mode & kUpd3T) ? 0 : j + 1;
     // one-sync step: alpha_j = c_r[j], coefficients of r' = r - alpha q_j - beta q_{j-1}:
     // Q_j^T r' = c_r - alpha_j g1 - beta_{j-1} g2 (all-reduced, normalised columns)

@@ -317,7 +317,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         }
         // DGKS-gated second CGS pass (fp64 CGS2, one GPU): the second pass runs only when the
         // first one removed more than 1 - 1/sqrt(2) of the norm (LOVE_NO_DGKS: always)
-        if (c->reorth_passes == 2 && c->comm == nullptr && !c->partial && !c->fused &&
+        if (c->reorth_passes == 2 && c->precision == LOVE_FP64 && c->comm == nullptr && !c->partial && !c->fused &&
             std::getenv("LOVE_NO_DGKS") == nullptr) {
             st.nrm2 = (double*)dalloc(*c, sizeof(double) * 2, s);
             st.dgks = 1;

@@ -8,6 +8,8 @@
 // runs of 4 rows.
 #include <cuda_runtime.h>
 
+#include <cuda_pipeline.h>
+
 #include <cmath>
 #include <cstdlib>
 
@@ -677,6 +679,20 @@ __device__ __forceinline__ double sorted3_mean(const Stencil& A, const double* _
 }
 
 // Queries counting-sorted by cell (SURVEY 8(f) NEXT #3a): a CTA stages the 64 stencil rows of
+// cp.async of the 64 stencil rows of cell c (k_pad values each) into dst, one commit group
+template <typename V>
+__device__ __forceinline__ void stage_rows3(const GridDev& g, const V* __restrict__ Rc, int k_pad, int nch, int c,
+                                            V* dst) {
+    constexpr int W = QV<V>::W;
+    const int base = c - g.stride[0] - g.stride[1] - 1;
+    for (int e = threadIdx.x; e < 64 * nch; e += blockDim.x) {
+        const int l = e / nch, ch = e - l * nch;
+        const int node = base + (l >> 4) * g.stride[0] + ((l >> 2) & 3) * g.stride[1] + (l & 3);
+        __pipeline_memcpy_async(dst + l * k_pad + ch * W, Rc + (int64_t)node * k_pad + ch * W, sizeof(V) * W);
+    }
+    __pipeline_commit();
+}
+
 // Rc of a cell in shared memory once.  Cells with at least kLanePerQuery queries: one lane per
 // query, every lane reading the same row chunk (a shared-memory broadcast feeds 32 queries);
 // sparser cells: a warp per query, lanes over 16-byte chunks of k.
@@ -695,25 +711,30 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
     constexpr int W = QV<V>::W;
     using VT = typename QV<V>::T;
     extern __shared__ __align__(16) unsigned char smraw[];
-    V* rows = reinterpret_cast<V*>(smraw);                       // [64][k_pad]
+    // two [64][k_pad] row buffers: the rows of the next occupied cell are copied in
+    // (cp.async, no registers) while the queries of the current one are answered
+    V* const rows0 = reinterpret_cast<V*>(smraw);
+    const int64_t bstride = 64 * (int64_t)k_pad;
     __shared__ double part[256];                                 // lane mode: [warp][lane] partial norms
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nch = k_pad / W;
     const int m = g.m_total;
     const int c_begin = blockIdx.x * cells_per_cta;
     const int c_end = min(m, c_begin + cells_per_cta);
-    for (int c = c_begin; c < c_end; ++c) {
-        const int p0 = qstart[c], p1 = qstart[c + 1];
-        if (p0 == p1) continue;
-        const int base = c - g.stride[0] - g.stride[1] - 1;      // node of stencil offset (0, 0, 0)
-        __syncthreads();                                        // previous cell's rows are free
-        for (int e = threadIdx.x; e < 64 * nch; e += blockDim.x) {
-            const int l = e / nch, ch = e - l * nch;
-            const int node = base + (l >> 4) * g.stride[0] + ((l >> 2) & 3) * g.stride[1] + (l & 3);
-            *reinterpret_cast<VT*>(rows + l * k_pad + ch * W) =
-                __ldg(reinterpret_cast<const VT*>(Rc + (int64_t)node * k_pad + ch * W));
-        }
+    int c = c_begin;
+    while (c < c_end && qstart[c] == qstart[c + 1]) ++c;        // first cell with queries
+    if (c < c_end) stage_rows3<V>(g, Rc, k_pad, nch, c, rows0);
+    int buf = 0;
+    while (c < c_end) {
+        int cn = c + 1;
+        while (cn < c_end && qstart[cn] == qstart[cn + 1]) ++cn;
+        if (cn < c_end) stage_rows3<V>(g, Rc, k_pad, nch, cn, rows0 + (buf ^ 1) * bstride);
+        if (cn < c_end) __pipeline_wait_prior(1);                // this cell's rows have landed
+        else __pipeline_wait_prior(0);
         __syncthreads();
+        const V* rows = rows0 + buf * bstride;
+        const int p0 = qstart[c], p1 = qstart[c + 1];
+        const int base = c - g.stride[0] - g.stride[1] - 1;      // node of stencil offset (0, 0, 0)
         const int nq = p1 - p0;
         if (nq >= lane_mode_min) {                              // lane per query
             // groups of 32 queries; with fewer groups than warps, wpg warps share a group and
@@ -750,6 +771,9 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
                                       mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
                 }
             }
+            __syncthreads();
+            c = cn;
+            buf ^= 1;
             continue;
         }
         for (int pos = p0 + wid; pos < p1; pos += nw) {         // warp per query
@@ -772,6 +796,9 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
             if (lane != 0) continue;
             finish_sorted3<V>(A, c4, s2, prior_mode, dot, mu, q, out, mean_out, counters);
         }
+        __syncthreads();                                        // this buffer is free for cell cn + 1
+        c = cn;
+        buf ^= 1;
     }
 }
 
@@ -869,7 +896,7 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
     }
     // d = 3 cell-sorted path: the 64 stencil rows of a cell (64 k_pad values) must fit in one
     // CTA's shared memory next to the kernel's static arrays; larger k takes the per-query path
-    const size_t sm3 = sizeof(V) * 64 * (size_t)c.k_pad;
+    const size_t sm3 = 2 * sizeof(V) * 64 * (size_t)c.k_pad;   // two row buffers
     if (Xb == nullptr && c.g.d == 3 && t >= 65536 && std::getenv("LOVE_NO_SORTED_QUERIES") == nullptr &&
         sm3 + sorted3_static_smem<V>() <= optin_smem()) {
         const int m = c.g.m_total;

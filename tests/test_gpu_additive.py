@@ -92,6 +92,14 @@ def test_additive_cfg6_scaled_fp32(probe):
     var, mean = c.predict_var(inp.Xs, return_mean=True)
     ov = O.predict_var(model, oc, inp.Xs)
     _assert_var(var.cpu().numpy().astype(np.float64), ov, _prior(model, inp.Xs), fp64=False)
+    # covariances of an fp32 cache come from its fp64 row copy (Rc64): the variance bound with
+    # sqrt(var_a var_b) and sqrt(P_a P_b) in place of |v| and P
+    Xb = inp.Xs[::-1].copy()
+    cov = c.predict_covar(inp.Xs, Xb).cpu().numpy().astype(np.float64)
+    ocov = O.predict_covar(model, oc, inp.Xs, Xb)
+    scale = np.sqrt(ov * O.predict_var(model, oc, Xb))
+    pscale = np.sqrt(_prior(model, inp.Xs) * _prior(model, Xb))
+    assert np.all(np.abs(cov - ocov) <= 1e-3 * scale + 1e-6 * pscale)
     om = O.predict_mean(model, oc, inp.Xs)
     assert np.max(np.abs(mean.cpu().numpy() - om)) < 1e-3 * np.abs(om).max()
 
