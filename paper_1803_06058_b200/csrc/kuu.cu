@@ -71,11 +71,11 @@ __device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
 inline size_t padded(size_t n) { return n + n / 8 + 1; }
 
 // One radix-R stage of an in-place Stockham FFT over G lines of length L in shared memory
-// (padded indices), run by a block of exactly G*L/8 threads (8/R butterflies per thread).
+// (padded indices), run by a block of exactly G*L/EPT threads (EPT/R butterflies per thread).
 // Every index into the register array is a compile-time constant (no local memory).
-template <int SIGN, int R>
+template <int SIGN, int R, int EPT = 8>
 __device__ __forceinline__ void fft_stage(C* buf, int L, int Ns, const C* tw) {
-    constexpr int PER = 8 / R;
+    constexpr int PER = EPT / R;
     const int nb = L / R;                        // butterflies per line
     const int step = L / (Ns * R);               // twiddle stride
     C v[PER][R];
@@ -120,6 +120,16 @@ __device__ void line_fft(C* buf, int L, const C* tw) {
     for (; Ns * 8 <= L; Ns *= 8) fft_stage<SIGN, 8>(buf, L, Ns, tw);
     if (Ns * 4 == L) fft_stage<SIGN, 4>(buf, L, Ns, tw);
     else if (Ns * 2 == L) fft_stage<SIGN, 2>(buf, L, Ns, tw);
+}
+
+// The same transform with 4 elements per thread (G*L/4 threads): radix-4 stages, then one
+// radix-2 stage.  Twice the threads and a shorter dependent chain per thread than the radix-8
+// form -- the axis passes run one 4-warp CTA per SM, where every fp64 latency is exposed.
+template <int SIGN>
+__device__ void line_fft4(C* buf, int L, const C* tw) {
+    int Ns = 1;
+    for (; Ns * 4 <= L; Ns *= 4) fft_stage<SIGN, 4, 4>(buf, L, Ns, tw);
+    if (Ns * 2 == L) fft_stage<SIGN, 2, 4>(buf, L, Ns, tw);
 }
 
 // copy a line-length twiddle table from global to shared memory
@@ -532,7 +542,7 @@ __global__ void __launch_bounds__(256) axis_line_kernel(const double* __restrict
 // P complex lines per CTA, P*N/8 threads (radix-8 Stockham, 8 elements per thread).
 // LFAST (I == 1): a pair is two consecutive lines (o, o+1) and threads walk along l;
 // otherwise a pair is (i, i+1) of one o and threads walk across pairs (coalesced in i).
-template <bool LFAST>
+template <bool LFAST, int EPT>
 __global__ void axis_conv_kernel(const double* __restrict__ in, double* __restrict__ out, const double* __restrict__ lam,
                                  const C* __restrict__ tw, int L, int I, int64_t O, int N, int P, int64_t npairs,
                                  double scale, const int* __restrict__ done) {
@@ -545,7 +555,7 @@ __global__ void axis_conv_kernel(const double* __restrict__ in, double* __restri
     const int64_t q0 = (int64_t)blockIdx.x * P;
     const int halfI = (I + 1) / 2;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EPT; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
         const int p = LFAST ? t / N : t % P, n = LFAST ? t % N : t / P;
         const int64_t q = q0 + p;
@@ -565,19 +575,23 @@ __global__ void axis_conv_kernel(const double* __restrict__ in, double* __restri
         }
         buf[pad(p * N + n)] = make_double2(x1, x2);
     }
-    __syncthreads();
-    line_fft<-1>(buf, N, tws);
+    double lv[EPT];                              // data-independent: loaded before the transform
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EPT; ++e) lv[e] = __ldg(&lam[(threadIdx.x + e * blockDim.x) % N]);
+    __syncthreads();
+    if (EPT == 4) line_fft4<-1>(buf, N, tws);
+    else line_fft<-1>(buf, N, tws);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
-        const double l = lam[t % N];
-        buf[pad(t)].x *= l;
-        buf[pad(t)].y *= l;
+        buf[pad(t)].x *= lv[e];
+        buf[pad(t)].y *= lv[e];
     }
     __syncthreads();
-    line_fft<+1>(buf, N, tws);
+    if (EPT == 4) line_fft4<+1>(buf, N, tws);
+    else line_fft<+1>(buf, N, tws);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EPT; ++e) {
         const int t = threadIdx.x + e * blockDim.x;
         const int p = LFAST ? t / N : t % P, n = LFAST ? t % N : t / P;
         const int64_t q = q0 + p;
@@ -717,15 +731,24 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
             const int64_t npairs = I == 1 ? (O + 1) / 2 : (int64_t)O * ((I + 1) / 2);
             const size_t sm = sizeof(C) * (N + padded((size_t)P * N));
             const int grid = (int)ceil_div(npairs, P);
+            // 4 elements per thread (radix-4) when the block stays <= 1024 threads (LOVE_AXIS_EPT=8: radix-8)
+            static const int ept_env = std::getenv("LOVE_AXIS_EPT") ? std::atoi(std::getenv("LOVE_AXIS_EPT")) : 4;
+            const bool e4 = ept_env == 4 && P * N / 4 <= 1024;
+            const int thr = P * N / (e4 ? 4 : 8);
+#define LOVE_AXIS_LAUNCH(LF, E)                                                                              \
+    do {                                                                                                     \
+        ensure_smem((const void*)axis_conv_kernel<LF, E>, sm);                                               \
+        LOVE_LAUNCH((axis_conv_kernel<LF, E>), grid, thr, sm, s, in, out, (const double*)c.ax_lam[d],        \
+                    (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale, t_done);                     \
+    } while (0)
             if (I == 1) {
-                ensure_smem((const void*)axis_conv_kernel<true>, sm);
-                LOVE_LAUNCH(axis_conv_kernel<true>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
-                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale, t_done);
+                if (e4) LOVE_AXIS_LAUNCH(true, 4);
+                else LOVE_AXIS_LAUNCH(true, 8);
             } else {
-                ensure_smem((const void*)axis_conv_kernel<false>, sm);
-                LOVE_LAUNCH(axis_conv_kernel<false>, grid, P * N / 8, sm, s, in, out, (const double*)c.ax_lam[d],
-                            (const C*)c.ax_tw[d], L, I, (int64_t)O, N, P, npairs, scale, t_done);
+                if (e4) LOVE_AXIS_LAUNCH(false, 4);
+                else LOVE_AXIS_LAUNCH(false, 8);
             }
+#undef LOVE_AXIS_LAUNCH
         } else if (I == 1) {
             const int64_t total = (int64_t)O * L;
             LOVE_LAUNCH(axis_line_kernel, (int)ceil_div(total, 256), 256, 0, s, in, out, col, (int64_t)O, L, scale, t_done);
