@@ -28,7 +28,8 @@
 namespace love {
 constexpr int kUpdB = LOVE_UPD_B;
 constexpr int kCondSteps = 2;
-template <typename V> int update_grid(int64_t nchunks, size_t smem);
+template <typename V> int update_grid(int64_t nchunks, size_t smem, int cg);
+int update_groups(int64_t nchunks);
 }
 
 namespace love {
@@ -461,7 +462,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
 // only (no reorthogonalisation columns; partial reorthogonalisation)
 constexpr int kUpdBeta = 1, kUpdAdvance = 2, kUpd3T = 4, kUpd1Sync = 8;
 
-template <typename V>
+template <typename V, int CG = 1>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
                                                             int pass, int mode, const V* __restrict__ r,
                                                             LanczosState st, double tol, int fold,
@@ -520,48 +521,113 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
     const double bj1 = j > 0 ? st.beta[j - 1] * st.qscale[j - 1] : 0.0;
     double b2 = 0.0;
     const int64_t nchunks = ldq / W;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nchunks;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = q * W;
-        double v[W];
-        load_src<V>(Q, ldq, r, from_r, j, aj, bj1, p, v);
-        V acc[W];
+    if constexpr (CG > 1) {
+        // small n (few chunks, long column sweeps): CG groups of 256 / CG threads share each
+        // chunk group, group g sweeping a contiguous 1/CG of the columns; the partial sums meet
+        // in shared memory and group 0 finishes the chunk
+        constexpr int T = 256 / CG;
+        using VT = typename VecT<V>::T;
+        __shared__ VT part[CG - 1][T];
+        const int grp = threadIdx.x / T, t = threadIdx.x % T;
+        const int per = (ncols + CG - 1) / CG;
+        const int cbeg = min(ncols, grp * per), cend = min(ncols, cbeg + per);
+        for (int64_t q0 = blockIdx.x * (int64_t)T; q0 < nchunks; q0 += (int64_t)gridDim.x * T) {
+            const int64_t q = q0 + t;
+            const bool live = q < nchunks;
+            const int64_t p = q * W;
+            V acc[W];
 #pragma unroll
-        for (int e = 0; e < W; ++e) acc[e] = V(0);
-        // columns are swept LAST to first: the dots pass streamed Q~ from column 0 up, so its
-        // last columns are the ones still in L2; the next step's dots pass starts at column
-        // 0, the one this pass reads last.
-        // batches of kUpdB columns: all kUpdB 16-byte loads are issued before the first FMA
-        // (same summation order as one column at a time)
-        const V* col = Q + (int64_t)(ncols - 1) * ldq + p;
-        int i = ncols - 1;
-        for (; i >= kUpdB - 1; i -= kUpdB) {
-            V a[kUpdB][W];
+            for (int e = 0; e < W; ++e) acc[e] = V(0);
+            if (live && cend > cbeg) {
+                const V* col = Q + (int64_t)(cend - 1) * ldq + p;
+                int i = cend - 1;
+                for (; i >= cbeg + kUpdB - 1; i -= kUpdB) {
+                    V a[kUpdB][W];
 #pragma unroll
-            for (int u = 0; u < kUpdB; ++u) vload<V>(col - (int64_t)u * ldq, a[u]);
+                    for (int u = 0; u < kUpdB; ++u) vload<V>(col - (int64_t)u * ldq, a[u]);
 #pragma unroll
-            for (int u = 0; u < kUpdB; ++u) {
-                const V ci = cfv[i - u];
+                    for (int u = 0; u < kUpdB; ++u) {
+                        const V ci = cfv[i - u];
 #pragma unroll
-                for (int e = 0; e < W; ++e) acc[e] += ci * a[u][e];
+                        for (int e = 0; e < W; ++e) acc[e] += ci * a[u][e];
+                    }
+                    col -= (int64_t)kUpdB * ldq;
+                }
+                for (; i >= cbeg; --i) {
+                    V a[W];
+                    vload<V>(col, a);
+                    const V ci = cfv[i];
+#pragma unroll
+                    for (int e = 0; e < W; ++e) acc[e] += ci * a[e];
+                    col -= ldq;
+                }
             }
-            col -= (int64_t)kUpdB * ldq;
-        }
-        for (; i >= 0; --i) {
-            V a[W];
-            vload<V>(col, a);
-            const V ci = cfv[i];
+            if (grp > 0) vstore<V>(reinterpret_cast<V*>(&part[grp - 1][t]), acc);
+            __syncthreads();
+            if (grp == 0 && live) {
 #pragma unroll
-            for (int e = 0; e < W; ++e) acc[e] += ci * a[e];
-            col -= ldq;
-        }
-        V o[W];
+                for (int h = 0; h < CG - 1; ++h) {
+                    V o2[W];
+                    vload<V>(reinterpret_cast<const V*>(&part[h][t]), o2);
 #pragma unroll
-        for (int e = 0; e < W; ++e) {
-            o[e] = (p + e < n) ? (V)(v[e] - (double)acc[e]) : V(0);
-            b2 += (double)o[e] * (double)o[e];
+                    for (int e = 0; e < W; ++e) acc[e] += o2[e];
+                }
+                double v[W];
+                load_src<V>(Q, ldq, r, from_r, j, aj, bj1, p, v);
+                V o[W];
+#pragma unroll
+                for (int e = 0; e < W; ++e) {
+                    o[e] = (p + e < n) ? (V)(v[e] - (double)acc[e]) : V(0);
+                    b2 += (double)o[e] * (double)o[e];
+                }
+                vstore<V>(Q + (int64_t)(j + 1) * ldq + p, o);
+            }
+            __syncthreads();
         }
-        vstore<V>(Q + (int64_t)(j + 1) * ldq + p, o);
+    } else {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nchunks;
+             q += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t p = q * W;
+            double v[W];
+            load_src<V>(Q, ldq, r, from_r, j, aj, bj1, p, v);
+            V acc[W];
+#pragma unroll
+            for (int e = 0; e < W; ++e) acc[e] = V(0);
+            // columns are swept LAST to first: the dots pass streamed Q~ from column 0 up, so its
+            // last columns are the ones still in L2; the next step's dots pass starts at column
+            // 0, the one this pass reads last.
+            // batches of kUpdB columns: all kUpdB 16-byte loads are issued before the first FMA
+            // (same summation order as one column at a time)
+            const V* col = Q + (int64_t)(ncols - 1) * ldq + p;
+            int i = ncols - 1;
+            for (; i >= kUpdB - 1; i -= kUpdB) {
+                V a[kUpdB][W];
+#pragma unroll
+                for (int u = 0; u < kUpdB; ++u) vload<V>(col - (int64_t)u * ldq, a[u]);
+#pragma unroll
+                for (int u = 0; u < kUpdB; ++u) {
+                    const V ci = cfv[i - u];
+#pragma unroll
+                    for (int e = 0; e < W; ++e) acc[e] += ci * a[u][e];
+                }
+                col -= (int64_t)kUpdB * ldq;
+            }
+            for (; i >= 0; --i) {
+                V a[W];
+                vload<V>(col, a);
+                const V ci = cfv[i];
+#pragma unroll
+                for (int e = 0; e < W; ++e) acc[e] += ci * a[e];
+                col -= ldq;
+            }
+            V o[W];
+#pragma unroll
+            for (int e = 0; e < W; ++e) {
+                o[e] = (p + e < n) ? (V)(v[e] - (double)acc[e]) : V(0);
+                b2 += (double)o[e] * (double)o[e];
+            }
+            vstore<V>(Q + (int64_t)(j + 1) * ldq + p, o);
+        }
     }
     if (beta2_out != nullptr) {
         b2 = block_sum(b2, red);
@@ -670,9 +736,18 @@ __global__ void stream_rc_kernel(RcStream rs) {
 }
 
 template <typename V>
+// launch of reorth_update_kernel<V, CG> for a runtime CG in {1, 2, 4}
+#define LOVE_UPDATE(V_, cg_, grid_, smem_, stream_, ...)                                                        \
+    do {                                                                                                        \
+        if ((cg_) == 4) LOVE_LAUNCH((reorth_update_kernel<V_, 4>), grid_, 256, smem_, stream_, __VA_ARGS__);     \
+        else if ((cg_) == 2) LOVE_LAUNCH((reorth_update_kernel<V_, 2>), grid_, 256, smem_, stream_, __VA_ARGS__);\
+        else LOVE_LAUNCH((reorth_update_kernel<V_, 1>), grid_, 256, smem_, stream_, __VA_ARGS__);               \
+    } while (0)
+
 struct StepPlan {
     Cache* c;
     int k, m, P, mean_y, gm, gu;
+    int ucg = 1;                  // column groups per CTA of the update (update_groups)
     bool fold;                    // single GPU: scalars in the update's last CTA, cache column in the gather
     RcStream rs;
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
@@ -737,7 +812,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0,
+            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0,
                         kUpdBeta | kUpdAdvance | kUpd1Sync, r, st, c.tol, 0, (const int*)nullptr);
         }
         {
@@ -755,7 +830,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         // q~_{j+1} against Q_j whose update finalises the step
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0, kUpdBeta | kUpd3T, r,
+            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0, kUpdBeta | kUpd3T, r,
                         st, c.tol, 1, (const int*)nullptr);
         }
         {
@@ -769,7 +844,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, 1,
+            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 1,
                         kUpdBeta | kUpdAdvance, r, st, c.tol, 1, (const int*)st.pro);
         }
         return;
@@ -786,7 +861,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_LAUNCH(reorth_update_kernel<V>, pl.gu, 256, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
+            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
                         pass == pl.P - 1 ? kUpdBeta | kUpdAdvance : 0, r, st, c.tol, pl.fold ? 1 : 0,
                         (const int*)nullptr);
         }
@@ -817,10 +892,11 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
                      pl.mean_y};
     pl.ldq = c.ldq;
     pl.gm = (int)std::min<int64_t>(ceil_div(pl.m, 256), 148 * 8);
-    pl.gu = update_grid<V>(c.ldq / VecT<V>::W, sizeof(double) * (pl.k + 1));
+    pl.ucg = update_groups(c.ldq / VecT<V>::W);
+    pl.gu = update_grid<V>(c.ldq / VecT<V>::W, sizeof(double) * (pl.k + 1), pl.ucg);
     pl.smu = sizeof(double) * (pl.k + 1);
     ensure_smem((const void*)reorth_dots_sweep_kernel<V, 1>, sizeof(double) * 8 * (pl.k + 1));
-    ensure_smem((const void*)reorth_update_kernel<V>, pl.smu);
+
     const LanczosState& st = c.st;
     {
         ProfScope ps(LOVE_PROF_SETUP, s);
@@ -1016,10 +1092,11 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
     ensure_smem((const void*)reorth_dots_sweep_kernel<double, 1>, smd);
     LOVE_LAUNCH((reorth_dots_sweep_kernel<double, 1>), dots_grid(ldq, 2, k), 256, smd, s, (const double*)Q, ldq,
                 k, pass, r, st, (const int*)nullptr);
-    const int gu = update_grid<double>(ldq / 2, sizeof(double) * (k + 1));
+    const int ucg = update_groups(ldq / 2);
+    const int gu = update_grid<double>(ldq / 2, sizeof(double) * (k + 1), ucg);
     const size_t smu = sizeof(double) * (k + 1);
-    ensure_smem((const void*)reorth_update_kernel<double>, smu);
-    LOVE_LAUNCH(reorth_update_kernel<double>, gu, 256, smu, s, Q, ldq, n, k, pass,
+
+    LOVE_UPDATE(double, ucg, gu, smu, s, Q, ldq, n, k, pass,
                 last_pass ? kUpdBeta | kUpdAdvance : 0, r, st, tol, 1, (const int*)nullptr);
 }
 
@@ -1028,22 +1105,39 @@ void launch_init_q0(const LanczosState& st, cudaStream_t s) { LOVE_LAUNCH(init_q
 // CTAs of the reorthogonalisation update for nchunks 16-byte chunks: one per chunk of 256
 // threads, capped at the CTAs resident on the GPU at once (a persistent grid-stride launch:
 // measured, cfg2 build 11.25 -> 10.95 ms against the 1.65-wave grid; LOVE_UPD_GRID overrides)
+// Column groups of the update for nchunks 16-byte chunks: small n runs few, long per-thread
+// column sweeps on few SMs; splitting the columns over 2 / 4 thread groups shortens them
+// (LOVE_UPD_CG overrides).  Measured: cfg5's sampling Lanczos (m = 10^4: 5000 chunks) and
+// main Lanczos (n = 10^5 fp64: 5 10^4 chunks); cfg2-4 (>= 1.25 10^5 chunks) keep one group.
+int update_groups(int64_t nchunks) {
+    if (const char* e = std::getenv("LOVE_UPD_CG")) {
+        const int v = std::atoi(e);
+        return v == 2 || v == 4 ? v : 1;
+    }
+    return nchunks <= 16384 ? 4 : nchunks <= 65536 ? 2 : 1;
+}
+
+// CTAs of the update: one per 256 / cg chunks, capped at the CTAs resident on the GPU at once
+// (a persistent grid-stride launch: measured, cfg2 build 11.25 -> 10.95 ms against the
+// 1.65-wave grid; LOVE_UPD_GRID overrides).  Also raises the kernel's shared-memory limit.
 template <typename V>
-int update_grid(int64_t nchunks, size_t smem) {
+int update_grid(int64_t nchunks, size_t smem, int cg) {
+    const void* fn = cg == 4 ? (const void*)reorth_update_kernel<V, 4>
+                   : cg == 2 ? (const void*)reorth_update_kernel<V, 2> : (const void*)reorth_update_kernel<V, 1>;
+    ensure_smem(fn, smem);
     int cap = 0;
     if (const char* e = std::getenv("LOVE_UPD_GRID")) cap = std::atoi(e);
     if (cap <= 0) {
         int dev = 0, sms = 0, per = 0;
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
         cuda_check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
-        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, reorth_update_kernel<V>, 256, smem),
-                   "update occupancy");
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 256, smem), "update occupancy");
         cap = std::max(1, sms * per);
     }
-    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nchunks, 256), cap));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nchunks, 256 / cg), cap));
 }
-template int update_grid<float>(int64_t, size_t);
-template int update_grid<double>(int64_t, size_t);
+template int update_grid<float>(int64_t, size_t, int);
+template int update_grid<double>(int64_t, size_t, int);
 
 // ---- ReplayThrottle (love_internal.h).  Per (thread, device): one mapped host int and a ring
 // of kReplayWindow events, created once.

@@ -436,7 +436,16 @@ __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ 
     double a = 0.0;
     if (r < m) {
         double acc = 0.0;
-        for (int c = 0; c < k_eff; ++c) acc += Rc[(int64_t)c * m + r] * ts[c];
+        // four partial sums: the column loads of a row are independent, keep 8 in flight
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+        int c = 0;
+#pragma unroll 2
+        for (; c + 4 <= k_eff; c += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a4[u] += Rc[(int64_t)(c + u) * m + r] * ts[c + u];
+        }
+        for (; c < k_eff; ++c) a4[0] += Rc[(int64_t)c * m + r] * ts[c];
+        acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
         const double vr = z[r] - acc;
         v[r] = vr;
         a = qcur[r] * vr;

@@ -11,6 +11,7 @@
 //  * gather: one thread per item loads the 4^d z values of its cell's stencil once and
 //    reuses them for every point of the item.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <type_traits>
 
 #include "love_internal.h"

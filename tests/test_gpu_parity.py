@@ -541,3 +541,31 @@ def test_block_queries_cooperative_equal_per_thread(ci, n, m, prior, monkeypatch
     ok = ~np.isnan(v2)
     np.testing.assert_allclose(v[ok], v2[ok], rtol=1e-10, atol=1e-14)
     np.testing.assert_allclose(mu[ok], mu2[ok], rtol=1e-10, atol=1e-14)
+
+
+def test_cache_precision_options():
+    """love_opts.cache_fp64 (reading A12b): ON gives an fp64 cache behind fp32 outputs (the
+    operator and export dtypes follow the cache), OFF keeps fp32 even after a breakdown, ON
+    with precision fp64 is an argument error; an fp32 problem that does not break down is not
+    rebuilt under AUTO."""
+    LoveCache, LoveError = _love()
+    p = scaled_config(2, n=20_011, m=(2000,), k=20, t=501)
+    inp = make_inputs(p)
+    auto = _build(p, inp)
+    assert auto.info()["k_eff"] == 20 and auto.info()["cache_precision"] == 0
+    on = _build(p, inp, cache_fp64=True)
+    i_on = on.info()
+    assert i_on["precision"] == 0 and i_on["cache_precision"] == 1
+    assert on.predict_var(inp.Xs).dtype == torch.float32
+    assert on.export("rc").dtype == torch.float64
+    v = np.random.default_rng(0).normal(size=p.n)
+    mv = on.ski_mvm(torch.tensor(v, dtype=torch.float64, device="cuda"))
+    assert mv.dtype == torch.float64
+    np.testing.assert_allclose(mv.cpu().numpy(), O.ski_mvm(_model(p, inp), v), rtol=1e-11, atol=1e-11)
+    with pytest.raises(LoveError) as e:
+        _build(p, inp, precision="fp64", cache_fp64=True)
+    assert e.value.status == 1
+    # the fp64-cache variances equal the LOVE_FP64 build's, rounded to fp32
+    f64 = _build(p, inp, precision="fp64")
+    np.testing.assert_allclose(on.predict_var(inp.Xs).cpu().numpy(), f64.predict_var(inp.Xs).cpu().numpy(),
+                               rtol=1e-6)
