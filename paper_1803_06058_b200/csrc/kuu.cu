@@ -190,7 +190,7 @@ __global__ void fft_small_kernel(const double* __restrict__ u, const double* __r
 }
 
 // ---- four-step pass A: for each n1, FFT over n2 of x[n1 + N1 n2], times w_N^{n1 k2}
-template <int G>
+template <int G, int EPT>
 __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
                                  const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y, const int* __restrict__ done) {
     pdl_wait();
@@ -202,16 +202,17 @@ __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __r
     const int n1_0 = blockIdx.x * G;
     const int N = N1 * N2;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n2 = t / G;
         const int idx = n1_0 + g + N1 * n2;
         buf[pad(g * N2 + n2)] = make_double2(idx < m ? u_at(u, Mc, m, idx) : 0.0, 0.0);
     }
     __syncthreads();
-    line_fft<-1>(buf, N2, tws);
+    if (EPT == 4) line_fft4<-1>(buf, N2, tws);
+    else line_fft<-1>(buf, N2, tws);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N2, k2 = t % N2;
         const int n1 = n1_0 + g;
@@ -222,7 +223,7 @@ __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __r
 // ---- four-step pass B: for each k2, FFT over n1 -> X[N2 k1 + k2];
 // mode 0: times lamB[k2*N1 + k1], inverse FFT over k1, times w_N^{-n1 k2}, store back
 // mode 1: store X in natural order into outc
-template <int G>
+template <int G, int EPT>
 __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __restrict__ tw1,
                                  const C* __restrict__ tw2, const C* __restrict__ twF,
                                  const double* __restrict__ lamB, C* __restrict__ outc, int mode, const int* __restrict__ done) {
@@ -235,16 +236,17 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
     const int k2_0 = blockIdx.x * G;
     const int N = N1 * N2;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n1 = t / G;
         buf[pad(g * N1 + n1)] = Y[(int64_t)n1 * N2 + k2_0 + g];
     }
     __syncthreads();
-    line_fft<-1>(buf, N1, tws);
+    if (EPT == 4) line_fft4<-1>(buf, N1, tws);
+    else line_fft<-1>(buf, N1, tws);
     if (mode == 1) {
     #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
             const int g = t % G, k1 = t / G;
             outc[(int64_t)N2 * k1 + k2_0 + g] = buf[pad(g * N1 + k1)];
@@ -252,7 +254,7 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
         return;
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N1, k1 = t % N1;
         const double l = lamB[(int64_t)(k2_0 + g) * N1 + k1];
@@ -260,9 +262,10 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
         buf[pad(t)].y *= l;
     }
     __syncthreads();
-    line_fft<+1>(buf, N1, tws);
+    if (EPT == 4) line_fft4<+1>(buf, N1, tws);
+    else line_fft<+1>(buf, N1, tws);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n1 = t / G;
         const int k2 = k2_0 + g;
@@ -271,7 +274,7 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
 }
 
 // ---- four-step pass C: for each n1, inverse FFT over k2; z[n1 + N1 n2] = Re(.)
-template <int G>
+template <int G, int EPT>
 __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
                                  double* __restrict__ z, const int* __restrict__ done) {
     pdl_wait();
@@ -282,15 +285,16 @@ __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2,
     load_tw(tws, tw2, N2);
     const int n1_0 = blockIdx.x * G;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t / N2, k2 = t % N2;
         buf[pad(t)] = Y[(int64_t)(n1_0 + g) * N2 + k2];
     }
     __syncthreads();
-    line_fft<+1>(buf, N2, tws);
+    if (EPT == 4) line_fft4<+1>(buf, N2, tws);
+    else line_fft<+1>(buf, N2, tws);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {               // exactly 8 elements per thread
+    for (int e = 0; e < EPT; ++e) {             // exactly EPT elements per thread
         const int t = threadIdx.x + e * blockDim.x;
         const int g = t % G, n2 = t / G;
         const int idx = n1_0 + g + N1 * n2;
@@ -663,7 +667,7 @@ constexpr int kLinesPerCta = 2;
 
 // convolution (mode 0) of u (m entries) or forward FFT (mode 1) of u (N entries)
 // complex four-step passes with G lines per CTA (mode 0: convolution, mode 1: forward only)
-template <int G>
+template <int G, int EPT>
 static void fft_four_step(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc,
                           int mode, cudaStream_t s) {
     const int N1 = c.fft_N1, N2 = c.fft_N2;
@@ -672,12 +676,14 @@ static void fft_four_step(const Cache& c, const double* u, const double* Mc, int
     const C* twF = (const C*)c.twF;
     const double* lam = (const double*)c.lam;
     const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
-    ensure_smem((const void*)fft_passA_kernel<G>, smA);
-    ensure_smem((const void*)fft_passB_kernel<G>, smB);
-    ensure_smem((const void*)fft_passC_kernel<G>, smA);
-    LOVE_LAUNCH(fft_passA_kernel<G>, N1 / G, G * N2 / 8, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
-    LOVE_LAUNCH(fft_passB_kernel<G>, N2 / G, G * N1 / 8, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode, t_done);
-    if (mode == 0) LOVE_LAUNCH(fft_passC_kernel<G>, N1 / G, G * N2 / 8, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
+    ensure_smem((const void*)fft_passA_kernel<G, EPT>, smA);
+    ensure_smem((const void*)fft_passB_kernel<G, EPT>, smB);
+    ensure_smem((const void*)fft_passC_kernel<G, EPT>, smA);
+    LOVE_LAUNCH((fft_passA_kernel<G, EPT>), N1 / G, G * N2 / EPT, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
+    LOVE_LAUNCH((fft_passB_kernel<G, EPT>), N2 / G, G * N1 / EPT, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode,
+                t_done);
+    if (mode == 0)
+        LOVE_LAUNCH((fft_passC_kernel<G, EPT>), N1 / G, G * N2 / EPT, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
 }
 
 void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc, int mode,
@@ -709,8 +715,18 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
     }
     // measured: 4 lines per CTA (16-byte loads in 64-byte runs) win at N <= 2^15 (cfg5 build
     // 6.11 -> 5.97 ms), 2 lines (twice the CTAs) at 2^17; 1 line loses everywhere
-    if (N <= (1 << 15)) fft_four_step<4>(c, u, Mc, m, z, work, outc, mode, s);
-    else fft_four_step<G>(c, u, Mc, m, z, work, outc, mode, s);
+    // 4 elements per thread (radix-4 stages, twice the threads per CTA) for the convolution
+    // passes of the Lanczos (LOVE_FFT_EPT=8: radix-8); the one-off forward transform of the
+    // setup keeps radix 8
+    static const int ept = std::getenv("LOVE_FFT_EPT") ? std::atoi(std::getenv("LOVE_FFT_EPT")) : 4;
+    const bool e4 = ept == 4 && mode == 0;
+    if (N <= (1 << 15)) {
+        if (e4) fft_four_step<4, 4>(c, u, Mc, m, z, work, outc, mode, s);
+        else fft_four_step<4, 8>(c, u, Mc, m, z, work, outc, mode, s);
+    } else {
+        if (e4) fft_four_step<G, 4>(c, u, Mc, m, z, work, outc, mode, s);
+        else fft_four_step<G, 8>(c, u, Mc, m, z, work, outc, mode, s);
+    }
 }
 
 void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {

@@ -27,7 +27,7 @@ namespace {
 constexpr int kMaxKs = 112;          // k' limit of the single-CTA Jacobi eigensolver (smem)
 
 // out[c] += sum_r A[r + c*lda] * x[r], c < ncol   (fp64, CTA row tiles, warps own columns)
-constexpr int kDotRows = 128;       // rows per CTA tile of dots_kernel (~m/128 CTAs)
+constexpr int kDotRows = 64;        // rows per CTA tile of dots_kernel (~m/64 CTAs)
 __global__ void __launch_bounds__(256) dots_kernel(const double* __restrict__ A, int64_t lda, int nrow, int ncol,
                                                    const double* __restrict__ x, double* __restrict__ out,
                                                    const int* __restrict__ stop) {
@@ -421,37 +421,41 @@ __global__ void samp_qcur_kernel(LanczosState st, const double* __restrict__ Q, 
         for (int i = threadIdx.x; i < kt; i += blockDim.x) t[i] = 0.0;
 }
 
-// v = z - Rc t (t = Rc^T q_j) and alpha_j += q_j . v   (fp64)
+// v = z - Rc t (t = Rc^T q_j) and alpha_j += q_j . v   (fp64).  A CTA owns 32 rows; its 8
+// warps split the k_eff columns (lanes over the rows: coalesced column reads), the partial sums
+// meet in shared memory.  (One thread per row looping over every column left the kernel on 40
+// SMs with a 49-load chain per thread.)
+constexpr int kSvRows = 32;
 __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ Rc, int m, int k_eff,
                                                      const double* __restrict__ z, const double* __restrict__ t,
                                                      const double* __restrict__ qcur, double* __restrict__ v,
                                                      LanczosState st) {
-    extern __shared__ double ts[];               // [k_eff]
+    __shared__ double psum[8][kSvRows];
     __shared__ double red[32];
     pdl_wait();
     if (st.flags[0]) return;
-    for (int i = threadIdx.x; i < k_eff; i += blockDim.x) ts[i] = t[i];
-    __syncthreads();
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    double a = 0.0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r = blockIdx.x * kSvRows + lane;
+    double acc = 0.0;
     if (r < m) {
-        double acc = 0.0;
-        // four partial sums: the column loads of a row are independent, keep 8 in flight
-        double a4[4] = {0.0, 0.0, 0.0, 0.0};
-        int c = 0;
-#pragma unroll 2
-        for (; c + 4 <= k_eff; c += 4) {
+        for (int c = wid; c < k_eff; c += 8) acc += Rc[(int64_t)c * m + r] * __ldg(&t[c]);
+    }
+    psum[wid][lane] = acc;
+    __syncthreads();
+    double a = 0.0;
+    if (wid == 0 && r < m) {
+        double tot = 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) a4[u] += Rc[(int64_t)(c + u) * m + r] * ts[c + u];
-        }
-        for (; c < k_eff; ++c) a4[0] += Rc[(int64_t)c * m + r] * ts[c];
-        acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
-        const double vr = z[r] - acc;
+        for (int w = 0; w < 8; ++w) tot += psum[w][lane];
+        const double vr = z[r] - tot;
         v[r] = vr;
         a = qcur[r] * vr;
     }
-    a = block_sum(a, red);
-    if (threadIdx.x == 0) atomicAdd(st.alpha_cur, a);
+    if (wid == 0) {
+        a = warp_sum(a);
+        if (lane == 0) atomicAdd(st.alpha_cur, a);
+    }
+    (void)red;
 }
 
 __global__ void fill_ones_kernel(double* __restrict__ v, int m) {
@@ -704,14 +708,13 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         cuda_check(cudaMemcpyAsync(st.flags, f, sizeof(f), cudaMemcpyHostToDevice, s), "sampling flags");
     }
     const double tol = 1e-10;
-    const int gm = (int)ceil_div(m, 256), gd = (int)ceil_div(m, kDotRows);
+    const int gm = (int)ceil_div(m, kSvRows), gd = (int)ceil_div(m, kDotRows);
     const int gq = (int)std::min<int64_t>(ceil_div(m, 256), 148 * 4);
-    ensure_smem((const void*)samp_v_kernel, sizeof(double) * std::max(k, 1));
     // probe b' = M 1 (reading A14) into Q~[:, 0]
     LOVE_LAUNCH(fill_ones_kernel, gq, 256, 0, s, qcur, m);
     launch_kuu(c, qcur, z, s);
     LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, t, (const int*)nullptr);
-    LOVE_LAUNCH(samp_v_kernel, gm, 256, sizeof(double) * std::max(k, 1), s, Rc, m, k, z, t, qcur, Qp, st);
+    LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, t, qcur, Qp, st);
     LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Qp, ldq, m, 1, Qp, st.bnorm2, (const int*)nullptr);
     cuda_check(cudaMemsetAsync(st.alpha_cur, 0, sizeof(double), s), "alpha clear");
     launch_init_q0(st, s);
@@ -723,7 +726,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
             launch_kuu(c, qcur, z, s);
         }
         LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, t, st.flags);
-        LOVE_LAUNCH(samp_v_kernel, gm, 256, sizeof(double) * std::max(k, 1), s, Rc, m, k, z, t, qcur, v, st);
+        LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, t, qcur, v, st);
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 0, 0, v, tol, s);
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 1, 1, v, tol, s);
     };

@@ -100,6 +100,18 @@ def test_cfg4_full_size_vs_oracle_fixture():
     # the mean is a Krylov solve (Eq. 3) at k = 100, far from converged at cfg4: fp32 vs fp64
     # Lanczos drift sets its error ("mean parity"), ~2e-3 of max|mean|
     assert np.max(np.abs(mg - d["mean"])) < 5e-3 * np.abs(d["mean"]).max()
+    c.free()
+    # the same build with fp64 factors (cache_fp64, reading A12b) follows the oracle's Krylov
+    # path: variances and means to the fp32 rounding of the outputs -- the fp32 mean error above
+    # is the fp32 Lanczos, not a defect of the cache or the query
+    c64 = _build(p, inp, cache_fp64=True)
+    assert c64.info()["k_eff"] == int(d["k_eff"]) and c64.info()["cache_precision"] == 1
+    v64, m64 = (x.cpu().numpy().astype(np.float64) for x in c64.predict_var(torch.from_numpy(d["Xs"]).cuda(),
+                                                                              return_mean=True))
+    rel = np.abs(v64 - d["var"]) / np.abs(d["var"])
+    print(f"cfg4 fp64 cache: max rel {rel.max():.3e}, mean err {np.max(np.abs(m64 - d['mean'])):.3e}")
+    assert rel.max() <= 1e-5
+    assert np.max(np.abs(m64 - d["mean"])) <= 1e-5 * np.abs(d["mean"]).max()
 
 
 def test_full_size_cfg6_additive():
