@@ -155,6 +155,7 @@ __device__ __forceinline__ double u_at(const double* __restrict__ u, const doubl
 }
 
 // ---- single-CTA convolution (mode 0) / forward transform (mode 1), N <= 4096
+template <int EPT>
 __global__ void fft_small_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N,
                                  const C* __restrict__ tw, const double* __restrict__ lam, double* __restrict__ z,
                                  C* __restrict__ outc, int mode, const int* __restrict__ done) {
@@ -164,27 +165,31 @@ __global__ void fft_small_kernel(const double* __restrict__ u, const double* __r
     C* tws = (C*)smraw;
     C* buf = tws + N;
     load_tw(tws, tw, N);
+    double lv[EPT];                             // data-independent: loaded before the transform
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EPT; ++e) lv[e] = mode == 1 ? 0.0 : __ldg(&lam[threadIdx.x + e * blockDim.x]);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
         const int i = threadIdx.x + e * blockDim.x;
         buf[pad(i)] = make_double2(i < m ? u_at(u, Mc, m, i) : 0.0, 0.0);
     }
     __syncthreads();
-    line_fft<-1>(buf, N, tws);
+    if (EPT == 4) line_fft4<-1>(buf, N, tws);
+    else line_fft<-1>(buf, N, tws);
     if (mode == 1) {
         #pragma unroll 8
         for (int i = threadIdx.x; i < N; i += blockDim.x) outc[i] = buf[pad(i)];
         return;
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < EPT; ++e) {
         const int i = threadIdx.x + e * blockDim.x;
-        const double l = lam[i];
-        buf[pad(i)].x *= l;
-        buf[pad(i)].y *= l;
+        buf[pad(i)].x *= lv[e];
+        buf[pad(i)].y *= lv[e];
     }
     __syncthreads();
-    line_fft<+1>(buf, N, tws);
+    if (EPT == 4) line_fft4<+1>(buf, N, tws);
+    else line_fft<+1>(buf, N, tws);
     #pragma unroll 8
     for (int i = threadIdx.x; i < m; i += blockDim.x) z[i] = buf[pad(i)].x;
 }
@@ -693,8 +698,15 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
     const double* lam = (const double*)c.lam;
     if (N1 == 0) {
         const size_t sm = sizeof(C) * (padded(N) + N);
-        ensure_smem((const void*)fft_small_kernel, sm);
-        LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, N / 8), sm, s, u, Mc, m, N, tw1, lam, z, outc, mode, t_done);
+        static const int ept = std::getenv("LOVE_FFT_EPT") ? std::atoi(std::getenv("LOVE_FFT_EPT")) : 4;
+        if (ept == 4 && mode == 0 && N >= 8 && N / 4 <= 1024) {
+            ensure_smem((const void*)fft_small_kernel<4>, sm);
+            LOVE_LAUNCH(fft_small_kernel<4>, 1, N / 4, sm, s, u, Mc, m, N, tw1, lam, z, outc, mode, t_done);
+        } else {
+            ensure_smem((const void*)fft_small_kernel<8>, sm);
+            LOVE_LAUNCH(fft_small_kernel<8>, 1, std::max(1, N / 8), sm, s, u, Mc, m, N, tw1, lam, z, outc, mode,
+                        t_done);
+        }
         return;
     }
     constexpr int G = kLinesPerCta;
@@ -815,8 +827,8 @@ void setup_kuu(Cache& c, cudaStream_t s) {
                 cuda_check(cudaMallocAsync((void**)&X, sizeof(C) * Nd, s), "axis lam alloc");
                 LOVE_LAUNCH(embed_kernel, (int)ceil_div(Nd, 256), 256, 0, s, c.cols64 + off, md, Nd, colN);
                 const size_t sm = sizeof(C) * (padded(Nd) + Nd);
-                ensure_smem((const void*)fft_small_kernel, sm);
-                LOVE_LAUNCH(fft_small_kernel, 1, std::max(1, Nd / 8), sm, s, colN, (const double*)nullptr, Nd, Nd,
+                ensure_smem((const void*)fft_small_kernel<8>, sm);
+                LOVE_LAUNCH(fft_small_kernel<8>, 1, std::max(1, Nd / 8), sm, s, colN, (const double*)nullptr, Nd, Nd,
                             (const C*)c.ax_tw[d], (const double*)nullptr, (double*)nullptr, X, 1, t_done);
                 LOVE_LAUNCH(lambda_store_kernel, (int)ceil_div(Nd, 256), 256, 0, s, X, Nd, 0, 0, 0, 1.0 / (double)Nd,
                             (double*)c.ax_lam[d]);
