@@ -15,6 +15,11 @@
 
 #include "love_internal.h"
 #include "ski_device.cuh"
+#include "tma.cuh"
+
+#ifndef LOVE_SORTED3_TMA
+#define LOVE_SORTED3_TMA 1
+#endif
 
 #ifndef LOVE_PAIRED_Q3
 #define LOVE_PAIRED_Q3 1
@@ -680,6 +685,26 @@ __device__ __forceinline__ double sorted3_mean(const Stencil& A, const double* _
 
 // Queries counting-sorted by cell (SURVEY 8(f) NEXT #3a): a CTA stages the 64 stencil rows of
 // cp.async of the 64 stencil rows of cell c (k_pad values each) into dst, one commit group
+// TMA: the 64 rows are 16 runs of 4 consecutive nodes along the last axis, each run
+// 4 k_pad contiguous values of the row-major Rc -- one cp.async.bulk per run, issued by one
+// thread, completing on the buffer's mbarrier (expect_tx of the 64 rows' bytes)
+template <typename V>
+__device__ __forceinline__ void stage_rows3_tma(const GridDev& g, const V* __restrict__ Rc, int k_pad, int c, V* dst,
+                                                uint64_t* bar) {
+    if (threadIdx.x != 0) return;
+    // the buffer was last read through the generic proxy (ordered by the __syncthreads that
+    // ended that cell): order those reads before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    const int base = c - g.stride[0] - g.stride[1] - 1;
+    const unsigned run = 4u * (unsigned)k_pad * (unsigned)sizeof(V);
+    mbar_expect_tx(bar, 16u * run);
+#pragma unroll
+    for (int ab = 0; ab < 16; ++ab) {
+        const int node = base + (ab >> 2) * g.stride[0] + (ab & 3) * g.stride[1];
+        bulk_g2s(dst + (size_t)ab * 4 * k_pad, Rc + (int64_t)node * k_pad, run, bar);
+    }
+}
+
 template <typename V>
 __device__ __forceinline__ void stage_rows3(const GridDev& g, const V* __restrict__ Rc, int k_pad, int nch, int c,
                                             V* dst) {
@@ -697,6 +722,7 @@ __device__ __forceinline__ void stage_rows3(const GridDev& g, const V* __restric
 // query, every lane reading the same row chunk (a shared-memory broadcast feeds 32 queries);
 // sparser cells: a warp per query, lanes over 16-byte chunks of k.
 constexpr int kLanePerQuery = 16;
+constexpr bool kSorted3Tma = LOVE_SORTED3_TMA;   // row staging by cp.async.bulk (else per-thread cp.async)
 
 template <typename V>
 __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
@@ -721,16 +747,33 @@ __global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, 
     const int m = g.m_total;
     const int c_begin = blockIdx.x * cells_per_cta;
     const int c_end = min(m, c_begin + cells_per_cta);
+    __shared__ __align__(8) uint64_t bars[2];                   // TMA completion, one per buffer
+    unsigned phase[2] = {0u, 0u};
+    if (kSorted3Tma && threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_init_fence();
+    }
+    if (kSorted3Tma) __syncthreads();
     int c = c_begin;
     while (c < c_end && qstart[c] == qstart[c + 1]) ++c;        // first cell with queries
-    if (c < c_end) stage_rows3<V>(g, Rc, k_pad, nch, c, rows0);
+    if (c < c_end) {
+        if (kSorted3Tma) stage_rows3_tma<V>(g, Rc, k_pad, c, rows0, &bars[0]);
+        else stage_rows3<V>(g, Rc, k_pad, nch, c, rows0);
+    }
     int buf = 0;
     while (c < c_end) {
         int cn = c + 1;
         while (cn < c_end && qstart[cn] == qstart[cn + 1]) ++cn;
-        if (cn < c_end) stage_rows3<V>(g, Rc, k_pad, nch, cn, rows0 + (buf ^ 1) * bstride);
-        if (cn < c_end) __pipeline_wait_prior(1);                // this cell's rows have landed
-        else __pipeline_wait_prior(0);
+        if (kSorted3Tma) {
+            if (cn < c_end) stage_rows3_tma<V>(g, Rc, k_pad, cn, rows0 + (buf ^ 1) * bstride, &bars[buf ^ 1]);
+            mbar_wait(&bars[buf], phase[buf]);                  // this cell's rows have landed
+            phase[buf] ^= 1u;
+        } else {
+            if (cn < c_end) stage_rows3<V>(g, Rc, k_pad, nch, cn, rows0 + (buf ^ 1) * bstride);
+            if (cn < c_end) __pipeline_wait_prior(1);            // this cell's rows have landed
+            else __pipeline_wait_prior(0);
+        }
         __syncthreads();
         const V* rows = rows0 + buf * bstride;
         const int p0 = qstart[c], p1 = qstart[c + 1];
