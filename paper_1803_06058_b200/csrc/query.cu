@@ -724,8 +724,11 @@ __device__ __forceinline__ void stage_rows3(const GridDev& g, const V* __restric
 constexpr int kLanePerQuery = 16;
 constexpr bool kSorted3Tma = LOVE_SORTED3_TMA;   // row staging by cp.async.bulk (else per-thread cp.async)
 
+#ifndef LOVE_SORTED3_MINB
+#define LOVE_SORTED3_MINB 4   // measured: 1 CTA per SM at 168 registers 5.5 ms, 3 CTAs 3.24 ms, 4 CTAs (64 registers, small spills) 3.15 ms per 4e6 queries
+#endif
 template <typename V>
-__global__ void __launch_bounds__(256) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
+__global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
                                                               double l2, int prior_mode, const V* __restrict__ Rc,
                                                               int k_pad, const double* __restrict__ amean,
                                                               const double* __restrict__ Xs,

@@ -36,8 +36,25 @@ constexpr bool kPaired3 = LOVE_PAIRED3;   // 3-D fp32 moments on FFMA2 pairs
 // (cfg4 gather 3.98 -> 4.19 ms per build): off
 constexpr bool kPairedGather3 = false;
 
+// minimum resident CTAs per SM for the 3-D item kernels (0: the compiler's choice)
+#ifndef LOVE_MOM3_MINB
+#define LOVE_MOM3_MINB 0
+#endif
+#ifndef LOVE_GATHER3_MINB
+#define LOVE_GATHER3_MINB 0
+#endif
+#if LOVE_MOM3_MINB > 0
+#define LOVE_MOM_BOUNDS(D) __launch_bounds__(256, (D) == 3 ? LOVE_MOM3_MINB : 1)
+#else
+#define LOVE_MOM_BOUNDS(D) __launch_bounds__(256)
+#endif
+#if LOVE_GATHER3_MINB > 0
+#define LOVE_GATHER_BOUNDS(D) __launch_bounds__(256, (D) == 3 ? LOVE_GATHER3_MINB : 1)
+#else
+#define LOVE_GATHER_BOUNDS(D) __launch_bounds__(256)
+#endif
 template <typename V, int D, typename MT>
-__global__ void __launch_bounds__(256) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
+__global__ void LOVE_MOM_BOUNDS(D) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
                                                       const V* __restrict__ f0, const V* __restrict__ f1,
                                                       const V* __restrict__ f2, const V* __restrict__ qbase,
                                                       StepRef ref, MT* __restrict__ M) {
@@ -253,7 +270,7 @@ __global__ void __launch_bounds__(256) nodepass_kernel(GridDev g, int64_t n_item
 }
 
 template <typename V, int D>
-__global__ void __launch_bounds__(256) gather_kernel(GridDev g, int64_t n_items,
+__global__ void LOVE_GATHER_BOUNDS(D) gather_kernel(GridDev g, int64_t n_items,
                                                      const int* __restrict__ item_cell,
                                                      const int* __restrict__ item_start,
                                                      const V* __restrict__ f0, const V* __restrict__ f1,
