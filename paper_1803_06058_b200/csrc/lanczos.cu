@@ -975,11 +975,21 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         cudaGraph_t g = nullptr;
         cudaGraphExec_t ge = nullptr;
         const int64_t before = g_launch_count.load();      // captured launches run once per replay
+        host_mark("pre_capture");
         cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
         enqueue_step<V>(pl, 0, s);
         enqueue_step<V>(pl, 1, s);
         cuda_check(cudaStreamEndCapture(s, &g), "end capture");
-        cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+        host_mark("capture");
+        // one GPU: the exec is cached across builds of the same shape (several GPUs: the graph
+        // holds NCCL kernels of a per-build communicator, instantiated fresh)
+        const bool cache_ge = c.comm == nullptr;
+        const std::string key = "lanczos/" + std::to_string(sizeof(V)) + "/" + std::to_string(c.g.d) + "/" +
+                                std::to_string(pl.P) + "/" + std::to_string((int)pl.partial) + "/" +
+                                std::to_string((int)pl.mfuse) + "/" + std::to_string(pl.ucg);
+        if (cache_ge) ge = graph_exec_cached(g, key);
+        else cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+        host_mark("instantiate");
         const int64_t nodes = g_launch_count.load() - before;
         g_launch_count -= nodes;
         // replays past a breakdown would only run early-exiting kernels: the host stops as soon
@@ -995,7 +1005,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
             if (thr != nullptr) thr->launched(i, s);
         }
         if ((pl.k & 1) && !stop) enqueue_step<V>(pl, pl.k - 1, s);
-        cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
+        if (!cache_ge) cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
         cuda_check(cudaGraphDestroy(g), "graph destroy");
     } else {
         for (int j = 0; j < pl.k; ++j) enqueue_step<V>(pl, j, s);

@@ -251,8 +251,10 @@ Cache* begin_build(const love_opts& o, double sigma2, int64_t n_local, int32_t& 
             nccl_comm_init(*c, dist->nccl_unique_id);
         }
         TempPool tmp(s);
-        // global n (k <= n_global)
-        {
+        // global n (k <= n_global); one GPU: the local n, no round trip
+        if (c->comm == nullptr) {
+            c->n_global = c->n;
+        } else {
             int64_t* dn = (int64_t*)tmp.get(sizeof(int64_t));
             cuda_check(cudaMemcpyAsync(dn, &c->n, sizeof(int64_t), cudaMemcpyHostToDevice, s), "n h2d");
             allreduce_sum_i64(*c, dn, 1, s);
@@ -338,11 +340,13 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (c->fused) setup_fused(*c, s);
     if (c->fused) run_lanczos_fused(*c, s);
     else run_lanczos(*c, s);
+    host_mark("lanczos_enqueued");
     int hfl[8];
     double bn2 = 0;
     cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
     cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
     cuda_check(cudaStreamSynchronize(s), "lanczos sync");
+    host_mark("lanczos_sync");
     cuda_check(cudaGetLastError(), "lanczos kernels");
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
     if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
@@ -402,6 +406,7 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
     cudaStream_t s = nullptr;
     try {
         if (out) *out = nullptr;
+        host_mark("start");
         validate_build(grid, rbf, sigma2, X, y, n_local, k, out);
         int dev = 0;
         cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
@@ -438,14 +443,15 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
         for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * (c->ldq + 4), s);   // padded to 16 B units
         if (g.d <= 2 && !c->fused) c->pcell = (int*)dalloc(*c, sizeof(int) * (c->ldq + 4), s);
         c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        host_mark("begin_build");
         prof_begin(LOVE_PROF_SETUP, s);
         launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);
-        {   // the range check is global: every rank must agree before continuing
+        if (c->comm != nullptr) {   // the range check is global: every rank must agree before continuing
             float fl = 0.f;
             int hflag = 0;
             cuda_check(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
             cuda_check(cudaStreamSynchronize(s), "sync");
-            if (c->comm != nullptr) {
+            {
                 float* df = (float*)tmp.get(sizeof(float));
                 fl = (float)hflag;
                 cuda_check(cudaMemcpyAsync(df, &fl, sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
@@ -460,7 +466,15 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
         // for the mean cache (Eq. 4) and column 0 is filled below
         if (c->probe == LOVE_PROBE_AVGCOL) c->ysort = dalloc(*c, vs * c->ldq, s);
         launch_counting_sort(*c, cell, frac64, y, c->n, c->probe == LOVE_PROBE_Y ? c->Q : c->ysort, s);
+        host_mark("interp+range_sync");
+        // one GPU: the range flag comes back with the item count (one synchronisation; a point
+        // off the grid was given cell 0, so the sort above stayed in bounds)
+        int hrange = 0;
+        if (c->comm == nullptr)
+            cuda_check(cudaMemcpyAsync(&hrange, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
         c->n_items = count_items_host(*c, s);
+        if (hrange) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
+        host_mark("sort+items_sync");
         c->item_cell = (int*)dalloc(*c, sizeof(int) * (c->n_items + 8), s);     // padded: staged in 16 B units
         c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
         launch_build_items(*c, s);
@@ -475,7 +489,10 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
         setup_kuu(*c, s);
         prof_end(LOVE_PROF_SETUP, s);
 
+        host_mark("setup_kuu");
         finish_build(c, o, k, s);
+        host_mark("finish");
+        host_marks_flush();
         *out = reinterpret_cast<love_cache*>(c);
         return LOVE_OK;
     } catch (...) {

@@ -311,6 +311,14 @@ void build_sampling_cache(Cache& c, cudaStream_t s);
 template <typename V> void launch_sample(const Cache& c, const double* Xs, int64_t t, int64_t ns,
                                          uint64_t seed, const double* zeta, V* out,
                                          cudaStream_t s);
+// Instantiated step graphs kept across builds (per thread, keyed by purpose + shape): a build
+// whose freshly captured graph has the topology of a cached one refreshes it with
+// cudaGraphExecUpdate (new buffer pointers) instead of instantiating again.  The returned exec
+// is owned by the cache (do not destroy it).
+cudaGraphExec_t graph_exec_cached(cudaGraph_t g, const std::string& key);
+// host-side timeline of a build (LOVE_HOST_TIMING=1: printed to stderr at the end of the build)
+void host_mark(const char* what);
+void host_marks_flush();
 // profile.cpp (phase timing, love_profile_*)
 bool profiling();
 void prof_begin(int cat, cudaStream_t s);

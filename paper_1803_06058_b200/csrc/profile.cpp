@@ -1,7 +1,12 @@
 // profile.cpp -- phase timing with CUDA events on the launching stream (love_profile_*).
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "love_internal.h"
@@ -39,6 +44,56 @@ thread_local cudaEvent_t t_open[LOVE_PROF_N] = {nullptr};
 }  // namespace
 
 bool profiling() { return prof().on; }
+
+namespace {
+struct HostMarks {
+    bool on = std::getenv("LOVE_HOST_TIMING") != nullptr;
+    std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> m;
+};
+HostMarks& marks() {
+    thread_local HostMarks h;
+    return h;
+}
+}  // namespace
+
+cudaGraphExec_t graph_exec_cached(cudaGraph_t g, const std::string& key) {
+    thread_local std::unordered_map<std::string, cudaGraphExec_t> cache;
+    static const bool off = std::getenv("LOVE_NO_GRAPH_CACHE") != nullptr;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const std::string k = key + "/dev" + std::to_string(dev);
+    if (!off) {
+        auto it = cache.find(k);
+        if (it != cache.end()) {
+            cudaGraphExecUpdateResultInfo info;
+            if (cudaGraphExecUpdate(it->second, g, &info) == cudaSuccess) return it->second;
+            (void)cudaGetLastError();
+            cudaGraphExecDestroy(it->second);
+            cache.erase(it);
+        }
+    }
+    cudaGraphExec_t ge = nullptr;
+    cuda_check(cudaGraphInstantiate(&ge, g, 0), "graph instantiate");
+    if (!off) cache[k] = ge;
+    return ge;
+}
+
+void host_mark(const char* what) {
+    HostMarks& h = marks();
+    if (h.on) h.m.emplace_back(what, std::chrono::steady_clock::now());
+}
+
+void host_marks_flush() {
+    HostMarks& h = marks();
+    if (!h.on || h.m.empty()) return;
+    std::fprintf(stderr, "[love host]");
+    for (size_t i = 1; i < h.m.size(); ++i)
+        std::fprintf(stderr, " %s %.1f", h.m[i].first,
+                     std::chrono::duration<double, std::micro>(h.m[i].second - h.m[i - 1].second).count());
+    std::fprintf(stderr, " | total %.1f us\n",
+                 std::chrono::duration<double, std::micro>(h.m.back().second - h.m.front().second).count());
+    h.m.clear();
+}
 
 void prof_begin(int cat, cudaStream_t s) {
     Profiler& p = prof();

@@ -744,7 +744,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
             step();
             cuda_check(cudaStreamEndCapture(s, &gph), "sampling capture end");
         }
-        cuda_check(cudaGraphInstantiate(&ge, gph, 0), "sampling graph instantiate");
+        ge = graph_exec_cached(gph, "sampling/" + std::to_string(c.g.d) + "/" + std::to_string((int)st.dgks));
         const int64_t nodes = g_launch_count.load() - before;
         g_launch_count -= nodes;
         // stop replaying after breakdown: the device sets the mapped host flag (ReplayThrottle),
@@ -760,8 +760,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
             thr.launched(i, s);
         }
         if ((ks & 1) && !stop) step();
-        cuda_check(cudaGraphExecDestroy(ge), "graph destroy");
-        cuda_check(cudaGraphDestroy(gph), "graph destroy");
+        cuda_check(cudaGraphDestroy(gph), "graph destroy");      // the exec stays cached
     } else {
         for (int j = 0; j < ks; ++j) step();
     }
