@@ -49,12 +49,53 @@ void ensure_smem(const void* fn, size_t bytes) {
     cur = bytes;
 }
 
+// Buffers up to kSlabPiece bytes are carved (256-byte aligned) from slabs of kSlab bytes that
+// are zeroed once when they are allocated: a build's few dozen state buffers cost a handful of
+// allocation / memset calls instead of two each (LOVE_NO_SLAB: one allocation per buffer).
+constexpr size_t kSlab = size_t(4) << 20, kSlabPiece = size_t(256) << 10;
+
 void* dalloc(Cache& c, size_t bytes, cudaStream_t s) {
+    void* p = nullptr;
+    bytes = std::max<size_t>(bytes, 16);
+    static const bool no_slab = std::getenv("LOVE_NO_SLAB") != nullptr;
+    if (!no_slab && bytes <= kSlabPiece) {
+        bytes = (bytes + 255) & ~size_t(255);
+        if (c.slab == nullptr || c.slab_used + bytes > kSlab) {
+            cuda_check(cudaMallocAsync(&p, kSlab, s), "cudaMallocAsync(slab)");
+            c.allocs.push_back(p);
+            cuda_check(cudaMemsetAsync(p, 0, kSlab, s), "cudaMemsetAsync(slab)");
+            c.slab = (char*)p;
+            c.slab_used = 0;
+        }
+        p = c.slab + c.slab_used;
+        c.slab_used += bytes;
+        return p;
+    }
+    cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    c.allocs.push_back(p);
+    cuda_check(cudaMemsetAsync(p, 0, bytes, s), "cudaMemsetAsync");
+    return p;
+}
+
+void* dalloc_unset(Cache& c, size_t bytes, cudaStream_t s) {
     void* p = nullptr;
     bytes = std::max<size_t>(bytes, 16);
     cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
     c.allocs.push_back(p);
-    cuda_check(cudaMemsetAsync(p, 0, bytes, s), "cudaMemsetAsync");
+    static const bool poison = std::getenv("LOVE_POISON") != nullptr;
+    if (poison) cuda_check(cudaMemsetAsync(p, 0xff, bytes, s), "cudaMemsetAsync(poison)");
+    return p;
+}
+
+void* pinned_scratch(size_t bytes) {
+    thread_local void* p = nullptr;
+    thread_local size_t cap = 0;
+    if (bytes > cap) {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = std::max<size_t>(bytes, 64 << 10);
+        cuda_check(cudaHostAlloc(&p, cap, cudaHostAllocDefault), "cudaHostAlloc(scratch)");
+    }
     return p;
 }
 
@@ -283,7 +324,8 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     c->u = dalloc(*c, sizeof(double) * M, s);
     c->z[0] = dalloc(*c, sizeof(double) * (M + 4), s);      // padded: tiles stage z in 16-byte units
     c->z[1] = dalloc(*c, sizeof(double) * (M + 4), s);
-    c->Rc_col = dalloc(*c, sizeof(double) * (size_t)M * k, s);
+    // column j is streamed at step j (the one-read pass: zero-filled)
+    c->Rc_col = c->fused ? dalloc(*c, sizeof(double) * (size_t)M * k, s) : dalloc_unset(*c, sizeof(double) * (size_t)M * k, s);
     c->a = dalloc(*c, sizeof(double) * M, s);
     c->counters = (unsigned long long*)dalloc(*c, sizeof(unsigned long long) * 2, s);
     {
@@ -341,12 +383,25 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     if (c->fused) run_lanczos_fused(*c, s);
     else run_lanczos(*c, s);
     host_mark("lanczos_enqueued");
-    int hfl[8];
-    double bn2 = 0;
-    cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
-    cuda_check(cudaMemcpyAsync(&bn2, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    // one D2H batch and one synchronisation: flags, |b|^2 and T's alpha_j, beta_j (contiguous
+    // in the scalar block) for every j < k
+    const size_t K = (size_t)k;
+    char* hb = (char*)pinned_scratch(sizeof(int) * 8 + sizeof(double) * (1 + 2 * K) + sizeof(int));
+    int* hfl = (int*)hb;
+    double* hbn = (double*)(hb + sizeof(int) * 8);
+    double* hab = hbn + 1;
+    cuda_check(cudaMemcpyAsync(hfl, c->st.flags, sizeof(int) * 8, cudaMemcpyDeviceToHost, s), "flags d2h");
+    cuda_check(cudaMemcpyAsync(hbn, c->st.bnorm2, sizeof(double), cudaMemcpyDeviceToHost, s), "d2h");
+    cuda_check(cudaMemcpyAsync(hab, c->st.alpha, sizeof(double) * 2 * K, cudaMemcpyDeviceToHost, s), "T d2h");
+    int* hrange = (int*)(hab + 2 * K);
+    *hrange = 0;
+    if (c->range_flag != nullptr)
+        cuda_check(cudaMemcpyAsync(hrange, c->range_flag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
     cuda_check(cudaStreamSynchronize(s), "lanczos sync");
     host_mark("lanczos_sync");
+    c->range_flag = nullptr;
+    if (*hrange) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
+    const double bn2 = *hbn;
     cuda_check(cudaGetLastError(), "lanczos kernels");
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};
     if (hfl[2]) throw LoveError{LOVE_ERR_NOT_PD, "Cholesky of T_k hit a non-positive pivot"};
@@ -364,17 +419,15 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         cuda_check(cudaMemcpy(pro, c->st.pro, sizeof(pro), cudaMemcpyDeviceToHost), "pro d2h");
         c->n_reorth_steps = pro[2];
     }
-    c->h_alpha.resize(c->k_eff);
-    c->h_beta.resize(std::max(c->k_eff - 1, 0));
-    cuda_check(cudaMemcpy(c->h_alpha.data(), c->st.alpha, sizeof(double) * c->k_eff, cudaMemcpyDeviceToHost),
-               "alpha d2h");
-    if (c->k_eff > 1)
-        cuda_check(cudaMemcpy(c->h_beta.data(), c->st.beta, sizeof(double) * (c->k_eff - 1),
-                              cudaMemcpyDeviceToHost), "beta d2h");
+    if (c->st.beta != c->st.alpha + K) throw LoveError{LOVE_ERR_CUDA, "internal: T layout"};
+    c->h_alpha.assign(hab, hab + c->k_eff);
+    c->h_beta.assign(hab + K, hab + K + std::max(c->k_eff - 1, 0));
+    host_mark("alpha_beta");
     if (c->probe == LOVE_PROBE_AVGCOL) mean_cache_eq4(*c, s);   // a = R^T T^{-1} Q^T y
     finish_cache(*c, s);
     c->var_blocks_off = o.var_blocks == LOVE_VAR_BLOCKS_OFF;
     build_var_blocks(*c, s);
+    host_mark("finish_enqueued");
     if (c->k_sample_req > 0) build_sampling_cache(*c, s);
     cuda_check(cudaStreamSynchronize(s), "build sync");
     cuda_check(cudaGetLastError(), "build kernels");
@@ -442,7 +495,15 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
         c->cell_item_start = (int*)dalloc(*c, sizeof(int) * (M + 1), s);
         for (int d = 0; d < g.d; ++d) c->frac[d] = dalloc(*c, vs * (c->ldq + 4), s);   // padded to 16 B units
         if (g.d <= 2 && !c->fused) c->pcell = (int*)dalloc(*c, sizeof(int) * (c->ldq + 4), s);
-        c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        // Q~: column j + 1 is written whole (ldq rows) by step j before anything reads it;
+        // column 0 (the probe, n rows) is zeroed first so that its padding rows are 0
+        // (the one-read pass reads ahead: zero-filled)
+        if (c->fused) {
+            c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        } else {
+            c->Q = dalloc_unset(*c, vs * c->ldq * (size_t)(k + 1), s);
+            cuda_check(cudaMemsetAsync(c->Q, 0, vs * c->ldq, s), "Q0 memset");
+        }
         host_mark("begin_build");
         prof_begin(LOVE_PROF_SETUP, s);
         launch_interp_points(*c, X, c->n, cell, frac64, dflag, s);
@@ -467,18 +528,27 @@ static love_status build_grid_once(const love_grid* grid, const love_rbf* rbf, d
         if (c->probe == LOVE_PROBE_AVGCOL) c->ysort = dalloc(*c, vs * c->ldq, s);
         launch_counting_sort(*c, cell, frac64, y, c->n, c->probe == LOVE_PROBE_Y ? c->Q : c->ysort, s);
         host_mark("interp+range_sync");
-        // one GPU: the range flag comes back with the item count (one synchronisation; a point
-        // off the grid was given cell 0, so the sort above stayed in bounds)
-        int hrange = 0;
-        if (c->comm == nullptr)
-            cuda_check(cudaMemcpyAsync(&hrange, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
-        c->n_items = count_items_host(*c, s);
-        if (hrange) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
-        host_mark("sort+items_sync");
-        c->item_cell = (int*)dalloc(*c, sizeof(int) * (c->n_items + 8), s);     // padded: staged in 16 B units
-        c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
-        launch_build_items(*c, s);
-        c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
+        // the item list (cells cut into <= kItemMax-point chunks) feeds the d >= 2 item kernels and
+        // the one-read pass; the d = 1 cell-moment scatter and per-point gather do without it, and
+        // then nothing before the Lanczos needs a synchronisation: the range flag is read back
+        // with the Lanczos flags (a point off the grid was given cell 0, so every pass stays in
+        // bounds until then)
+        if (g.d >= 2 || c->fused || c->comm != nullptr) {
+            // one GPU: the range flag comes back with the item count (one synchronisation)
+            int hrange = 0;
+            if (c->comm == nullptr)
+                cuda_check(cudaMemcpyAsync(&hrange, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag d2h");
+            c->n_items = count_items_host(*c, s);
+            if (hrange) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
+            host_mark("sort+items_sync");
+            c->item_cell = (int*)dalloc(*c, sizeof(int) * (c->n_items + 8), s);     // padded: staged in 16 B units
+            c->item_start = (int*)dalloc(*c, sizeof(int) * (c->n_items + 9), s);
+            launch_build_items(*c, s);
+            c->M = dalloc(*c, sizeof(double) * (size_t)(1 << (2 * g.d)) * std::max<int64_t>(c->n_items, 1), s);
+        } else {
+            c->n_items = -1;
+            c->range_flag = dflag;
+        }
         if (g.d == 1 && !c->fused) c->Mc = dalloc(*c, sizeof(double) * 4 * (size_t)(M + 4), s);
         if (g.d >= 2) {
             c->pullT = dalloc(*c, sizeof(double) * (size_t)(g.d == 2 ? 4 : 16) * M, s);
@@ -562,7 +632,15 @@ static love_status build_additive_once(const love_axis* axes, int32_t d, double 
         TempPool tmp(s);
         int* dflag = (int*)tmp.get(sizeof(int) * 2);
         cuda_check(cudaMemsetAsync(dflag, 0, sizeof(int) * 2, s), "memset");
-        c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        // Q~: column j + 1 is written whole (ldq rows) by step j before anything reads it;
+        // column 0 (the probe, n rows) is zeroed first so that its padding rows are 0
+        // (the one-read pass reads ahead: zero-filled)
+        if (c->fused) {
+            c->Q = dalloc(*c, vs * c->ldq * (size_t)(k + 1), s);
+        } else {
+            c->Q = dalloc_unset(*c, vs * c->ldq * (size_t)(k + 1), s);
+            cuda_check(cudaMemsetAsync(c->Q, 0, vs * c->ldq, s), "Q0 memset");
+        }
         prof_begin(LOVE_PROF_SETUP, s);
         additive_setup(*c, X, y, dflag, s);
         {   // the range check is global: every rank must agree before continuing
@@ -661,6 +739,12 @@ love_status love_cache_info(const love_cache* cache, love_info* info) {
         info->n_global = c->n_global;
         info->m_total = c->g.m_total;
         info->n_items = c->n_items;
+        if (c->n_items < 0) {   // not listed at build time: the count of the per-cell item scan
+            int nit = 0;
+            cuda_check(cudaMemcpy(&nit, c->cell_item_start + c->g.m_total, sizeof(int), cudaMemcpyDeviceToHost),
+                       "items d2h");
+            info->n_items = nit;
+        }
         info->b_norm = c->b_norm;
         info->alpha = c->h_alpha.data();
         info->beta = c->h_beta.data();

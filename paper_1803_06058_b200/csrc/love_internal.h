@@ -135,7 +135,9 @@ struct Cache {
 
     // ---------------- training points (sorted by flat cell)
     int64_t n = 0, n_global = 0, ldq = 0;
-    int64_t n_items = 0;
+    int64_t n_items = 0;                 // -1: not listed (d = 1 single-GPU path; love_cache_info reads the count)
+    const int* range_flag = nullptr;     // build only: device flag of an off-grid training point, checked
+                                         // with the Lanczos flags when no earlier synchronisation did
     void* frac[3] = {nullptr, nullptr, nullptr};   // V[n] per dim (sorted order)
     int* perm = nullptr;                 // [n] sorted -> original
     int* pcell = nullptr;                // d <= 2: [ldq + 4] cell of each sorted point (0 past n)
@@ -208,6 +210,8 @@ struct Cache {
     std::vector<double> h_evals;         // eigenvalues of T' (sampling cache)
 
     std::vector<void*> allocs;           // everything to release
+    char* slab = nullptr;                // small buffers are carved from zeroed slabs (dalloc)
+    size_t slab_used = 0;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -225,6 +229,10 @@ void cuda_check(cudaError_t e, const char* what);
 // raises a kernel's dynamic shared-memory limit once (cudaFuncSetAttribute is a host call)
 void ensure_smem(const void* fn, size_t bytes);
 void* dalloc(Cache& c, size_t bytes, cudaStream_t s);   // zero-filled, owned by the cache
+void* pinned_scratch(size_t bytes);                      // this thread's pinned host staging buffer
+// owned by the cache, NOT zero-filled: only for buffers every reader finds written first
+// (LOVE_POISON=1 fills them with NaN bytes instead, to prove it)
+void* dalloc_unset(Cache& c, size_t bytes, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // Launchers (each file defines its own kernels; V = float | double)

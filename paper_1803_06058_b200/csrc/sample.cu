@@ -83,13 +83,26 @@ __device__ __forceinline__ int sturm_count(const double* a, const double* b2, in
     double pm = 1.0, pc = a[0] - x;
     if (pc == 0.0) pc = -1e-300;                 // a zero pivot is taken as -tiny (negative)
     int cnt = pc < 0.0;
-    for (int k = 1; k < n; ++k) {
-        double pn = (a[k] - x) * pc - b2[k - 1] * pm;
-        if (pn == 0.0) pn = -1e-300 * pc;        // pivot p_k / p_{k-1} = -tiny
-        cnt += (pn > 0.0) != (pc > 0.0);
-        pm = pc;
-        pc = pn;
-        if ((k & 7) == 0) {
+    // blocks of 8 terms (k = 8, 16, ... end a block: the rescale points), fully unrolled so the
+    // shared-memory loads of a block issue ahead of the dependent chain
+    for (int kb = 1; kb < n; kb += 8) {
+        double ak[8], bk[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            ak[u] = kb + u < n ? a[kb + u] : 0.0;
+            bk[u] = kb + u < n ? b2[kb + u - 1] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (kb + u < n) {
+                double pn = (ak[u] - x) * pc - bk[u] * pm;
+                if (pn == 0.0) pn = -1e-300 * pc;        // pivot p_k / p_{k-1} = -tiny
+                cnt += (pn > 0.0) != (pc > 0.0);
+                pm = pc;
+                pc = pn;
+            }
+        }
+        if (kb + 7 < n) {                         // k = kb + 7 = 8, 16, ...
             const double sc = rcp64(fabs(pc) + fabs(pm));
             pc *= sc;
             pm *= sc;
@@ -98,10 +111,72 @@ __device__ __forceinline__ int sturm_count(const double* a, const double* b2, in
     return cnt;
 }
 
+// Gershgorin interval of T' (padded by 2 ulp), ||T'||_1 and max b_i^2 (thread 0)
+__device__ __forceinline__ void gershgorin(const double* a, const double* b, const double* b2, int n, double* lo_out,
+                                           double* hi_out, double* norm1, double* b2max) {
+    double lo = 1e300, hi = -1e300, nrm = 0.0, bm = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + fabs(b[i]);
+        lo = fmin(lo, a[i] - r);
+        hi = fmax(hi, a[i] + r);
+        nrm = fmax(nrm, fabs(a[i]) + r);
+        bm = fmax(bm, b2[i]);
+    }
+    const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300;
+    *lo_out = lo - pad;
+    *hi_out = hi + pad;
+    *norm1 = nrm;
+    *b2max = bm;
+}
+
+// eigenvalue i of T' by multisection: the 8 lanes `sub` of an aligned lane group split the
+// interval into 9 per round, 19 rounds from the Gershgorin interval (9^-19 ~ 2^-60 of it)
+__device__ __forceinline__ double multisection(const double* a, const double* b2, int n, int i, int sub, double lo,
+                                               double hi) {
+    const int lane = threadIdx.x & 31;
+    for (int it = 0; it < 19; ++it) {
+        const double x = lo + (hi - lo) * (double)(sub + 1) * (1.0 / 9.0);
+        const int cnt = i < n ? sturm_count(a, b2, n, x) : 0;
+        // new interval: between the last x with cnt <= i and the first x with cnt > i
+        double nlo = lo, nhi = hi;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const double xt = __shfl_sync(0xffffffffu, x, (lane & ~7) + t);
+            const int ct = __shfl_sync(0xffffffffu, cnt, (lane & ~7) + t);
+            if (ct <= i) nlo = fmax(nlo, xt);
+            else nhi = fmin(nhi, xt);
+        }
+        lo = nlo;
+        hi = nhi;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// Stage 1 spread over ceil(n / 8) CTAs (8 eigenvalues x 8 lanes each): the Sturm-count chains
+// are FP64-pipe bound on one SM
+__global__ void __launch_bounds__(64) tridiag_eigvals_kernel(const double* __restrict__ alpha,
+                                                             const double* __restrict__ beta, int n,
+                                                             double* __restrict__ lam) {
+    __shared__ double a[kMaxKs], b[kMaxKs], b2[kMaxKs];
+    __shared__ double s_lo, s_hi, s_norm1, s_b2max;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        a[i] = alpha[i];
+        b[i] = i + 1 < n ? beta[i] : 0.0;
+        b2[i] = b[i] * b[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) gershgorin(a, b, b2, n, &s_lo, &s_hi, &s_norm1, &s_b2max);
+    __syncthreads();
+    const int i = blockIdx.x * 8 + (threadIdx.x >> 3), sub = threadIdx.x & 7;
+    const double l = multisection(a, b2, n, i, sub, s_lo, s_hi);
+    if (i < n && sub == 0) lam[i] = l;
+}
+
+// lam_in != nullptr: the eigenvalues come from tridiag_eigvals_kernel (stage 1 skipped)
 __global__ void __launch_bounds__(512) tridiag_root_kernel(const double* __restrict__ alpha,
                                                            const double* __restrict__ beta, int n,
                                                            double* __restrict__ Wout, double* __restrict__ evals,
-                                                           double ctol) {
+                                                           double ctol, const double* __restrict__ lam_in) {
     __shared__ double a[kMaxKs], b[kMaxKs], b2[kMaxKs], lam[kMaxKs], sl[kMaxKs];
     extern __shared__ double Vsm[];                      // [n][n + 1], column i = eigenvector i
     const int LV = n + 1 + (n & 1 ? 1 : 0);     // odd: column sweeps spread over the banks
@@ -112,46 +187,19 @@ __global__ void __launch_bounds__(512) tridiag_root_kernel(const double* __restr
         a[i] = alpha[i];
         b[i] = i + 1 < n ? beta[i] : 0.0;
         b2[i] = b[i] * b[i];
+        if (lam_in != nullptr) lam[i] = lam_in[i];
     }
     __syncthreads();
-    if (tid == 0) {
-        double lo = 1e300, hi = -1e300, nrm = 0.0, bm = 0.0;
-        for (int i = 0; i < n; ++i) {
-            const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + fabs(b[i]);
-            lo = fmin(lo, a[i] - r);
-            hi = fmax(hi, a[i] + r);
-            nrm = fmax(nrm, fabs(a[i]) + r);
-            bm = fmax(bm, b2[i]);
-        }
-        const double pad = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 1e-300;
-        s_lo = lo - pad;
-        s_hi = hi + pad;
-        s_norm1 = nrm;
-        s_b2max = bm;
-    }
+    if (tid == 0) gershgorin(a, b, b2, n, &s_lo, &s_hi, &s_norm1, &s_b2max);
     __syncthreads();
     const double pivmin = 1e-290 * fmax(1.0, s_b2max);
-    // 1. multisection: 8 threads (sub) per eigenvalue i = tid / 8, 9 sub-intervals per round,
-    // 19 rounds: 9^-19 ~ 2^-60 of the Gershgorin interval
-    for (int i0 = 0; i0 < n; i0 += 64) {
-        const int i = i0 + (tid >> 3), sub = tid & 7;
-        double lo = s_lo, hi = s_hi;
-        for (int it = 0; it < 19; ++it) {
-            const double x = lo + (hi - lo) * (double)(sub + 1) * (1.0 / 9.0);
-            const int cnt = i < n ? sturm_count(a, b2, n, x) : 0;
-            // new interval: between the last x with cnt <= i and the first x with cnt > i
-            double nlo = lo, nhi = hi;
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const double xt = __shfl_sync(0xffffffffu, x, (tid & 31 & ~7) + t);
-                const int ct = __shfl_sync(0xffffffffu, cnt, (tid & 31 & ~7) + t);
-                if (ct <= i) nlo = fmax(nlo, xt);
-                else nhi = fmin(nhi, xt);
-            }
-            lo = nlo;
-            hi = nhi;
+    // 1. multisection: 8 threads (sub) per eigenvalue i = tid / 8
+    if (lam_in == nullptr) {
+        for (int i0 = 0; i0 < n; i0 += 64) {
+            const int i = i0 + (tid >> 3), sub = tid & 7;
+            const double l = multisection(a, b2, n, i, sub, s_lo, s_hi);
+            if (i < n && sub == 0) lam[i] = l;
         }
-        if (i < n && sub == 0) lam[i] = 0.5 * (lo + hi);
     }
     __syncthreads();
     // 2. twisted factorisation per eigenvalue (thread i)
@@ -383,23 +431,57 @@ __global__ void __launch_bounds__(512) jacobi_root_kernel(const double* __restri
 }
 
 // S[row][c] = sum_i Q'[row + i*ldq] W[i][c]  -> V (fp32 / fp64) row-major m x ks_pad
+// S = Q'~ diag(qscale) W (reading A18: S = Q' T'^{1/2}), 32 rows per CTA: the rows' Q' values
+// (transposed, [i][row]) and W staged in shared memory; thread = (column c and c + 64, 8 rows),
+// the 8 row values of each i read as one broadcast; the sum over i runs in ascending order as
+// an FMA chain per output
+constexpr int kRootRows = 32;
 template <typename V>
-__global__ void __launch_bounds__(256) root_kernel(const double* __restrict__ Qp, int64_t ldq, int m, int n,
-                                                   const double* __restrict__ qscale,
-                                                   const double* __restrict__ W, int ks_pad, V* __restrict__ S) {
-    extern __shared__ double Ws[];               // [n][n]
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Ws[e] = W[e];
+__global__ void __launch_bounds__(256) root_tile_kernel(const double* __restrict__ Qp, int64_t ldq, int m, int n,
+                                                        const double* __restrict__ qscale,
+                                                        const double* __restrict__ W, int ks_pad, V* __restrict__ S) {
+    extern __shared__ __align__(16) double sm[];
+    double* Qt = sm;                              // [n][kRootRows]
+    double* Ws = sm + (size_t)n * kRootRows;      // [n][ks_pad], columns >= n zero
+    const int r0 = blockIdx.x * kRootRows;
+    for (int e = threadIdx.x; e < n * ks_pad; e += blockDim.x) {
+        const int i = e / ks_pad, c = e - i * ks_pad;
+        Ws[e] = c < n ? W[i * n + c] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kRootRows * n; e += blockDim.x) {
+        const int i = e / kRootRows, r = e - i * kRootRows;     // coalesced along the rows of column i
+        const int row = r0 + r;
+        Qt[e] = row < m ? qscale[i] * Qp[(int64_t)i * ldq + row] : 0.0;
+    }
     __syncthreads();
-    const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (row >= m) return;
-    double q[kMaxKs];
-    for (int i = 0; i < n; ++i) q[i] = qscale[i] * Qp[(int64_t)i * ldq + row];
-    for (int c = lane; c < ks_pad; c += 32) {
-        double acc = 0.0;
-        if (c < n)
-            for (int i = 0; i < n; ++i) acc += q[i] * Ws[i * n + c];
-        S[(int64_t)row * ks_pad + c] = (V)acc;
+    const int c = threadIdx.x & 63, rg = threadIdx.x >> 6;    // rows rg*8 .. rg*8+7
+    const bool c0 = c < ks_pad, c1 = c + 64 < ks_pad;
+    double a0[8], a1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a0[u] = a1[u] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double2* q2 = reinterpret_cast<const double2*>(Qt + i * kRootRows + rg * 8);
+        double q[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double2 t = q2[u];
+            q[2 * u] = t.x;
+            q[2 * u + 1] = t.y;
+        }
+        const double w0 = c0 ? Ws[i * ks_pad + c] : 0.0;
+        const double w1 = c1 ? Ws[i * ks_pad + c + 64] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0[u] = fma(q[u], w0, a0[u]);
+            a1[u] = fma(q[u], w1, a1[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const int row = r0 + rg * 8 + u;
+        if (row >= m) break;
+        if (c0) S[(int64_t)row * ks_pad + c] = (V)a0[u];
+        if (c1) S[(int64_t)row * ks_pad + c + 64] = (V)a1[u];
     }
 }
 
@@ -407,19 +489,6 @@ __global__ void __launch_bounds__(256) root_kernel(const double* __restrict__ Qp
 // grid Lanczos machinery (device step index, CUDA-graph replay, the same reorthogonalisation
 // kernels in fp64, two CGS passes); only the operator differs.  Q~ columns are unnormalised,
 // q_j = qscale[j] Q~[:, j].
-
-// q_j into the fixed MVM input buffer (the K_UU kernels read a fixed pointer); zero t
-__global__ void samp_qcur_kernel(LanczosState st, const double* __restrict__ Q, int64_t ld, int m,
-                                 double* __restrict__ qcur, double* __restrict__ t, int kt) {
-    pdl_wait();
-    if (st.flags[0]) return;
-    const int j = *st.jdev;
-    const double sc = st.qscale[j];
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-        qcur[i] = sc * Q[(int64_t)j * ld + i];
-    if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < kt; i += blockDim.x) t[i] = 0.0;
-}
 
 // v = z - Rc t (t = Rc^T q_j) and alpha_j += q_j . v   (fp64).  A CTA owns 32 rows; its 8
 // warps split the k_eff columns (lanes over the rows: coalesced column reads), the partial sums
@@ -429,9 +498,8 @@ constexpr int kSvRows = 32;
 __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ Rc, int m, int k_eff,
                                                      const double* __restrict__ z, const double* __restrict__ t,
                                                      const double* __restrict__ qcur, double* __restrict__ v,
-                                                     LanczosState st) {
+                                                     LanczosState st, double* __restrict__ t_next) {
     __shared__ double psum[8][kSvRows];
-    __shared__ double red[32];
     pdl_wait();
     if (st.flags[0]) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -455,7 +523,37 @@ __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ 
         a = warp_sum(a);
         if (lane == 0) atomicAdd(st.alpha_cur, a);
     }
-    (void)red;
+    // the other t buffer (read by the previous step, accumulated by the next) starts from zero
+    if (blockIdx.x == 0)
+        for (int c = threadIdx.x; c < k_eff; c += blockDim.x) t_next[c] = 0.0;
+}
+
+// q_j = s_j Q~'[:, j] (fp64) and t += Rc^T q_j over this CTA's kDotRows rows (dots_kernel's
+// column loop; t was zeroed by the step before)
+__global__ void __launch_bounds__(256) samp_qcur_dots_kernel(LanczosState st, const double* __restrict__ Q, int64_t ld,
+                                                             int m, const double* __restrict__ Rc, int ncol,
+                                                             double* __restrict__ qcur, double* __restrict__ t) {
+    pdl_wait();
+    if (st.flags[0]) return;
+    __shared__ double xs[kDotRows];
+    const int j = *st.jdev;
+    const double sc = st.qscale[j];
+    const int r0 = blockIdx.x * kDotRows;
+    const int nr = min(kDotRows, m - r0);
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+        const double q = sc * Q[(int64_t)j * ld + r0 + i];
+        qcur[r0 + i] = q;
+        xs[i] = q;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int c = wid; c < ncol; c += nw) {
+        const double* a = Rc + (int64_t)c * m + r0;
+        double acc = 0.0;
+        for (int i = lane; i < nr; i += 32) acc += a[i] * xs[i];
+        acc = warp_sum(acc);
+        if (lane == 0) atomicAdd(&t[c], acc);
+    }
 }
 
 __global__ void fill_ones_kernel(double* __restrict__ v, int m) {
@@ -666,6 +764,15 @@ __global__ void __launch_bounds__(256) sample_gemm2_kernel(const float* __restri
 
 }  // namespace
 
+static __global__ void samp_flags_kernel(int* flags, int ks) {
+    if (threadIdx.x == 0) {
+        flags[0] = 0;
+        flags[1] = ks;
+        flags[2] = 0;
+        flags[3] = 0;
+    }
+}
+
 void build_sampling_cache(Cache& c, cudaStream_t s) {
     ProfScope ps(LOVE_PROF_SAMPLE_CACHE, s);
     const int ks = c.k_sample_req;
@@ -678,7 +785,10 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     double* v = (double*)dalloc(c, sizeof(double) * ldq, s);
     double* qcur = (double*)dalloc(c, sizeof(double) * (m + 4), s);
     double* z = (double*)dalloc(c, sizeof(double) * (m + 4), s);
-    double* t = (double*)dalloc(c, sizeof(double) * std::max(k, 1), s);
+    // t = Rc^T q_j, two buffers by step parity (a step accumulates one, its samp_v zeroes the other)
+    double* tb[2];
+    tb[0] = (double*)dalloc(c, sizeof(double) * 2 * std::max(k, 1), s);
+    tb[1] = tb[0] + std::max(k, 1);
     // state of the M-Lanczos (reading A15: no Cholesky of T'; breakdown rule A12, tol 1e-10)
     LanczosState st{};
     {
@@ -704,29 +814,31 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
             st.nrm2 = (double*)dalloc(c, sizeof(double) * 2, s);
             st.dgks = 1;
         }
-        const int f[4] = {0, ks, 0, 0};
-        cuda_check(cudaMemcpyAsync(st.flags, f, sizeof(f), cudaMemcpyHostToDevice, s), "sampling flags");
+        LOVE_LAUNCH(samp_flags_kernel, 1, 32, 0, s, st.flags, ks);
     }
+    host_mark("samp_alloc");
     const double tol = 1e-10;
     const int gm = (int)ceil_div(m, kSvRows), gd = (int)ceil_div(m, kDotRows);
     const int gq = (int)std::min<int64_t>(ceil_div(m, 256), 148 * 4);
     // probe b' = M 1 (reading A14) into Q~[:, 0]
     LOVE_LAUNCH(fill_ones_kernel, gq, 256, 0, s, qcur, m);
     launch_kuu(c, qcur, z, s);
-    LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, t, (const int*)nullptr);
-    LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, t, qcur, Qp, st);
+    LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, tb[1], (const int*)nullptr);
+    LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, tb[1], qcur, Qp, st, tb[0]);
     LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Qp, ldq, m, 1, Qp, st.bnorm2, (const int*)nullptr);
     cuda_check(cudaMemsetAsync(st.alpha_cur, 0, sizeof(double), s), "alpha clear");
     launch_init_q0(st, s);
     // one step: q_j -> K_UU q_j, Rc^T q_j -> v, alpha -> two CGS passes (the last finalises)
+    int par = 0;
     auto step = [&]() {
-        LOVE_LAUNCH(samp_qcur_kernel, gq, 256, 0, s, st, (const double*)Qp, ldq, m, qcur, t, k);
+        double* t = tb[par];
+        LOVE_LAUNCH(samp_qcur_dots_kernel, gd, 256, 0, s, st, (const double*)Qp, ldq, m, Rc, k, qcur, t);
         {
             DoneScope ds(st.flags);
             launch_kuu(c, qcur, z, s);
         }
-        LOVE_LAUNCH(dots_kernel, gd, 256, 0, s, Rc, (int64_t)m, m, k, qcur, t, st.flags);
-        LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, t, qcur, v, st);
+        LOVE_LAUNCH(samp_v_kernel, gm, 256, 0, s, Rc, m, k, z, t, qcur, v, st, tb[par ^ 1]);
+        par ^= 1;
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 0, 0, v, tol, s);
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 1, 1, v, tol, s);
     };
@@ -744,7 +856,9 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
             step();
             cuda_check(cudaStreamEndCapture(s, &gph), "sampling capture end");
         }
+        host_mark("samp_capture");
         ge = graph_exec_cached(gph, "sampling/" + std::to_string(c.g.d) + "/" + std::to_string((int)st.dgks));
+        host_mark("samp_instantiate");
         const int64_t nodes = g_launch_count.load() - before;
         g_launch_count -= nodes;
         // stop replaying after breakdown: the device sets the mapped host flag (ReplayThrottle),
@@ -764,9 +878,11 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     } else {
         for (int j = 0; j < ks; ++j) step();
     }
+    host_mark("samp_enqueued");
     int hfl[4];
     cuda_check(cudaMemcpyAsync(hfl, st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
     cuda_check(cudaStreamSynchronize(s), "sampling sync");
+    host_mark("samp_sync");
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "sampling probe M 1 is zero"};
     // every step that ran to the end set done at i = ks - 1 or at the breakdown step
     const int ke = hfl[0] ? hfl[1] : ks;
@@ -784,23 +900,27 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         // the opt-in limit counts static + dynamic shared memory (the kernel's static arrays
         // are ~6 KB): request it whenever the sum passes 48 KB
         ensure_smem((const void*)tridiag_root_kernel, smv + 8192);
+        static const bool one_cta = std::getenv("LOVE_EIG_ONE_CTA") != nullptr;
+        if (!one_cta) LOVE_LAUNCH(tridiag_eigvals_kernel, (int)ceil_div(ke, 8), 64, 0, s, st.alpha, st.beta, ke, ev);
         LOVE_LAUNCH(tridiag_root_kernel, 1, 512, smv, s, st.alpha, st.beta, ke, W, ev,
-                    std::getenv("LOVE_EIG_CTOL") ? std::atof(std::getenv("LOVE_EIG_CTOL")) : 1e-9);
+                    std::getenv("LOVE_EIG_CTOL") ? std::atof(std::getenv("LOVE_EIG_CTOL")) : 1e-9,
+                    one_cta ? (const double*)nullptr : (const double*)ev);
     }
     c.S = dalloc(c, c.vsize * (size_t)m * c.ks_pad, s);
-    const size_t smr = sizeof(double) * ke * ke;
+    // S = Q' diag(qscale) W, 32 rows per CTA (the rows' Q' values and W staged in shared memory)
+    const size_t smr = sizeof(double) * ((size_t)ke * c.ks_pad + (size_t)kRootRows * ke);
+    const int gr = (int)ceil_div(m, kRootRows);
     if (c.precision == LOVE_FP64) {
-        ensure_smem((const void*)root_kernel<double>, smr);
-        LOVE_LAUNCH(root_kernel<double>, (int)ceil_div(m, 8), 256, smr, s, Qp, ldq, m, ke, st.qscale, W, c.ks_pad,
-                    (double*)c.S);
+        ensure_smem((const void*)root_tile_kernel<double>, smr);
+        LOVE_LAUNCH(root_tile_kernel<double>, gr, 256, smr, s, Qp, ldq, m, ke, st.qscale, W, c.ks_pad, (double*)c.S);
     } else {
-        ensure_smem((const void*)root_kernel<float>, smr);
-        LOVE_LAUNCH(root_kernel<float>, (int)ceil_div(m, 8), 256, smr, s, Qp, ldq, m, ke, st.qscale, W, c.ks_pad,
-                    (float*)c.S);
+        ensure_smem((const void*)root_tile_kernel<float>, smr);
+        LOVE_LAUNCH(root_tile_kernel<float>, gr, 256, smr, s, Qp, ldq, m, ke, st.qscale, W, c.ks_pad, (float*)c.S);
     }
     c.h_evals.resize(ke);
     cuda_check(cudaMemcpyAsync(c.h_evals.data(), ev, sizeof(double) * ke, cudaMemcpyDeviceToHost, s), "evals");
     cuda_check(cudaStreamSynchronize(s), "sampling sync");
+    host_mark("samp_root");
 }
 
 template <typename VS>

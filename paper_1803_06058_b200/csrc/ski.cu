@@ -257,6 +257,35 @@ __global__ void __launch_bounds__(256) pull_first_kernel(GridDev g, const double
     u[x] = sum * ref.scale[step_j(ref)];
 }
 
+// d = 3: pull_mid and pull_first in one pass (each T entry is read by exactly one node):
+//   u[i0, i1, i2] = s_j * sum_a ( sum_b T[a*4 + b][i0 - a + 1, i1 - b + 1, i2] )
+// with the same two summation orders as the separate passes (bitwise the same u)
+__global__ void __launch_bounds__(256) pull_mid_first_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
+                                                             double* __restrict__ u) {
+    pdl_wait();
+    const int m = g.m_total;
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= m || step_done(ref)) return;
+    const int i0 = x / g.stride[0];
+    const int i1 = (x / g.stride[1]) % g.m[1];
+    double sum = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int c0 = i0 - a + 1;
+        if (c0 < 0 || c0 >= g.m[0]) continue;
+        const int64_t xa = x + (int64_t)(1 - a) * g.stride[0];
+        double va = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int c1 = i1 - b + 1;
+            if (c1 < 0 || c1 >= g.m[1]) continue;
+            va += T[(int64_t)(a * 4 + b) * m + xa + (1 - b) * g.stride[1]];
+        }
+        sum += va;
+    }
+    u[x] = sum * ref.scale[step_j(ref)];
+}
+
 // u[i] = scale * sum over slots l of sum over items of cell (i - l + 1) of M[l][item]
 template <int D>
 __global__ void __launch_bounds__(256) nodepass_kernel(GridDev g, int64_t n_items,
@@ -555,9 +584,14 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             constexpr int SG = LOVE_PULL3_SG;
             LOVE_LAUNCH((pull_last_kernel<3, MT, SG>), (int)ceil_div((int64_t)m * (16 / SG), 256), 256, 0, s, c.g,
                         ni, c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
-            LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g, (const double*)c.pullT,
-                        ref, (double*)c.pullV);
-            LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);
+            static const bool split = std::getenv("LOVE_PULL_MF") != nullptr && std::atoi(std::getenv("LOVE_PULL_MF")) == 0;
+            if (split) {
+                LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g,
+                            (const double*)c.pullT, ref, (double*)c.pullV);
+                LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);
+            } else {
+                LOVE_LAUNCH(pull_mid_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
+            }
         }
         return;
     }
