@@ -31,6 +31,52 @@ struct DoneScope {
     ~DoneScope() { t_done = prev; }
 };
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+// ---- in-pipeline kernel trace (liblove_trace.so with LOVE_TRACE=1): per (step j, kernel id) the
+// earliest CTA start after griddepcontrol.wait, from %globaltimer (ns), recorded by thread 0 of
+// every CTA (a kernel's slot = the next kernel's start - its start; start only, so that the
+// streaming kernels keep their register allocation).  Each translation unit holds its own device pointer
+// (LOVE_TRACE_TU), bound stream-ordered around the Lanczos replays; nullptr = off (one load
+// and a branch per CTA).
+constexpr int kTraceKernels = 16;
+enum TraceKid {
+    kTrMoments = 0, kTrPullLast = 1, kTrPullMid = 2, kTrPullFirst = 3, kTrFft0 = 4, kTrFft1 = 5, kTrFft2 = 6,
+    kTrGather = 7, kTrDots0 = 8, kTrUpdate0 = 9, kTrDots1 = 10, kTrUpdate1 = 11, kTrNodepass = 12,
+    kTrArrive = 13, kTrAdvanced = 14   // update's CTAs at the step counter [first, last]; the last CTA done
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_start(unsigned long long* base, int kid, int j) {
+    if (base != nullptr && threadIdx.x == 0 && threadIdx.y == 0)
+        atomicMin(base + ((size_t)j * kTraceKernels + kid) * 2, gtimer());
+}
+__device__ __forceinline__ void trace_arrive(unsigned long long* base, int kid, int j) {
+    if (base != nullptr && threadIdx.x == 0 && threadIdx.y == 0) {
+        const unsigned long long t = gtimer();
+        atomicMin(base + ((size_t)j * kTraceKernels + kid) * 2, t);
+        atomicMax(base + ((size_t)j * kTraceKernels + kid) * 2 + 1, t);
+    }
+}
+#define LOVE_TRACE_TU(name)                                                                   \
+    static __device__ unsigned long long* g_love_trace = nullptr;                            \
+    void trace_bind_##name(unsigned long long* p, cudaStream_t s) {                          \
+        cudaMemcpyToSymbolAsync(g_love_trace, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s); \
+    }
+// compiled in only for the measurement build (make trace -> liblove_trace.so, -DLOVE_TRACE_ON)
+#ifdef LOVE_TRACE_ON
+#define LOVE_TRACE(kid, j) ::love::trace_start(g_love_trace, (kid), (j))
+#define LOVE_TRACE_ARRIVE(kid, j) ::love::trace_arrive(g_love_trace, (kid), (j))
+#else
+#define LOVE_TRACE(kid, j) \
+    do {                   \
+    } while (0)
+#define LOVE_TRACE_ARRIVE(kid, j) \
+    do {                          \
+    } while (0)
+#endif
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>

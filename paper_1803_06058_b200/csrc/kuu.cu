@@ -21,6 +21,8 @@
 
 namespace love {
 
+LOVE_TRACE_TU(kuu)
+
 namespace {
 
 using C = double2;
@@ -160,6 +162,7 @@ __global__ void fft_small_kernel(const double* __restrict__ u, const double* __r
                                  const C* __restrict__ tw, const double* __restrict__ lam, double* __restrict__ z,
                                  C* __restrict__ outc, int mode, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft0, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -199,6 +202,7 @@ template <int G, int EPT>
 __global__ void fft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
                                  const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft0, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -233,6 +237,7 @@ __global__ void fft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __r
                                  const C* __restrict__ tw2, const C* __restrict__ twF,
                                  const double* __restrict__ lamB, C* __restrict__ outc, int mode, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft1, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -283,6 +288,7 @@ template <int G, int EPT>
 __global__ void fft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
                                  double* __restrict__ z, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft2, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -322,6 +328,7 @@ template <int G>
 __global__ void rfft_passA_kernel(const double* __restrict__ u, const double* __restrict__ Mc, int m, int N1, int N2,
                                   const C* __restrict__ tw2, const C* __restrict__ twF, C* __restrict__ Y, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft0, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -362,6 +369,7 @@ __global__ void rfft_passB_kernel(C* __restrict__ Y, int N1, int N2, const C* __
                                   const C* __restrict__ tw2, const C* __restrict__ twF, const C* __restrict__ twU1,
                                   const C* __restrict__ twU2, const double* __restrict__ lamN, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft1, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -436,6 +444,7 @@ template <int G>
 __global__ void rfft_passC_kernel(const C* __restrict__ Y, int m, int N1, int N2, const C* __restrict__ tw2,
                                   double* __restrict__ z, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(kTrFft2, done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -556,6 +565,7 @@ __global__ void axis_conv_kernel(const double* __restrict__ in, double* __restri
                                  const C* __restrict__ tw, int L, int I, int64_t O, int N, int P, int64_t npairs,
                                  double scale, const int* __restrict__ done) {
     pdl_wait();
+    LOVE_TRACE(O == 1 ? kTrFft0 : (LFAST ? kTrFft2 : kTrFft1), done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
     extern __shared__ __align__(16) unsigned char smraw[];
     C* tws = (C*)smraw;
@@ -668,11 +678,10 @@ inline int ilog2(int64_t x) {
 }
 
 constexpr int kSmallFFT = 4096;
-constexpr int kLinesPerCta = 2;
 
 // convolution (mode 0) of u (m entries) or forward FFT (mode 1) of u (N entries)
-// complex four-step passes with G lines per CTA (mode 0: convolution, mode 1: forward only)
-template <int G, int EPT>
+// complex four-step passes: GA columns per CTA in passes A / C, GB lines per CTA in pass B
+template <int GA, int GB, int EPT>
 static void fft_four_step(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc,
                           int mode, cudaStream_t s) {
     const int N1 = c.fft_N1, N2 = c.fft_N2;
@@ -680,15 +689,31 @@ static void fft_four_step(const Cache& c, const double* u, const double* Mc, int
     const C* tw2 = (const C*)c.tw2;
     const C* twF = (const C*)c.twF;
     const double* lam = (const double*)c.lam;
-    const size_t smA = sizeof(C) * (padded((size_t)G * N2) + N2), smB = sizeof(C) * (padded((size_t)G * N1) + N1);
-    ensure_smem((const void*)fft_passA_kernel<G, EPT>, smA);
-    ensure_smem((const void*)fft_passB_kernel<G, EPT>, smB);
-    ensure_smem((const void*)fft_passC_kernel<G, EPT>, smA);
-    LOVE_LAUNCH((fft_passA_kernel<G, EPT>), N1 / G, G * N2 / EPT, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
-    LOVE_LAUNCH((fft_passB_kernel<G, EPT>), N2 / G, G * N1 / EPT, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc, mode,
-                t_done);
+    const size_t smA = sizeof(C) * (padded((size_t)GA * N2) + N2), smB = sizeof(C) * (padded((size_t)GB * N1) + N1);
+    ensure_smem((const void*)fft_passA_kernel<GA, EPT>, smA);
+    ensure_smem((const void*)fft_passB_kernel<GB, EPT>, smB);
+    ensure_smem((const void*)fft_passC_kernel<GA, EPT>, smA);
+    LOVE_LAUNCH((fft_passA_kernel<GA, EPT>), N1 / GA, GA * N2 / EPT, smA, s, u, Mc, m, N1, N2, tw2, twF, work, t_done);
+    LOVE_LAUNCH((fft_passB_kernel<GB, EPT>), N2 / GB, GB * N1 / EPT, smB, s, work, N1, N2, tw1, tw2, twF, lam, outc,
+                mode, t_done);
     if (mode == 0)
-        LOVE_LAUNCH((fft_passC_kernel<G, EPT>), N1 / G, G * N2 / EPT, smA, s, (const C*)work, m, N1, N2, tw2, z, t_done);
+        LOVE_LAUNCH((fft_passC_kernel<GA, EPT>), N1 / GA, GA * N2 / EPT, smA, s, (const C*)work, m, N1, N2, tw2, z,
+                    t_done);
+}
+
+// measurement switches: LOVE_FFT_GA / LOVE_FFT_GB (lines per CTA, EPT = 4 convolution only)
+template <int EPT>
+static bool fft_four_step_env(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc,
+                              int mode, cudaStream_t s) {
+    static const int ga = std::getenv("LOVE_FFT_GA") ? std::atoi(std::getenv("LOVE_FFT_GA")) : 0;
+    static const int gb = std::getenv("LOVE_FFT_GB") ? std::atoi(std::getenv("LOVE_FFT_GB")) : 0;
+    if (ga == 0 || gb == 0 || mode != 0 || EPT != 4) return false;
+#define LOVE_FS(A_, B_) \
+    if (ga == A_ && gb == B_) { fft_four_step<A_, B_, EPT>(c, u, Mc, m, z, work, outc, mode, s); return true; }
+    LOVE_FS(1, 1) LOVE_FS(1, 2) LOVE_FS(1, 4) LOVE_FS(2, 1) LOVE_FS(2, 2) LOVE_FS(2, 4) LOVE_FS(4, 1) LOVE_FS(4, 2)
+    LOVE_FS(4, 4) LOVE_FS(8, 1) LOVE_FS(8, 2) LOVE_FS(8, 4) LOVE_FS(16, 1) LOVE_FS(16, 2)
+#undef LOVE_FS
+    return false;
 }
 
 void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z, C* work, C* outc, int mode,
@@ -709,7 +734,7 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
         }
         return;
     }
-    constexpr int G = kLinesPerCta;
+    constexpr int G = 2;
     if (mode == 0 && c.rfft_N1 != 0) {          // real-input half-length convolution
         const int R1 = c.rfft_N1, R2 = c.rfft_N2;
         const C* r1 = (const C*)c.rtw1;
@@ -732,12 +757,13 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
     // setup keeps radix 8
     static const int ept = std::getenv("LOVE_FFT_EPT") ? std::atoi(std::getenv("LOVE_FFT_EPT")) : 4;
     const bool e4 = ept == 4 && mode == 0;
+    if (e4 && fft_four_step_env<4>(c, u, Mc, m, z, work, outc, mode, s)) return;
     if (N <= (1 << 15)) {
-        if (e4) fft_four_step<4, 4>(c, u, Mc, m, z, work, outc, mode, s);
-        else fft_four_step<4, 8>(c, u, Mc, m, z, work, outc, mode, s);
+        if (e4) fft_four_step<4, 4, 4>(c, u, Mc, m, z, work, outc, mode, s);
+        else fft_four_step<4, 4, 8>(c, u, Mc, m, z, work, outc, mode, s);
     } else {
-        if (e4) fft_four_step<G, 4>(c, u, Mc, m, z, work, outc, mode, s);
-        else fft_four_step<G, 8>(c, u, Mc, m, z, work, outc, mode, s);
+        if (e4) fft_four_step<G, G, 4>(c, u, Mc, m, z, work, outc, mode, s);
+        else fft_four_step<G, G, 8>(c, u, Mc, m, z, work, outc, mode, s);
     }
 }
 
@@ -862,7 +888,9 @@ void setup_kuu(Cache& c, cudaStream_t s) {
         LOVE_LAUNCH(twiddle_table_kernel, (int)ceil_div(N, 256), 256, 0, s, (C*)c.tw1, N, N);
     } else {
         const int lg = ilog2(N);
-        c.fft_N1 = 1 << (lg / 2);
+        // N1 = 2^(lg/2) (LOVE_FFT_LG1: measurement switch)
+        const int lg1 = std::getenv("LOVE_FFT_LG1") ? std::atoi(std::getenv("LOVE_FFT_LG1")) : lg / 2;
+        c.fft_N1 = 1 << lg1;
         c.fft_N2 = N / c.fft_N1;
         c.tw1 = dalloc(c, sizeof(C) * c.fft_N1, s);
         c.tw2 = dalloc(c, sizeof(C) * c.fft_N2, s);

@@ -26,6 +26,8 @@
 #define LOVE_UPD_B 8
 #endif
 namespace love {
+
+LOVE_TRACE_TU(lanczos)
 constexpr int kUpdB = LOVE_UPD_B;
 constexpr int kCondSteps = 2;
 template <typename V> int update_grid(int64_t nchunks, size_t smem, int cg);
@@ -164,11 +166,19 @@ __device__ __forceinline__ void load_src(const V* __restrict__ Q, int64_t ldq, c
 // 8; the 8 per-lane partials of a block are reduced across the warp by a butterfly
 // reduce-scatter (xor 4, 2, 1: 7 shuffles) plus xor 8, 16, after which lane l holds column
 // 8b + (l & 7) summed over the warp; lanes 0..7 park it in shared memory (fp64).
+// (trace build: held at the production 32 registers, 8 CTAs per SM)
+#ifdef LOVE_TRACE_ON
+#define LOVE_DOTS_BOUNDS __launch_bounds__(256, 8)
+#else
+#define LOVE_DOTS_BOUNDS __launch_bounds__(256)
+#endif
 template <typename V, int CPT>
-__global__ void __launch_bounds__(256) reorth_dots_sweep_kernel(const V* __restrict__ Q, int64_t ldq, int k, int pass,
+__global__ void LOVE_DOTS_BOUNDS reorth_dots_sweep_kernel(const V* __restrict__ Q, int64_t ldq, int k, int pass,
                                                                 const V* __restrict__ r, LanczosState st,
                                                                 const int* __restrict__ gate) {
     pdl_wait();
+    LOVE_TRACE(pass == 0 ? kTrDots0 : kTrDots1, *st.jdev);
+    if (sizeof(V) == 8 && st.dgks && pass == 1 && st.flags[7]) return;   // DGKS: the step has advanced
     constexpr int W = VecT<V>::W;
     extern __shared__ __align__(16) double smd[];
     const int j = *st.jdev;
@@ -282,6 +292,7 @@ template <typename V>
 __global__ void __launch_bounds__(256) reorth_dots3_kernel(const V* __restrict__ Q, int64_t ldq, int k,
                                                            const V* __restrict__ r, LanczosState st) {
     pdl_wait();
+    LOVE_TRACE(kTrDots0, *st.jdev);
     constexpr int W = VecT<V>::W;
     extern __shared__ __align__(16) double smd[];
     const int j = *st.jdev;
@@ -378,52 +389,59 @@ __global__ void clear_acc_kernel(LanczosState st, int k) {
 // Scalars of index i once alpha_i and beta_i^2 are complete (same rules as the prologue):
 // alpha_i, row i of the Cholesky of T, g_i = (L^{-1} e_1)_i, beta_i, the
 // breakdown test (reading A12) and the scale of q_{i+1}.  One thread.
-__device__ __forceinline__ void finalize_index(const LanczosState& st, int i, int k, double tol) {
+// (returns true when the Lanczos stops here or had stopped).  Every input is loaded before the
+// first use: the step's serial tail pays one memory round trip for them, not one per use.
+__device__ __forceinline__ bool finalize_index(const LanczosState& st, int i, int k, double tol) {
     int* fl = st.flags;
-    if (fl[1] <= i || fl[2] || fl[3]) return;
-    const double al = st.alpha_cur[0];
-    const double amax = fmax(st.amax_bmax[0], fabs(al));
+    const int f0 = fl[0], f1 = fl[1], f2 = fl[2], f3 = fl[3];
+    const double al = st.alpha_cur[0], am0 = st.amax_bmax[0], bm0 = st.amax_bmax[1], b2 = st.beta2_cur[0];
+    const double lsub = (st.chol && i > 0) ? st.Ls[i - 1] : 0.0;
+    const double gprev = (st.chol && i > 0) ? st.g[i - 1] : 0.0;
+    if (f1 <= i || f2 || f3) return f0 != 0;
+    const double amax = fmax(am0, fabs(al));
     double ld = 1.0;
     if (st.chol) {                                  // row i of the Cholesky of T
-        const double lsub = i > 0 ? st.Ls[i - 1] : 0.0;
         const double piv = al - lsub * lsub;
         if (!(piv > 0.0)) {
             fl[2] = 1;
             fl[0] = 1;
             fl[1] = i;
-            return;
+            return true;
         }
         ld = sqrt(piv);
         st.Ld[i] = ld;
-        st.g[i] = (i == 0) ? 1.0 / ld : -lsub * st.g[i - 1] / ld;
+        st.g[i] = (i == 0) ? 1.0 / ld : -lsub * gprev / ld;
     }
     st.alpha[i] = al;
     st.amax_bmax[0] = amax;
     if (i + 1 == k) {
         fl[0] = 1;
         fl[1] = k;
-        return;
+        return true;
     }
-    const double b = sqrt(st.beta2_cur[0]);
-    const double bmax = fmax(st.amax_bmax[1], b);
+    const double b = sqrt(b2);
+    const double bmax = fmax(bm0, b);
     st.amax_bmax[1] = bmax;
     if (!(b >= tol * (amax + 2.0 * bmax))) {
         fl[0] = 1;
         fl[1] = i + 1;
-    } else {
-        st.beta[i] = b;
-        if (st.chol) st.Ls[i] = b / ld;
-        st.qscale[i + 1] = 1.0 / b;
+        return true;
     }
+    st.beta[i] = b;
+    if (st.chol) st.Ls[i] = b / ld;
+    st.qscale[i + 1] = 1.0 / b;
+    return f0 != 0;
 }
 
 // Last-CTA-done step advance (every CTA calls it once at its end): the last CTA optionally
 // finalises the scalars of index j (single GPU: beta_j^2 is complete once every CTA of the
 // update has added its part) and writes j + 1 to the step index.
-__device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
-                                             double tol = 0.0) {
+
+// true in the last CTA of the grid to get here (every CTA calls it once)
+__device__ __forceinline__ bool last_cta(const LanczosState& st) {
     __shared__ int last;
     __syncthreads();
+    LOVE_TRACE_ARRIVE(kTrArrive, *st.jdev);
     if (threadIdx.x == 0) {
         __threadfence();
         const unsigned prev = atomicAdd(reinterpret_cast<unsigned*>(st.step_ctr), 1u);
@@ -431,30 +449,65 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
         if (last) __threadfence();
     }
     __syncthreads();
-    if (!last) return;
-    if (fin) {
-        if (threadIdx.x == 0) finalize_index(st, j, k, tol);
-        __syncthreads();                             // scalars read before the accumulators clear
+    return last != 0;
+}
+
+// the last CTA's part of advance_step.  No trailing fence: the next kernel reads these after
+// griddepcontrol.wait (the grid has completed and its writes are visible); only the host's
+// mapped done flag needs the system fence.
+__device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bool fin, int k, double tol) {
+    if (fin)   // the reorthogonalisation dot accumulators (the scalars do not read them)
         for (int64_t i = threadIdx.x; i < st.c_len; i += blockDim.x) st.c_cur[i] = 0.0;
-    }
     if (threadIdx.x == 0) {
+        bool done;
         if (fin) {
+            done = finalize_index(st, j, k, tol);
             st.alpha_cur[0] = 0.0;
             st.beta2_cur[0] = 0.0;
             if (st.nrm2 != nullptr) st.nrm2[0] = st.nrm2[1] = 0.0;
+        } else {
+            done = st.flags[0] != 0;
         }
-        if (st.hdone != nullptr && st.flags[0]) {    // tell the host to stop replaying
+        if (st.hdone != nullptr && done) {           // tell the host to stop replaying
             *(volatile int*)st.hdone = 1;
             __threadfence_system();
         }
+        LOVE_TRACE(kTrAdvanced, j);
         st.step_ctr[0] = 0;
         st.jdev[0] = j + 1;
         if (st.cond != 0) {                          // inside the WHILE graph node
             st.flags[6] += 1;
-            if (st.flags[0] || j + 1 >= st.cond_limit) cudaGraphSetConditional(st.cond, 0);
+            if (done || j + 1 >= st.cond_limit) cudaGraphSetConditional(st.cond, 0);
         }
-        __threadfence();
     }
+}
+
+__device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
+                                             double tol = 0.0) {
+    if (last_cta(st)) advance_finish(st, j, fin, k, tol);
+}
+
+// DGKS-gated CGS2 (fp64, one GPU): the last CTA of the FIRST pass's update decides.  If
+// ||r''||^2 >= ||r'||^2 / 2 the second pass is not needed: beta_j^2 = ||r''||^2 and the step
+// advances right here; flags[7] = 1 tells the second pass's two kernels of this step to return
+// at once (no grid-wide step counter, no scalars).  Otherwise flags[7] = 0 and the second pass
+// runs and advances as before.
+__device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool fin, int k, double tol) {
+    if (!last_cta(st)) return;
+    const bool skip = !(st.nrm2[1] < 0.5 * st.nrm2[0]);
+    if (!skip) {
+        if (threadIdx.x == 0) {
+            st.flags[7] = 0;
+            st.step_ctr[0] = 0;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) {
+        st.beta2_cur[0] = st.nrm2[1];
+        st.flags[7] = 1;
+    }
+    __syncthreads();
+    advance_finish(st, j, fin, k, tol);
 }
 
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
@@ -468,14 +521,18 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
                                                             LanczosState st, double tol, int fold,
                                                             const int* __restrict__ gate) {
     pdl_wait();
+    LOVE_TRACE(pass == 0 ? kTrUpdate0 : kTrUpdate1, *st.jdev);
     constexpr int W = VecT<V>::W;
     extern __shared__ double cf[];             // [j+1] coefficient of Q~[:, i], as V
     V* __restrict__ cfv = reinterpret_cast<V*>(cf);
     __shared__ double red[32];
+    // DGKS: the first pass's update already advanced the step (dgks_decide)
+    if (sizeof(V) == 8 && st.dgks && pass == 1 && st.flags[7]) return;
     const int j = *st.jdev;
     // the last pass's update is the last kernel of step j: its last CTA to finish advances
     // the device step index (every CTA has read j by then), also on the early-exit paths
     if (st.flags[0] || j >= k - 1) {
+        if (sizeof(V) == 8 && st.dgks && pass == 0 && blockIdx.x == 0 && threadIdx.x == 0) st.flags[7] = 0;
         // one-sync step: alpha of the last step comes from the dots vector (no gather partials)
         if ((mode & kUpd1Sync) && !st.flags[0] && j == k - 1 && blockIdx.x == 0 && threadIdx.x == 0)
             st.alpha_cur[0] = st.c_cur[j];
@@ -634,6 +691,9 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         if (threadIdx.x == 0) atomicAdd(beta2_out, b2);
     }
     if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
+    if constexpr (sizeof(V) == 8) {
+        if (st.dgks == 2 && pass == 0 && !(mode & kUpdAdvance)) dgks_decide(st, j, fold != 0, k, tol);
+    }
 }
 
 // Rc (fp64, m x k_eff column-major) -> V, m x k_pad row-major (zero padded)
@@ -911,6 +971,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(init_q0_kernel, 1, 32, 0, s, st);
     }
+    trace_begin(c, pl.k, s);
     // the step graph is also captured on several GPUs: its all-reduces have fixed addresses
     const bool graph = !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr;
     // one GPU: early stop of the replays at breakdown (the device sets a mapped host flag; on
@@ -1011,6 +1072,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
         for (int j = 0; j < pl.k; ++j) enqueue_step<V>(pl, j, s);
     }
     c.st.hdone = nullptr;
+    if (c.trace != nullptr) trace_end(s);
     if (pl.fold) {   // the last streamed column (its scalars were finalised by the last update)
         ProfScope ps(LOVE_PROF_SCALARS, s);
         LOVE_LAUNCH(stream_rc_kernel, pl.gm, 256, 0, s, pl.rs);

@@ -364,7 +364,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         if (c->reorth_passes == 2 && c->precision == LOVE_FP64 && c->comm == nullptr && !c->partial && !c->fused &&
             std::getenv("LOVE_NO_DGKS") == nullptr) {
             st.nrm2 = (double*)dalloc(*c, sizeof(double) * 2, s);
-            st.dgks = 1;
+            st.dgks = std::getenv("LOVE_DGKS_LATE") ? 1 : 2;   // 2: the first pass decides (dgks_decide)
         }
         if (c->comm == nullptr) {                        // one GPU: spread the dot atomics
             st.crep = 4;                                 // measured: 4 beats 8 and 16 (cfg2, cfg3)
@@ -401,6 +401,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
     host_mark("lanczos_sync");
     c->range_flag = nullptr;
     if (*hrange) throw LoveError{LOVE_ERR_RANGE, "a training point needs a grid node outside the grid"};
+    trace_report(*c, hfl[1]);
     const double bn2 = *hbn;
     cuda_check(cudaGetLastError(), "lanczos kernels");
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "the Lanczos probe vector is zero"};

@@ -210,6 +210,7 @@ struct Cache {
     std::vector<double> h_evals;         // eigenvalues of T' (sampling cache)
 
     std::vector<void*> allocs;           // everything to release
+    unsigned long long* trace = nullptr; // LOVE_TRACE: [k][kTraceKernels][start, end] (ns)
     char* slab = nullptr;                // small buffers are carved from zeroed slabs (dalloc)
     size_t slab_used = 0;
 };
@@ -300,6 +301,14 @@ void run_lanczos_fused(Cache& c, cudaStream_t s);   // lanczos_fused.cu
 void setup_fused(Cache& c, cudaStream_t s);
 void finish_cache(Cache& c, cudaStream_t s);    // Rc -> row-major m x k_pad
 void launch_rc_rows64(const Cache& c, double* out, cudaStream_t s);   // fp64 row-major Rc (m x k_pad)
+// in-pipeline kernel trace (LOVE_TRACE=1, common.cuh): per-translation-unit binders, and the
+// build-side driver (trace_begin before the Lanczos replays, trace_report after its sync)
+void trace_bind_ski(unsigned long long* p, cudaStream_t s);
+void trace_bind_kuu(unsigned long long* p, cudaStream_t s);
+void trace_bind_lanczos(unsigned long long* p, cudaStream_t s);
+void trace_begin(Cache& c, int k, cudaStream_t s);
+void trace_end(cudaStream_t s);
+void trace_report(Cache& c, int k_eff);
 void avgcol_probe(Cache& c, cudaStream_t s);    // Q~[:, 0] = (1/m) W^T K_UU 1   (probe avg)
 void mean_cache_eq4(Cache& c, cudaStream_t s);  // a = Rc L^{-1} Q^T y after the Lanczos loop
 // query.cu

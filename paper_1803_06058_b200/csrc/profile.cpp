@@ -1,6 +1,7 @@
 // profile.cpp -- phase timing with CUDA events on the launching stream (love_profile_*).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -44,6 +45,99 @@ thread_local cudaEvent_t t_open[LOVE_PROF_N] = {nullptr};
 }  // namespace
 
 bool profiling() { return prof().on; }
+
+// ---- in-pipeline kernel trace (LOVE_TRACE=1, common.cuh)
+void trace_begin(Cache& c, int k, cudaStream_t s) {
+#ifdef LOVE_TRACE_ON
+    static const bool on = std::getenv("LOVE_TRACE") != nullptr;
+#else
+    const bool on = false;
+#endif
+    if (!on || k < 1) return;
+    const size_t rows = (size_t)k * kTraceKernels;
+    c.trace = (unsigned long long*)dalloc_unset(c, rows * 2 * sizeof(unsigned long long), s);
+    cuda_check(cudaMemsetAsync(c.trace, 0, rows * 2 * sizeof(unsigned long long), s), "trace memset");
+    cuda_check(cudaMemset2DAsync(c.trace, 2 * sizeof(unsigned long long), 0xff, sizeof(unsigned long long), rows, s),
+               "trace memset");
+    trace_bind_ski(c.trace, s);
+    trace_bind_kuu(c.trace, s);
+    trace_bind_lanczos(c.trace, s);
+}
+
+void trace_end(cudaStream_t s) {
+    trace_bind_ski(nullptr, s);
+    trace_bind_kuu(nullptr, s);
+    trace_bind_lanczos(nullptr, s);
+}
+
+// One JSON line on stderr: per kernel id its mean slot (its first CTA start after the wait to
+// the next kernel's first start, the next step's first kernel for the last one), over the steps
+// 2 .. k_eff - 3, and the mean step period.
+void trace_report(Cache& c, int k_eff) {
+    if (c.trace == nullptr) return;
+    static const char* names[kTraceKernels] = {"moments", "pull_last", "pull_mid", "pull_first", "fft0", "fft1",
+                                               "fft2", "gather", "dots0", "update0", "dots1", "update1",
+                                               "nodepass", "k13", "k14", "k15"};
+    const int k = k_eff;
+    std::vector<unsigned long long> h((size_t)k * kTraceKernels * 2);
+    cuda_check(cudaMemcpy(h.data(), c.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+               "trace d2h");
+    const unsigned long long kNone = ~0ull;
+    auto starts = [&](int j) {
+        std::vector<std::pair<unsigned long long, int>> o;
+        const unsigned long long* r = h.data() + (size_t)j * kTraceKernels * 2;
+        for (int q = 0; q < kTraceKernels; ++q)
+            if (r[2 * q] != kNone && q != kTrArrive && q != kTrAdvanced) o.push_back({r[2 * q], q});
+        std::sort(o.begin(), o.end());
+        return o;
+    };
+    double slot[kTraceKernels] = {0};
+    int cnt[kTraceKernels] = {0};
+    double period = 0.0;
+    int np = 0;
+    // the step's advancing update: its start -> first CTA at the counter -> last CTA at the
+    // counter -> the last CTA's scalars done -> the next step's first kernel start
+    double adv[4] = {0, 0, 0, 0};
+    int na = 0;
+    for (int j = 2; j + 3 < k; ++j) {
+        const auto o = starts(j), on = starts(j + 1);
+        if (o.empty() || on.empty()) continue;
+        const unsigned long long* r = h.data() + (size_t)j * kTraceKernels * 2;
+        if (r[2 * kTrArrive] != kNone && r[2 * kTrAdvanced] != kNone) {
+            const unsigned long long us = o.back().first;      // the last kernel of the step
+            adv[0] += (double)((long long)r[2 * kTrArrive] - (long long)us);
+            adv[1] += (double)(r[2 * kTrArrive + 1] - r[2 * kTrArrive]);
+            adv[2] += (double)((long long)r[2 * kTrAdvanced] - (long long)r[2 * kTrArrive + 1]);
+            adv[3] += (double)((long long)on[0].first - (long long)r[2 * kTrAdvanced]);
+            ++na;
+        }
+        for (size_t i = 0; i < o.size(); ++i) {
+            const unsigned long long nxt = i + 1 < o.size() ? o[i + 1].first : on[0].first;
+            slot[o[i].second] += (double)(nxt - o[i].first);
+            cnt[o[i].second] += 1;
+        }
+        period += (double)(on[0].first - o[0].first);
+        ++np;
+    }
+    std::string out = "{\"trace\": {\"steps\": " + std::to_string(np) + ", \"period_us\": " +
+                      std::to_string(np ? period / np / 1000.0 : 0.0) + ", \"slot_us\": {";
+    bool first = true;
+    for (int q = 0; q < kTraceKernels; ++q) {
+        if (!cnt[q]) continue;
+        out += std::string(first ? "" : ", ") + "\"" + names[q] + "\": " + std::to_string(slot[q] / cnt[q] / 1000.0);
+        first = false;
+    }
+    out += "}";
+    if (na)
+        out += ", \"advance_us\": {\"to_first_arrival\": " + std::to_string(adv[0] / na / 1000.0) +
+               ", \"arrival_spread\": " + std::to_string(adv[1] / na / 1000.0) + ", \"last_cta_scalars\": " +
+               std::to_string(adv[2] / na / 1000.0) + ", \"to_next_kernel\": " + std::to_string(adv[3] / na / 1000.0) +
+               "}";
+    out += "}}";
+    std::fprintf(stderr, "%s\n", out.c_str());
+    c.trace = nullptr;                           // the buffer stays with the cache's allocations
+}
+
 
 namespace {
 struct HostMarks {

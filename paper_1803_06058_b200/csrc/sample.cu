@@ -812,7 +812,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         st.chol = 0;
         if (std::getenv("LOVE_NO_DGKS") == nullptr) {   // DGKS-gated second CGS pass (lanczos.cu)
             st.nrm2 = (double*)dalloc(c, sizeof(double) * 2, s);
-            st.dgks = 1;
+            st.dgks = std::getenv("LOVE_DGKS_LATE") ? 1 : 2;   // 2: the first pass decides (dgks_decide)
         }
         LOVE_LAUNCH(samp_flags_kernel, 1, 32, 0, s, st.flags, ks);
     }

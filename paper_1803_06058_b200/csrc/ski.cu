@@ -19,6 +19,8 @@
 
 namespace love {
 
+LOVE_TRACE_TU(ski)
+
 namespace {
 
 constexpr int kBatch = 8;   // points loaded per batch (memory-level parallelism)
@@ -59,6 +61,7 @@ __global__ void LOVE_MOM_BOUNDS(D) moments_kernel(int64_t n_items, const int* __
                                                       const V* __restrict__ f2, const V* __restrict__ qbase,
                                                       StepRef ref, MT* __restrict__ M) {
     pdl_wait();
+    LOVE_TRACE(kTrMoments, step_j(ref));
     using A = typename AccT<V, D>::type;
     constexpr int S = Slots<D>::value;
     const int64_t it = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(256) moments2_tpc_kernel(int64_t n_items, cons
                                                            const V* __restrict__ qbase, StepRef ref,
                                                            double* __restrict__ M) {
     pdl_wait();
+    LOVE_TRACE(kTrMoments, step_j(ref));
     constexpr int B = 4;
     const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t it = gt >> 1;
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_ite
                                                         const MT* __restrict__ M, StepRef ref,
                                                         double* __restrict__ T) {
     pdl_wait();
+    LOVE_TRACE(kTrPullLast, step_j(ref));
     constexpr int SO = D == 2 ? 4 : 16;
     static_assert(SO % SG == 0, "slot groups");
     const int m = g.m_total;
@@ -225,6 +230,7 @@ __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_ite
 __global__ void __launch_bounds__(256) pull_mid_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
                                                        double* __restrict__ Vout) {
     pdl_wait();
+    LOVE_TRACE(kTrPullMid, step_j(ref));
     const int m = g.m_total;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= 4 * (int64_t)m || step_done(ref)) return;
@@ -243,6 +249,7 @@ __global__ void __launch_bounds__(256) pull_mid_kernel(GridDev g, const double* 
 __global__ void __launch_bounds__(256) pull_first_kernel(GridDev g, const double* __restrict__ X, StepRef ref,
                                                          double* __restrict__ u) {
     pdl_wait();
+    LOVE_TRACE(kTrPullFirst, step_j(ref));
     const int m = g.m_total;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= m || step_done(ref)) return;
@@ -263,6 +270,7 @@ __global__ void __launch_bounds__(256) pull_first_kernel(GridDev g, const double
 __global__ void __launch_bounds__(256) pull_mid_first_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
                                                              double* __restrict__ u) {
     pdl_wait();
+    LOVE_TRACE(kTrPullMid, step_j(ref));
     const int m = g.m_total;
     const int x = blockIdx.x * blockDim.x + threadIdx.x;
     if (x >= m || step_done(ref)) return;
@@ -308,6 +316,7 @@ __global__ void LOVE_GATHER_BOUNDS(D) gather_kernel(GridDev g, int64_t n_items,
                                                      V* __restrict__ r, double* __restrict__ alpha_base,
                                                      RcStream rs, int ngather) {
     pdl_wait();
+    LOVE_TRACE(kTrGather, step_j(ref));
     if ((int)blockIdx.x >= ngather) {          // extra CTAs: the streamed cache column (last: the
         // d >= 2 gather is the longer job, its CTAs go first)
         stream_rc_column(rs, (blockIdx.x - ngather) * blockDim.x + threadIdx.x, (gridDim.x - ngather) * blockDim.x);
@@ -420,6 +429,7 @@ __global__ void __launch_bounds__(256) gather_pts1_kernel(GridDev g, int64_t n, 
                                                           V* __restrict__ r, double* __restrict__ alpha_base,
                                                           RcStream rs, int nstream) {
     pdl_wait();
+    LOVE_TRACE(kTrGather, step_j(ref));
     // the first nstream CTAs stream the cache column (they start first and overlap the gather)
     if ((int)blockIdx.x < nstream) {
         stream_rc_column(rs, blockIdx.x * blockDim.x + threadIdx.x, nstream * blockDim.x);
@@ -471,6 +481,7 @@ __global__ void __launch_bounds__(256) moments_cell1_kernel(int m, const int* __
                                                             const V* __restrict__ f0, const V* __restrict__ qbase,
                                                             StepRef ref, double* __restrict__ Mc) {
     pdl_wait();
+    LOVE_TRACE(kTrMoments, step_j(ref));
     // TPC lanes per cell (aligned lane groups): lane `sub` takes points p0 + sub, p0 + sub + TPC, ...
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int c = gt / TPC, sub = gt % TPC;
@@ -512,6 +523,7 @@ __global__ void __launch_bounds__(256) moments_cell1_kernel(int m, const int* __
 __global__ void __launch_bounds__(256) nodepass_cell1_kernel(int m, const double* __restrict__ Mc, StepRef ref,
                                                              double* __restrict__ u) {
     pdl_wait();
+    LOVE_TRACE(kTrNodepass, step_j(ref));
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m || step_done(ref)) return;
     const int ld = m + 4;
