@@ -391,12 +391,29 @@ __global__ void clear_acc_kernel(LanczosState st, int k) {
 // breakdown test (reading A12) and the scale of q_{i+1}.  One thread.
 // (returns true when the Lanczos stops here or had stopped).  Every input is loaded before the
 // first use: the step's serial tail pays one memory round trip for them, not one per use.
-__device__ __forceinline__ bool finalize_index(const LanczosState& st, int i, int k, double tol) {
+struct FinIn {                                     // finalize_index's inputs other than beta^2
+    int f0, f1, f2, f3;
+    double al, am0, bm0, lsub, gprev;
+};
+__device__ __forceinline__ FinIn fin_inputs(const LanczosState& st, int i) {
+    const int* fl = st.flags;
+    FinIn f;
+    f.f0 = fl[0];
+    f.f1 = fl[1];
+    f.f2 = fl[2];
+    f.f3 = fl[3];
+    f.al = st.alpha_cur[0];
+    f.am0 = st.amax_bmax[0];
+    f.bm0 = st.amax_bmax[1];
+    f.lsub = (st.chol && i > 0) ? st.Ls[i - 1] : 0.0;
+    f.gprev = (st.chol && i > 0) ? st.g[i - 1] : 0.0;
+    return f;
+}
+__device__ __forceinline__ bool finalize_index(const LanczosState& st, int i, int k, double tol, const FinIn& in) {
     int* fl = st.flags;
-    const int f0 = fl[0], f1 = fl[1], f2 = fl[2], f3 = fl[3];
-    const double al = st.alpha_cur[0], am0 = st.amax_bmax[0], bm0 = st.amax_bmax[1], b2 = st.beta2_cur[0];
-    const double lsub = (st.chol && i > 0) ? st.Ls[i - 1] : 0.0;
-    const double gprev = (st.chol && i > 0) ? st.g[i - 1] : 0.0;
+    const int f0 = in.f0, f1 = in.f1, f2 = in.f2, f3 = in.f3;
+    const double al = in.al, am0 = in.am0, bm0 = in.bm0, b2 = st.beta2_cur[0];
+    const double lsub = in.lsub, gprev = in.gprev;
     if (f1 <= i || f2 || f3) return f0 != 0;
     const double amax = fmax(am0, fabs(al));
     double ld = 1.0;
@@ -455,13 +472,14 @@ __device__ __forceinline__ bool last_cta(const LanczosState& st) {
 // the last CTA's part of advance_step.  No trailing fence: the next kernel reads these after
 // griddepcontrol.wait (the grid has completed and its writes are visible); only the host's
 // mapped done flag needs the system fence.
-__device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bool fin, int k, double tol) {
+__device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bool fin, int k, double tol,
+                                               const FinIn& in) {
     if (fin)   // the reorthogonalisation dot accumulators (the scalars do not read them)
         for (int64_t i = threadIdx.x; i < st.c_len; i += blockDim.x) st.c_cur[i] = 0.0;
     if (threadIdx.x == 0) {
         bool done;
         if (fin) {
-            done = finalize_index(st, j, k, tol);
+            done = finalize_index(st, j, k, tol, in);
             st.alpha_cur[0] = 0.0;
             st.beta2_cur[0] = 0.0;
             if (st.nrm2 != nullptr) st.nrm2[0] = st.nrm2[1] = 0.0;
@@ -482,9 +500,13 @@ __device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bo
     }
 }
 
+// (thread 0 loads the scalar inputs before the step counter: their round trip overlaps the fence
+// and the counter's)
 __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
                                              double tol = 0.0) {
-    if (last_cta(st)) advance_finish(st, j, fin, k, tol);
+    FinIn in{};
+    if (fin && threadIdx.x == 0) in = fin_inputs(st, j);
+    if (last_cta(st)) advance_finish(st, j, fin, k, tol, in);
 }
 
 // DGKS-gated CGS2 (fp64, one GPU): the last CTA of the FIRST pass's update decides.  If
@@ -493,6 +515,8 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
 // at once (no grid-wide step counter, no scalars).  Otherwise flags[7] = 0 and the second pass
 // runs and advances as before.
 __device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool fin, int k, double tol) {
+    FinIn in{};
+    if (fin && threadIdx.x == 0) in = fin_inputs(st, j);
     if (!last_cta(st)) return;
     const bool skip = !(st.nrm2[1] < 0.5 * st.nrm2[0]);
     if (!skip) {
@@ -507,7 +531,7 @@ __device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool 
         st.flags[7] = 1;
     }
     __syncthreads();
-    advance_finish(st, j, fin, k, tol);
+    advance_finish(st, j, fin, k, tol, in);
 }
 
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
