@@ -8,6 +8,8 @@
 // kItemMax consecutive points of one cell: every later pass streams them in that order.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "love_internal.h"
 
 namespace love {
@@ -174,26 +176,32 @@ __global__ void gather_sorted_kernel(int d, const int* __restrict__ perm, int64_
     }
 }
 
-__global__ void items_per_cell_kernel(const int* __restrict__ start, int m_total, int* __restrict__ nit) {
+__global__ void items_per_cell_kernel(const int* __restrict__ start, int m_total, int* __restrict__ nit, int imax) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m_total) return;
-    nit[c] = (int)ceil_div(start[c + 1] - start[c], kItemMax);
+    nit[c] = (int)ceil_div(start[c + 1] - start[c], imax);
 }
 
 __global__ void build_items_kernel(const int* __restrict__ start, const int* __restrict__ item0,
                                    int m_total, int64_t n, int* __restrict__ item_cell,
-                                   int* __restrict__ item_start) {
+                                   int* __restrict__ item_start, int imax) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= m_total) return;
     const int b = start[c], e = start[c + 1];
     const int it0 = item0[c];
     // ceil(cnt / kItemMax) items of (nearly) equal size: the lanes of a warp loop alike
-    const int cnt = e - b, nit = (cnt + kItemMax - 1) / kItemMax;
+    const int cnt = e - b, nit = (cnt + imax - 1) / imax;
     for (int i = 0; i < nit; ++i) {
         item_cell[it0 + i] = c;
         item_start[it0 + i] = b + (int)((int64_t)i * cnt / nit);
     }
     if (c == m_total - 1) item_start[item0[m_total]] = (int)n;
+}
+
+// points per item: kItemMax (LOVE_ITEM_MAX = 1 .. kItemMax: measurement switch)
+inline int item_max() {
+    static const int v = std::getenv("LOVE_ITEM_MAX") ? std::atoi(std::getenv("LOVE_ITEM_MAX")) : kItemMax;
+    return v >= 1 && v <= kItemMax ? v : kItemMax;
 }
 
 inline int grid_for(int64_t n, int threads) {
@@ -242,7 +250,7 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
                         frac64, y, (float*)c.frac[0], (float*)c.frac[1], (float*)c.frac[2],
                         (float*)b_out, cell, c.pcell);
     }
-    LOVE_LAUNCH(items_per_cell_kernel, (int)ceil_div(M, 256), 256, 0, s, c.cell_start, M, count);
+    LOVE_LAUNCH(items_per_cell_kernel, (int)ceil_div(M, 256), 256, 0, s, c.cell_start, M, count, item_max());
     exclusive_scan(count, M, c.cell_item_start, s);
     cuda_check(cudaFreeAsync(count, s), "sort free");
 }
@@ -258,7 +266,7 @@ int64_t count_items_host(Cache& c, cudaStream_t s) {
 void launch_build_items(Cache& c, cudaStream_t s) {
     const int M = c.g.m_total;
     LOVE_LAUNCH(build_items_kernel, (int)ceil_div(M, 256), 256, 0, s, c.cell_start,
-                c.cell_item_start, M, c.n, c.item_cell, c.item_start);
+                c.cell_item_start, M, c.n, c.item_cell, c.item_start, item_max());
 }
 
 }  // namespace love
