@@ -42,7 +42,8 @@ constexpr int kTraceKernels = 16;
 enum TraceKid {
     kTrMoments = 0, kTrPullLast = 1, kTrPullMid = 2, kTrPullFirst = 3, kTrFft0 = 4, kTrFft1 = 5, kTrFft2 = 6,
     kTrGather = 7, kTrDots0 = 8, kTrUpdate0 = 9, kTrDots1 = 10, kTrUpdate1 = 11, kTrNodepass = 12,
-    kTrArrive = 13, kTrAdvanced = 14   // update's CTAs at the step counter [first, last]; the last CTA done
+    kTrArrive = 13, kTrAdvanced = 14,  // update's CTAs at the step counter [first, last]; the last CTA done
+    kTrSampV = 15                      // sampling Lanczos: v = z - Rc t (its step head is kTrMoments)
 };
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;

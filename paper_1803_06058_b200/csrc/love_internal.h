@@ -306,6 +306,7 @@ void launch_rc_rows64(const Cache& c, double* out, cudaStream_t s);   // fp64 ro
 void trace_bind_ski(unsigned long long* p, cudaStream_t s);
 void trace_bind_kuu(unsigned long long* p, cudaStream_t s);
 void trace_bind_lanczos(unsigned long long* p, cudaStream_t s);
+void trace_bind_sample(unsigned long long* p, cudaStream_t s);
 void trace_begin(Cache& c, int k, cudaStream_t s);
 void trace_end(cudaStream_t s);
 void trace_report(Cache& c, int k_eff);

@@ -62,12 +62,14 @@ void trace_begin(Cache& c, int k, cudaStream_t s) {
     trace_bind_ski(c.trace, s);
     trace_bind_kuu(c.trace, s);
     trace_bind_lanczos(c.trace, s);
+    trace_bind_sample(c.trace, s);
 }
 
 void trace_end(cudaStream_t s) {
     trace_bind_ski(nullptr, s);
     trace_bind_kuu(nullptr, s);
     trace_bind_lanczos(nullptr, s);
+    trace_bind_sample(nullptr, s);
 }
 
 // One JSON line on stderr: per kernel id its mean slot (its first CTA start after the wait to
@@ -77,7 +79,7 @@ void trace_report(Cache& c, int k_eff) {
     if (c.trace == nullptr) return;
     static const char* names[kTraceKernels] = {"moments", "pull_last", "pull_mid", "pull_first", "fft0", "fft1",
                                                "fft2", "gather", "dots0", "update0", "dots1", "update1",
-                                               "nodepass", "k13", "k14", "k15"};
+                                               "nodepass", "k13", "k14", "samp_v"};
     const int k = k_eff;
     std::vector<unsigned long long> h((size_t)k * kTraceKernels * 2);
     cuda_check(cudaMemcpy(h.data(), c.trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost),

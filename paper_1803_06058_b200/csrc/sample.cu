@@ -22,6 +22,8 @@
 
 namespace love {
 
+LOVE_TRACE_TU(sample)
+
 namespace {
 
 constexpr int kMaxKs = 112;          // k' limit of the single-CTA Jacobi eigensolver (smem)
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ 
                                                      LanczosState st, double* __restrict__ t_next) {
     __shared__ double psum[8][kSvRows];
     pdl_wait();
+    LOVE_TRACE(kTrSampV, *st.jdev);
     if (st.flags[0]) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r = blockIdx.x * kSvRows + lane;
@@ -534,6 +537,7 @@ __global__ void __launch_bounds__(256) samp_qcur_dots_kernel(LanczosState st, co
                                                              int m, const double* __restrict__ Rc, int ncol,
                                                              double* __restrict__ qcur, double* __restrict__ t) {
     pdl_wait();
+    LOVE_TRACE(kTrMoments, *st.jdev);
     if (st.flags[0]) return;
     __shared__ double xs[kDotRows];
     const int j = *st.jdev;
@@ -546,13 +550,26 @@ __global__ void __launch_bounds__(256) samp_qcur_dots_kernel(LanczosState st, co
         xs[i] = q;
     }
     __syncthreads();
+    // four columns per warp at a time: their loads and their warp reductions are independent
+    // chains (one column at a time left a load -> shuffle-reduce -> atomic chain per column)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int c = wid; c < ncol; c += nw) {
-        const double* a = Rc + (int64_t)c * m + r0;
-        double acc = 0.0;
-        for (int i = lane; i < nr; i += 32) acc += a[i] * xs[i];
-        acc = warp_sum(acc);
-        if (lane == 0) atomicAdd(&t[c], acc);
+    for (int c0 = wid; c0 < ncol; c0 += 4 * nw) {
+        double acc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * nw;
+            acc[u] = 0.0;
+            if (c < ncol) {
+                const double* a = Rc + (int64_t)c * m + r0;
+                for (int i = lane; i < nr; i += 32) acc[u] += a[i] * xs[i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = warp_sum(acc[u]);
+        if (lane == 0)
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (c0 + u * nw < ncol) atomicAdd(&t[c0 + u * nw], acc[u]);
     }
 }
 
@@ -843,6 +860,7 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         launch_reorth_pass_f64(st, Qp, ldq, m, ks, 1, 1, v, tol, s);
     };
     const bool graph = !profiling() && std::getenv("LOVE_NO_GRAPH") == nullptr && ks >= 4;
+    trace_begin(c, ks, s);
     ReplayThrottle thr(c.device);
     if (graph) st.hdone = thr.d;
     if (graph) {
@@ -879,10 +897,12 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
         for (int j = 0; j < ks; ++j) step();
     }
     host_mark("samp_enqueued");
+    if (c.trace != nullptr) trace_end(s);
     int hfl[4];
     cuda_check(cudaMemcpyAsync(hfl, st.flags, sizeof(hfl), cudaMemcpyDeviceToHost, s), "flags d2h");
     cuda_check(cudaStreamSynchronize(s), "sampling sync");
     host_mark("samp_sync");
+    trace_report(c, hfl[0] ? hfl[1] : ks);
     if (hfl[3]) throw LoveError{LOVE_ERR_ZERO_PROBE, "sampling probe M 1 is zero"};
     // every step that ran to the end set done at i = ks - 1 or at the breakdown step
     const int ke = hfl[0] ? hfl[1] : ks;
