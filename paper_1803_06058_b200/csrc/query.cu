@@ -21,6 +21,11 @@
 #define LOVE_SORTED3_TMA 1
 #endif
 
+#ifndef LOVE_SORTED3_BALANCE
+#define LOVE_SORTED3_BALANCE 1
+#endif
+constexpr bool kSorted3Balance = LOVE_SORTED3_BALANCE;   // d = 3 lane mode: remainder groups split k
+
 #ifndef LOVE_PAIRED_Q3
 #define LOVE_PAIRED_Q3 1
 #endif
@@ -786,20 +791,23 @@ __global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel
             // groups of 32 queries; with fewer groups than warps, wpg warps share a group and
             // split its k chunks (partial norms combined in shared memory)
             const int groups = (nq + 31) >> 5;
-            if (groups >= nw) {                                 // a warp per group of 32
-                for (int gi = wid; gi < groups; gi += nw) {
-                    const int pos = p0 + gi * 32 + lane;
-                    if (pos >= p1) continue;
-                    const int q = perm[pos];
-                    const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
-                    double dot = 0.0;
-                    for (int ch = 0; ch < nch; ++ch) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
-                    finish_sorted3<V>(A, c4, s2, prior_mode, dot,
-                                      mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
-                }
-            } else {                                            // wpg warps per group: split k
-                const int wpg = nw / groups;
-                const int gi = wid / wpg, sub = wid - gi * wpg;
+            // whole rounds of nw groups: a warp per group of 32; the remaining groups (fewer than
+            // nw) share the warps below, splitting k (no round with idle warps at the barrier)
+            const int full = kSorted3Balance ? groups / nw * nw : (groups >= nw ? groups : 0);
+            for (int gi = wid; gi < full; gi += nw) {
+                const int pos = p0 + gi * 32 + lane;
+                if (pos >= p1) continue;
+                const int q = perm[pos];
+                const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
+                double dot = 0.0;
+                for (int ch = 0; ch < nch; ++ch) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+                finish_sorted3<V>(A, c4, s2, prior_mode, dot,
+                                  mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
+            }
+            if (groups > full) {                                // wpg warps per group: split k
+                const int rem = groups - full;
+                const int wpg = nw / rem;
+                const int gi = full + wid / wpg, sub = wid - (wid / wpg) * wpg;
                 const int pos = p0 + gi * 32 + lane;
                 const bool live = gi < groups && pos < p1;
                 const int q = live ? perm[pos] : 0;
