@@ -26,6 +26,11 @@
 #endif
 constexpr bool kSorted3Balance = LOVE_SORTED3_BALANCE;   // d = 3 lane mode: remainder groups split k
 
+#ifndef LOVE_SORTED3_HOIST
+#define LOVE_SORTED3_HOIST 1
+#endif
+constexpr bool kSorted3Hoist = LOVE_SORTED3_HOIST;       // lane-mode weights packed once per query
+
 #ifndef LOVE_PAIRED_Q3
 #define LOVE_PAIRED_Q3 1
 #endif
@@ -732,6 +737,64 @@ constexpr bool kSorted3Tma = LOVE_SORTED3_TMA;   // row staging by cp.async.bulk
 #ifndef LOVE_SORTED3_MINB
 #define LOVE_SORTED3_MINB 4   // measured: 1 CTA per SM at 168 registers 5.5 ms, 3 CTAs 3.24 ms, 4 CTAs (64 registers, small spills) 3.15 ms per 4e6 queries
 #endif
+// The stencil weights of a lane-mode query in the form the fp32 chunk loop uses, made once per
+// query instead of once per chunk (the Stencil itself lives in local memory at 64 registers)
+struct Q3W {
+    f32x2 c[4];      // (w2[c], w2[c])
+    f32x2 b[4];      // (w1[b], w1[b])
+    double a[4];     // w0[a]
+};
+__device__ __forceinline__ Q3W make_q3w(const Stencil& A) {
+    Q3W w;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float c = (float)A.w[2][i], b = (float)A.w[1][i];
+        w.c[i] = pk2(c, c);
+        w.b[i] = pk2(b, b);
+        w.a[i] = A.w[0][i];
+    }
+    return w;
+}
+// the same FMAs in the same order as sorted3_chunk's fp32 path
+__device__ __forceinline__ double sorted3_chunk_w(const Q3W& w, const float* rows, int k_pad, int ch) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        f32x2 ra01 = 0ull, ra23 = 0ull;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            f32x2 rb01 = 0ull, rb23 = 0ull;
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const float4 v = *reinterpret_cast<const float4*>(rows + (a * 16 + b * 4 + cc) * k_pad + ch * 4);
+                rb01 = fma2(w.c[cc], pk2(v.x, v.y), rb01);
+                rb23 = fma2(w.c[cc], pk2(v.z, v.w), rb23);
+            }
+            ra01 = fma2(w.b[b], rb01, ra01);
+            ra23 = fma2(w.b[b], rb23, ra23);
+        }
+        acc[0] += w.a[a] * (double)lo2(ra01);
+        acc[1] += w.a[a] * (double)hi2(ra01);
+        acc[2] += w.a[a] * (double)lo2(ra23);
+        acc[3] += w.a[a] * (double)hi2(ra23);
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dot += acc[e] * acc[e];
+    return dot;
+}
+template <typename V>
+__device__ __forceinline__ double sorted3_dot(const Stencil& A, const V* rows, int k_pad, int ch0, int nch, int step) {
+    double dot = 0.0;
+    if constexpr (sizeof(V) == 4 && LOVE_PAIRED_Q3 && kSorted3Hoist) {
+        const Q3W w = make_q3w(A);
+        for (int ch = ch0; ch < nch; ch += step) dot += sorted3_chunk_w(w, rows, k_pad, ch);
+    } else {
+        for (int ch = ch0; ch < nch; ch += step) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+    }
+    return dot;
+}
+
 template <typename V>
 __global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
                                                               double l2, int prior_mode, const V* __restrict__ Rc,
@@ -799,8 +862,7 @@ __global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel
                 if (pos >= p1) continue;
                 const int q = perm[pos];
                 const Stencil A = make_stencil<3>(g, Xs + (int64_t)q * 3);
-                double dot = 0.0;
-                for (int ch = 0; ch < nch; ++ch) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+                const double dot = sorted3_dot<V>(A, rows, k_pad, 0, nch, 1);
                 finish_sorted3<V>(A, c4, s2, prior_mode, dot,
                                   mean_out ? sorted3_mean(A, amean, g, base) : 0.0, q, out, mean_out, counters);
             }
@@ -815,7 +877,7 @@ __global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel
                 double dot = 0.0;
                 if (live) {
                     A = make_stencil<3>(g, Xs + (int64_t)q * 3);
-                    for (int ch = sub; ch < nch; ch += wpg) dot += sorted3_chunk<V>(A, rows, k_pad, ch);
+                    dot = sorted3_dot<V>(A, rows, k_pad, sub, nch, wpg);
                 }
                 part[wid * 32 + lane] = dot;                    // [warp][lane]
                 __syncthreads();
