@@ -198,10 +198,10 @@ __global__ void __launch_bounds__(256) moments2_tpc_kernel(int64_t n_items, cons
 // Thread per (node x, group of SG outer slots): d = 3 has 16 outer slots so, split over
 // 16 / SG threads per node (x fastest: coalesced M and T along the grid), fewer registers
 // and shorter chains per thread than one thread per node.
-template <int D, typename MT, int SG>
+template <int D, typename MT, int SG, typename TT = double>
 __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_items, const int* __restrict__ cis,
                                                         const MT* __restrict__ M, StepRef ref,
-                                                        double* __restrict__ T) {
+                                                        TT* __restrict__ T) {
     pdl_wait();
     LOVE_TRACE(kTrPullLast, step_j(ref));
     constexpr int SO = D == 2 ? 4 : 16;
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) pull_last_kernel(GridDev g, int64_t n_ite
                 for (int so = 0; so < SG; ++so) sum[so] += (double)M[(int64_t)((so0 + so) * 4 + c) * n_items + it];
         }
 #pragma unroll
-        for (int so = 0; so < SG; ++so) T[(int64_t)(so0 + so) * m + x] = sum[so];
+        for (int so = 0; so < SG; ++so) T[(int64_t)(so0 + so) * m + x] = (TT)sum[so];
         return;
     }
     // d = 2: the four cells' item ranges first, then the first item of every cell (4 SG
@@ -301,7 +301,8 @@ __global__ void __launch_bounds__(256) pull_first_kernel(GridDev g, const double
 // d = 3: pull_mid and pull_first in one pass (each T entry is read by exactly one node):
 //   u[i0, i1, i2] = s_j * sum_a ( sum_b T[a*4 + b][i0 - a + 1, i1 - b + 1, i2] )
 // with the same two summation orders as the separate passes (bitwise the same u)
-__global__ void __launch_bounds__(256) pull_mid_first_kernel(GridDev g, const double* __restrict__ T, StepRef ref,
+template <typename TT>
+__global__ void __launch_bounds__(256) pull_mid_first_kernel(GridDev g, const TT* __restrict__ T, StepRef ref,
                                                              double* __restrict__ u) {
     pdl_wait();
     LOVE_TRACE(kTrPullMid, step_j(ref));
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(256) pull_mid_first_kernel(GridDev g, const do
         for (int b = 0; b < 4; ++b) {
             const int c1 = i1 - b + 1;
             if (c1 < 0 || c1 >= g.m[1]) continue;
-            va += T[(int64_t)(a * 4 + b) * m + xa + (1 - b) * g.stride[1]];
+            va += (double)T[(int64_t)(a * 4 + b) * m + xa + (1 - b) * g.stride[1]];
         }
         sum += va;
     }
@@ -628,15 +629,28 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             MT* Mf = (MT*)c.M;
             if (ni) LOVE_LAUNCH((moments_kernel<V, 3, MT>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, Mf);
             constexpr int SG = LOVE_PULL3_SG;
-            LOVE_LAUNCH((pull_last_kernel<3, MT, SG>), (int)ceil_div((int64_t)m * (16 / SG), 256), 256, 0, s, c.g,
-                        ni, c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
+            // fp32 moments: the per-slot last-axis sums T are stored in fp32 too (half the bytes of
+            // the T round trip; u is summed in fp64 by the next pull); LOVE_PULL_T64=1: fp64 T
+            static const bool t64 = std::getenv("LOVE_PULL_T64") != nullptr;
+            const bool tf32 = std::is_same<MT, float>::value && !t64;
+            if (tf32)
+                LOVE_LAUNCH((pull_last_kernel<3, MT, SG, float>), (int)ceil_div((int64_t)m * (16 / SG), 256), 256, 0, s,
+                            c.g, ni, c.cell_item_start, (const MT*)Mf, ref, (float*)c.pullT);
+            else
+                LOVE_LAUNCH((pull_last_kernel<3, MT, SG>), (int)ceil_div((int64_t)m * (16 / SG), 256), 256, 0, s, c.g,
+                            ni, c.cell_item_start, (const MT*)Mf, ref, (double*)c.pullT);
             static const bool split = std::getenv("LOVE_PULL_MF") != nullptr && std::atoi(std::getenv("LOVE_PULL_MF")) == 0;
-            if (split) {
+            if (split && !tf32) {
                 LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g,
                             (const double*)c.pullT, ref, (double*)c.pullV);
                 LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);
             } else {
-                LOVE_LAUNCH(pull_mid_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullT, ref, u);
+                if (tf32)
+                    LOVE_LAUNCH(pull_mid_first_kernel<float>, (int)ceil_div(m, 256), 256, 0, s, c.g,
+                                (const float*)c.pullT, ref, u);
+                else
+                    LOVE_LAUNCH(pull_mid_first_kernel<double>, (int)ceil_div(m, 256), 256, 0, s, c.g,
+                                (const double*)c.pullT, ref, u);
             }
         }
         return;
