@@ -896,7 +896,7 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         const double scale = (d == g.d - 1) ? c.rbf.outputscale : 1.0;
         const double* col = c.cols64 + off;
         // FP64 tensor-core axis product for the short axes (L = 64; the shapes must tile: L a
-        // multiple of 64, I = 1 or a multiple of 32), 16 columns per CTA when 32 would leave
+        // multiple of 64 up to 512 (shared memory), I = 1 or a multiple of 32), 16 columns per CTA when 32 would leave
         // fewer than ~100 CTAs.  Measured in-graph: cfg4 (64^3) 9.5 -> 7.0 us per axis, build
         // 31.0 -> 30.2 ms; at L = 256 (cfg3) the FFT wins (7.9 vs 8.7 ms).
         // LOVE_AXIS_MMA (read per call): unset = auto (L <= 64), 0 = FFT, 1 = DMMA for every
@@ -904,7 +904,7 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         const char* mma_env = std::getenv("LOVE_AXIS_MMA");
         const int mma_mode = mma_env ? std::atoi(mma_env) : -1;
         const int64_t ncols = I == 1 ? (int64_t)O : (int64_t)O * I;
-        if (mma_mode != 0 && (mma_mode > 0 || L <= 64) && L % 64 == 0 && L <= 1024 && (I == 1 || I % 32 == 0)) {
+        if (mma_mode != 0 && (mma_mode > 0 || L <= 64) && L % 64 == 0 && L <= 512 && (I == 1 || I % 32 == 0)) {
             const bool nt16 = ncols / 32 * (L / 64) < 100 && (I == 1 || I % 16 == 0);
             const int NT = nt16 ? 16 : 32;
             const size_t sm = sizeof(double) * ((size_t)L + (size_t)std::max(L, 64) * (NT + 1));
