@@ -858,7 +858,10 @@ struct StepPlan {
 // dots grid: one CTA per 256 row chunks, and column groups when that leaves the GPU idle
 inline dim3 dots_grid(int64_t ldq, int W, int k) {
     const int gx = (int)ceil_div(ldq / W, 256);
-    const int cg = std::max(1, std::min({16, (148 * 2) / std::max(gx, 1), (k + 7) / 8}));
+    // column groups fill the GPU up to `target` CTAs, 4 per SM (2 per SM: cfg5 4.78 vs 4.70 ms,
+    // cfg3 7.90 vs 7.81 ms; 8 per SM between them; LOVE_DOTS_TARGET overrides)
+    static const int target = std::getenv("LOVE_DOTS_TARGET") ? std::atoi(std::getenv("LOVE_DOTS_TARGET")) : 148 * 4;
+    const int cg = std::max(1, std::min({16, target / std::max(gx, 1), (k + 7) / 8}));
     return dim3((unsigned)gx, (unsigned)cg);
 }
 
