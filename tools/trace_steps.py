@@ -48,7 +48,11 @@ def main():
         r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "one_build.py"), "--config", str(cfg)],
                            env=env, capture_output=True, text=True, check=True)
         lines = [ln for ln in r.stderr.splitlines() if ln.startswith('{"trace"')]
-        tr = json.loads(lines[-1])["trace"]
+        # one_build.py builds twice (the second is the recorded one); a build prints the main
+        # Lanczos line, then (k_sample > 0) the sampling Lanczos line
+        per_build = 2 if getattr(get_config(cfg), "k_sample", 0) else 1
+        lines = lines[-per_build:]
+        tr = json.loads(lines[0])["trace"]
         p = get_config(cfg)
         rec = {"config": p.name, "n": p.n, "m": list(p.m), "k": p.k, "precision": p.precision,
                "source": "liblove_trace.so (LOVE_TRACE=1), tools/one_build.py --config %d, second build" % cfg,
@@ -70,6 +74,11 @@ def main():
                 "slot_us": tr["slot_us"]["dots0"] + tr["slot_us"]["update0"],
                 "achieved_gbs": (dots_b + upd_b) / t / 1e9, "peak_gbs": peak, "peak_source": peak_src,
                 "frac": (dots_b + upd_b) / t / 1e9 / peak, "note": note}
+        if per_build == 2:
+            ts = json.loads(lines[1])["trace"]
+            rec["sampling_lanczos"] = {"steps": ts["steps"], "period_us": ts["period_us"], "slot_us": ts["slot_us"],
+                                       "note": "the M-Lanczos of the sampling cache (Eqs. 12-13); its step head is "
+                                               "samp_qcur_dots (listed as 'moments')"}
         out = "%s_cfg%d.json" % (a.out, cfg)
         with open(out, "w") as f:
             json.dump(rec, f, indent=1)
