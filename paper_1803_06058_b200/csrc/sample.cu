@@ -533,17 +533,19 @@ __global__ void __launch_bounds__(256) samp_v_kernel(const double* __restrict__ 
 
 // q_j = s_j Q~'[:, j] (fp64) and t += Rc^T q_j over this CTA's kDotRows rows (dots_kernel's
 // column loop; t was zeroed by the step before)
+constexpr int kQdMaxRows = 256;
 __global__ void __launch_bounds__(256) samp_qcur_dots_kernel(LanczosState st, const double* __restrict__ Q, int64_t ld,
                                                              int m, const double* __restrict__ Rc, int ncol,
-                                                             double* __restrict__ qcur, double* __restrict__ t) {
+                                                             double* __restrict__ qcur, double* __restrict__ t,
+                                                             int rows) {
     pdl_wait();
     LOVE_TRACE(kTrMoments, *st.jdev);
     if (st.flags[0]) return;
-    __shared__ double xs[kDotRows];
+    __shared__ double xs[kQdMaxRows];
     const int j = *st.jdev;
     const double sc = st.qscale[j];
-    const int r0 = blockIdx.x * kDotRows;
-    const int nr = min(kDotRows, m - r0);
+    const int r0 = blockIdx.x * rows;
+    const int nr = min(rows, m - r0);
     for (int i = threadIdx.x; i < nr; i += blockDim.x) {
         const double q = sc * Q[(int64_t)j * ld + r0 + i];
         qcur[r0 + i] = q;
@@ -846,10 +848,15 @@ void build_sampling_cache(Cache& c, cudaStream_t s) {
     cuda_check(cudaMemsetAsync(st.alpha_cur, 0, sizeof(double), s), "alpha clear");
     launch_init_q0(st, s);
     // one step: q_j -> K_UU q_j, Rc^T q_j -> v, alpha -> two CGS passes (the last finalises)
+    // rows per CTA of q_j / Rc^T q_j (fewer CTAs: fewer serialised fp64 atomics per column of
+    // t; LOVE_QD_ROWS = 64 .. 256)
+    const int qd_rows = std::getenv("LOVE_QD_ROWS") ? std::max(32, std::min(kQdMaxRows, std::atoi(std::getenv("LOVE_QD_ROWS"))))
+                                                     : 128;
     int par = 0;
     auto step = [&]() {
         double* t = tb[par];
-        LOVE_LAUNCH(samp_qcur_dots_kernel, gd, 256, 0, s, st, (const double*)Qp, ldq, m, Rc, k, qcur, t);
+        LOVE_LAUNCH(samp_qcur_dots_kernel, (int)ceil_div(m, qd_rows), 256, 0, s, st, (const double*)Qp, ldq, m, Rc, k,
+                    qcur, t, qd_rows);
         {
             DoneScope ds(st.flags);
             launch_kuu(c, qcur, z, s);
