@@ -1064,7 +1064,9 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     // measured: the half-length real path wins at N = 2^18 but not at 2^17 (cfg2 with the
     // shortened embedding: 11.2 vs 11.4 ms per build) or 2^15: the passes are latency-bound and
     // half as many CTAs hide less of it
-    if (c.fft_N1 != 0 && N >= (1 << 18) && std::getenv("LOVE_NO_RFFT") == nullptr) {
+    // real-input half-length passes from N >= 2^18 (LOVE_RFFT_MIN = log2 of the threshold)
+    const int rfft_min = std::getenv("LOVE_RFFT_MIN") ? std::atoi(std::getenv("LOVE_RFFT_MIN")) : 18;
+    if (c.fft_N1 != 0 && N >= (1 << rfft_min) && std::getenv("LOVE_NO_RFFT") == nullptr) {
         // real-input path: N' = N/2 = R1 * R2 (R1 = 2^floor(lg N'/2)), tables and lambda[0..N']
         const int Np = N / 2, lgp = ilog2(Np);
         c.rfft_N1 = 1 << (lgp / 2);
