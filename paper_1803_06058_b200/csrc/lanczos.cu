@@ -12,6 +12,7 @@
 // Rc = K_UU W Q_k L^{-T} and Rc Rc^T = R^T R' of P:282-285.  Mean cache (Eq. 6 via Eq. 3,
 // probe y): a = ||y|| Rc L^{-1} e_1, also streamed.
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #include <algorithm>
 #include <cstdlib>
@@ -1286,6 +1287,62 @@ bool ReplayThrottle::admit(int i) {
 void ReplayThrottle::launched(int i, cudaStream_t s) {
     cuda_check(cudaEventRecord(ev[i % kReplayWindow], s), "replay event");
 }
+
+// L2 residency of the Lanczos basis' first columns: both reorthogonalisation passes of every
+// step read columns 0, 1, ..., so when Q~ is several times the L2 the first 48 MB of it are
+// marked persisting for the build (stream access-policy window, inherited by the captured
+// kernel nodes) and released afterwards.  Measured (same-box A/B, MB set aside): cfg2 (Q~
+// 404 MB) 10.27 -> 10.17 ms at 48 / 64; cfg4 (808 MB) 29.91 -> 29.35 ms at 48, 31.05 at 72;
+// cfg3 (202 MB) and cfg5 (80 MB, already L2-sized) slower.  LOVE_L2_PERSIST = MB (0: off).
+struct L2Persist {
+    cudaStream_t s = nullptr;
+    bool on = false;
+    size_t prev_limit = 0;                    // the device's set-aside before the build (restored)
+    L2Persist(const Cache& c, cudaStream_t st) : s(st) {
+        if (c.comm != nullptr || c.Q == nullptr) return;
+        const size_t qbytes = c.vsize * (size_t)c.ldq * (size_t)(c.k_req + 1);
+        const char* e = std::getenv("LOVE_L2_PERSIST");
+        const double mb = e ? std::atof(e) : (qbytes >= (size_t(384) << 20) ? 48.0 : 0.0);
+        if (!(mb > 0.0)) return;
+        int dev = 0, maxp = 0, maxw = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        if (maxp <= 0 || maxw <= 0) return;
+        const size_t persist = std::min<size_t>((size_t)(mb * 1048576.0), (size_t)maxp);
+        const size_t window = std::min<size_t>({persist, (size_t)maxw, qbytes});
+        if (cudaDeviceGetLimit(&prev_limit, cudaLimitPersistingL2CacheSize) != cudaSuccess) return;
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist) != cudaSuccess) return;
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.base_ptr = c.Q;
+        v.accessPolicyWindow.num_bytes = window;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+        if (std::getenv("LOVE_L2_DEBUG"))
+            std::fprintf(stderr, "[love l2] max persist %d MB, max window %d MB, window %.1f MB, on %d\n",
+                         maxp >> 20, maxw >> 20, window / 1048576.0, (int)on);
+    }
+    ~L2Persist() {
+        if (!on) return;
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_limit);
+    }
+};
+
+void* l2_persist_begin(const Cache& c, cudaStream_t s) {
+    L2Persist* p = new L2Persist(c, s);
+    if (!p->on) {
+        delete p;
+        return nullptr;
+    }
+    return p;
+}
+void l2_persist_end(void* h) { delete static_cast<L2Persist*>(h); }
 
 void run_lanczos(Cache& c, cudaStream_t s) {
     if (c.precision == LOVE_FP64) lanczos_impl<double>(c, s);

@@ -380,6 +380,10 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
 
     // ---- k Lanczos steps + streamed Cholesky / Rc / mean cache
     if (c->fused) setup_fused(*c, s);
+    struct L2Scope {
+        void* h;
+        ~L2Scope() { l2_persist_end(h); }
+    } l2{c->fused ? nullptr : l2_persist_begin(*c, s)};
     if (c->fused) run_lanczos_fused(*c, s);
     else run_lanczos(*c, s);
     host_mark("lanczos_enqueued");

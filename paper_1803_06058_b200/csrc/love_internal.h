@@ -281,6 +281,10 @@ void setup_kuu(Cache& c, cudaStream_t s);
 void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
+// L2 residency of Q~'s first columns for one build (nullptr: not used); end after the build's
+// final synchronisation (restores the device's persisting-L2 set-aside)
+void* l2_persist_begin(const Cache& c, cudaStream_t s);
+void l2_persist_end(void* h);
 // Host side of the early stop of step-graph replays (ReplayThrottle in lanczos.cu): a mapped
 // host flag the device sets at breakdown, and at most kReplayWindow replays in flight beyond the
 // last one the host has seen complete.
