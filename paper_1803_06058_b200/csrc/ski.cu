@@ -58,6 +58,17 @@ constexpr bool kPairedGather3 = false;
 #else
 #define LOVE_GATHER_BOUNDS(D) __launch_bounds__(256)
 #endif
+// LOVE_TAIL_BREAK: the compute loop of a point batch stops at the item's end instead of running
+// the zero-weighted padding of the last batch (cfg4 in-graph: moments 29.8 -> 25.4 us per step)
+#ifndef LOVE_TAIL_BREAK
+#define LOVE_TAIL_BREAK 1
+#endif
+#if LOVE_TAIL_BREAK
+#define LOVE_BATCH_END(cond) if (cond) break
+#else
+#define LOVE_BATCH_END(cond) (void)0
+#endif
+
 template <typename V, int D, typename MT>
 __global__ void LOVE_MOM_BOUNDS(D) moments_kernel(int64_t n_items, const int* __restrict__ item_start,
                                                       const V* __restrict__ f0, const V* __restrict__ f1,
@@ -90,6 +101,7 @@ __global__ void LOVE_MOM_BOUNDS(D) moments_kernel(int64_t n_items, const int* __
             }
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) {
+                LOVE_BATCH_END(pb + u >= p1);
                 float w0[4], w1[4], w2[4];
                 keys4<float>(fa[u], w0);
                 keys4<float>(fb[u], w1);
@@ -174,6 +186,7 @@ __global__ void __launch_bounds__(256) moments2_tpc_kernel(int64_t n_items, cons
         }
 #pragma unroll
         for (int u = 0; u < B; ++u) {
+            LOVE_BATCH_END(pb + 2 * u >= p1);
             double w0[4], w1[4];
             keys4<double>(fa[u], w0);
             keys4<double>(fb[u], w1);
@@ -413,6 +426,7 @@ __global__ void LOVE_GATHER_BOUNDS(D) gather_kernel(GridDev g, int64_t n_items,
             } else {
 #pragma unroll
             for (int u = 0; u < kBatch; ++u) {
+                if (D == 3) LOVE_BATCH_END(pb + u >= p1);
                 A w0[4], w1[4], w2[4];
                 keys4<A>(fa[u], w0);
                 if (D > 1) keys4<A>(fb[u], w1);
