@@ -40,6 +40,12 @@ constexpr bool kPaired3 = LOVE_PAIRED3;   // 3-D fp32 moments on FFMA2 pairs
 // the paired 3-D gather (two points per FFMA2) is bitwise identical but measured slower
 // (cfg4 gather 3.98 -> 4.19 ms per build): off
 constexpr bool kPairedGather3 = false;
+// the 3-D fp32 gather with the stencil's b-pairs packed (z[a][b][c], z[a][b+1][c]): the 64 c-level
+// FMAs of a point as 32 FFMA2, the same FMA per slot in the same order as stencil_dot<float, 3>
+#ifndef LOVE_BPAIR_GATHER3
+#define LOVE_BPAIR_GATHER3 1
+#endif
+constexpr bool kBPairGather3 = LOVE_BPAIR_GATHER3;
 
 // minimum resident CTAs per SM for the 3-D item kernels (0: the compiler's choice)
 #ifndef LOVE_MOM3_MINB
@@ -380,7 +386,65 @@ __global__ void LOVE_GATHER_BOUNDS(D) gather_kernel(GridDev g, int64_t n_items,
     const double sc = ref.scale[j];
     const A vsc = (A)sc, vsig = (A)(sigma2 * sc);
     double alpha = 0.0;
-    if (it < n_items) {
+    if constexpr (D == 3 && std::is_same<A, float>::value && kBPairGather3) {
+        if (it < n_items) {
+            f32x2 zp[32];                          // [a][b pair][c]
+            {
+                float zl[64];
+                load_stencil<float, 3>(g, z, stencil_base<3>(g, item_cell[it]), zl);
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int bp = 0; bp < 2; ++bp)
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc)
+                            zp[(a * 2 + bp) * 4 + cc] = pk2(zl[(a * 4 + 2 * bp) * 4 + cc], zl[(a * 4 + 2 * bp + 1) * 4 + cc]);
+            }
+            const int p0 = item_start[it], p1 = item_start[it + 1];
+            for (int pb = p0; pb < p1; pb += kBatch) {
+                float qv[kBatch], fa[kBatch], fb[kBatch], fc[kBatch];
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const int p = pb + u;
+                    const bool in = p < p1;
+                    qv[u] = in ? (float)q[p] : 0.f;
+                    fa[u] = in ? (float)f0[p] : 0.f;
+                    fb[u] = in ? (float)f1[p] : 0.f;
+                    fc[u] = in ? (float)f2[p] : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    LOVE_BATCH_END(pb + u >= p1);
+                    float w0[4], w1[4], w2[4];
+                    keys4<float>(fa[u], w0);
+                    keys4<float>(fb[u], w1);
+                    keys4<float>(fc[u], w2);
+                    float acc = 0.f;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        f32x2 t01 = 0ull, t23 = 0ull;      // (tb[a][0], tb[a][1]), (tb[a][2], tb[a][3])
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc) {
+                            const f32x2 ww = pk2(w2[cc], w2[cc]);
+                            t01 = fma2(ww, zp[(a * 2) * 4 + cc], t01);
+                            t23 = fma2(ww, zp[(a * 2 + 1) * 4 + cc], t23);
+                        }
+                        float ta = 0.f;
+                        ta = fmaf(w1[0], lo2(t01), ta);
+                        ta = fmaf(w1[1], hi2(t01), ta);
+                        ta = fmaf(w1[2], lo2(t23), ta);
+                        ta = fmaf(w1[3], hi2(t23), ta);
+                        acc = fmaf(w0[a], ta, acc);
+                    }
+                    const V rv = (V)(acc + vsig * qv[u]);
+                    if (pb + u < p1) {
+                        r[pb + u] = rv;
+                        alpha += (double)(vsc * qv[u]) * (double)rv;
+                    }
+                }
+            }
+        }
+    } else if (it < n_items) {
         A zl[S];
         load_stencil<A, D>(g, z, stencil_base<D>(g, item_cell[it]), zl);
         const int p0 = item_start[it], p1 = item_start[it + 1];
