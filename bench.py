@@ -567,6 +567,16 @@ def main():
                 "achieved": q_ach, "peak": peak, "unit": "GB/s", "frac": q_ach / peak,
                 "bytes_per_query": bq, "kernel_ms": qk_ms,
                 "timing": "CUDA events around the query launches (profiled steps)"}
+    if p.kind != "additive" and p.d == 3 and occ:
+        # the cell-sorted kernel reads its rows from shared memory: its bound is the FP32 FMA
+        # pipe -- per query and k value the separable contraction sum_a w0 sum_b w1 sum_c w2 R
+        # takes 64 + 16 + 4 FMAs (2 FLOP each)
+        fpk, fsrc = fp32_peak()
+        qfl = 2.0 * 84 * k_eff * t_loc
+        q_tf = qfl / (qk_ms / 1e3) / 1e12
+        query_rf["alu"] = {"bound": "alu", "flop": qfl, "achieved": q_tf, "peak": fpk, "unit": "TFLOP/s",
+                           "frac": q_tf / fpk, "peak_source": fsrc,
+                           "model": "t * k_eff * (64 + 16 + 4) FMA of the per-query separable contraction"}
     if p.kind != "additive" and p.d <= 2:
         # the cell-block table (m blocks) is L2-resident: the DRAM floor is each query's x* and
         # result plus the table once, far below the gathered bytes
