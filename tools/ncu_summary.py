@@ -19,7 +19,12 @@ KEYS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("smsp__inst_executed.sum", "warp instructions"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active lanes per instruction"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput %"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
 ]
+STALL = "smsp__average_warps_issue_stalled_"
 
 
 def main():
@@ -37,6 +42,16 @@ def main():
                 continue
             u = units[hdr.index(k)] if k in hdr else ""
             print(f"  {label:28s} {v} {u}")
+        st = []
+        for h in hdr:
+            if h.startswith(STALL) and h.endswith("_per_issue_active.ratio") and d.get(h):
+                try:
+                    st.append((float(d[h]), h[len(STALL):-len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        if st:
+            st.sort(reverse=True)
+            print("  stalls per issue (top 6)      " + ", ".join(f"{n} {v:.2f}" for v, n in st[:6]))
 
 
 if __name__ == "__main__":
