@@ -1,5 +1,8 @@
-// profile.cpp -- phase timing with CUDA events on the launching stream (love_profile_*).
+// profile.cpp -- phase timing with CUDA events on the launching stream (love_profile_*), and
+// NVTX ranges over the same phases for external profilers (LOVE_NVTX=1: ncu --nvtx
+// --nvtx-include "love.reorth_update/" ..., header-only NVTX v3, no library to link).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -191,7 +194,19 @@ void host_marks_flush() {
     h.m.clear();
 }
 
+namespace {
+const char* const kNvtxNames[LOVE_PROF_N] = {"love.setup", "love.scatter", "love.kuu", "love.gather",
+                                             "love.reorth_dots", "love.reorth_update", "love.scalars_rc",
+                                             "love.finish", "love.query", "love.sample_cache", "love.sample",
+                                             "love.comm", "love.fused_pass", "love.sample_gemm"};
+bool nvtx_on() {
+    static const bool v = std::getenv("LOVE_NVTX") != nullptr && std::atoi(std::getenv("LOVE_NVTX")) != 0;
+    return v;
+}
+}  // namespace
+
 void prof_begin(int cat, cudaStream_t s) {
+    if (nvtx_on() && cat >= 0 && cat < LOVE_PROF_N) nvtxRangePushA(kNvtxNames[cat]);
     Profiler& p = prof();
     if (!p.on) return;
     std::lock_guard<std::mutex> g(p.mu);
@@ -201,6 +216,7 @@ void prof_begin(int cat, cudaStream_t s) {
 }
 
 void prof_end(int cat, cudaStream_t s) {
+    if (nvtx_on() && cat >= 0 && cat < LOVE_PROF_N) nvtxRangePop();
     Profiler& p = prof();
     if (!p.on || t_open[cat] == nullptr) return;
     std::lock_guard<std::mutex> g(p.mu);
