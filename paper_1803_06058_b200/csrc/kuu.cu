@@ -896,17 +896,23 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         const double scale = (d == g.d - 1) ? c.rbf.outputscale : 1.0;
         const double* col = c.cols64 + off;
         // FP64 tensor-core axis product for the short axes (L = 64; the shapes must tile: L a
-        // multiple of 64 up to 512 (shared memory), I = 1 or a multiple of 32), 16 columns per CTA when 32 would leave
-        // fewer than ~100 CTAs.  Measured in-graph: cfg4 (64^3) 9.5 -> 7.0 us per axis, build
-        // 31.0 -> 30.2 ms; at L = 256 (cfg3) the FFT wins (7.9 vs 8.7 ms).
-        // LOVE_AXIS_MMA (read per call): unset = auto (L <= 64), 0 = FFT, 1 = DMMA for every
+        // multiple of 64 up to 512 (shared memory), I = 1 or a multiple of 32).  Measured in-graph: cfg4 (64^3) 9.5 -> 7.0 us per axis, build
+        // 31.0 -> 30.2 ms; at L = 256 (cfg3) the FFT won with 32-column tiles (7.9 vs 8.7 ms) and
+        // loses with 8-column ones (axis slots 8.0 + 6.9 -> 6.3 + 6.7 us, cfg3 7.69 -> 7.47 ms).
+        // LOVE_AXIS_MMA (read per call): unset = auto (L <= 256), 0 = FFT, 1 = DMMA for every
         // L that tiles, 2 = SIMT fp64 (measured: as DMMA at cfg4, slower at cfg3)
         const char* mma_env = std::getenv("LOVE_AXIS_MMA");
         const int mma_mode = mma_env ? std::atoi(mma_env) : -1;
         const int64_t ncols = I == 1 ? (int64_t)O : (int64_t)O * I;
-        if (mma_mode != 0 && (mma_mode > 0 || L <= 64) && L % 64 == 0 && L <= 512 && (I == 1 || I % 32 == 0)) {
-            const bool nt16 = ncols / 32 * (L / 64) < 100 && (I == 1 || I % 16 == 0);
-            const int NT = nt16 ? 16 : 32;
+        if (mma_mode != 0 && (mma_mode > 0 || L <= 256) && L % 64 == 0 && L <= 512 && (I == 1 || I % 32 == 0)) {
+            static const int nt_env = std::getenv("LOVE_AXIS_NT") ? std::atoi(std::getenv("LOVE_AXIS_NT")) : 0;
+            // columns per CTA: halved from 32 while the grid has fewer than 4 CTAs per SM (measured
+            // in-graph, cfg4: 128 CTAs of 32 columns 7.0 us per axis, 256 of 16 6.2 us, 512 of 8
+            // 5.0 us; cfg4 28.62 -> 28.04 ms); LOVE_AXIS_NT = 8 / 16 / 32 overrides
+            int NT = 32;
+            while (NT > 8 && ncols / NT * (L / 64) < 4 * 148) NT /= 2;
+            if (nt_env == 8 || nt_env == 16 || nt_env == 32) NT = nt_env;
+            if (I != 1 && I % NT != 0) NT = 32;
             const size_t sm = sizeof(double) * ((size_t)L + (size_t)std::max(L, 64) * (NT + 1));
             dim3 grid((unsigned)ceil_div(ncols, NT), (unsigned)(L / 64));
 #define LOVE_AXMMA(LF, NT_)                                                                                  \
@@ -920,10 +926,12 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
         }                                                                                                    \
     } while (0)
             if (I == 1) {
-                if (nt16) LOVE_AXMMA(true, 16);
+                if (NT == 8) LOVE_AXMMA(true, 8);
+                else if (NT == 16) LOVE_AXMMA(true, 16);
                 else LOVE_AXMMA(true, 32);
             } else {
-                if (nt16) LOVE_AXMMA(false, 16);
+                if (NT == 8) LOVE_AXMMA(false, 8);
+                else if (NT == 16) LOVE_AXMMA(false, 16);
                 else LOVE_AXMMA(false, 32);
             }
 #undef LOVE_AXMMA
