@@ -659,6 +659,20 @@ __global__ void convert_kernel(const A* __restrict__ in, B* __restrict__ out, in
         out[i] = (B)in[i];
 }
 
+// threads per CTA of the 3-D item kernels (LOVE_ITEM_BLOCK3 = 64 .. 256, a multiple of 32).
+// At 128 registers a CTA of 128 threads is retired (and its slot refilled) when its 4 warps are
+// done, not 8: the items' uneven lengths idle fewer warp slots.  Measured (cfg4, in-graph):
+// 256 threads moments 25.7 / gather 33.3 us, 192: 26.1 / 36.8, 128: 23.1 / 31.4, 64: 22.7 / 31.5;
+// cfg4 28.02 -> 27.60 ms at 128.
+int item_block3() {
+    static const int v = [] {
+        const char* e = std::getenv("LOVE_ITEM_BLOCK3");
+        const int b = e ? std::atoi(e) : 128;
+        return b >= 64 && b <= 256 && b % 32 == 0 ? b : 128;
+    }();
+    return v;
+}
+
 }  // namespace
 
 void launch_nodepass(const Cache& c, StepRef ref, double* u, cudaStream_t s) {
@@ -705,7 +719,11 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
             // the 3-D moments are stored in their accumulation type (fp32 in LOVE_FP32 mode)
             using MT = typename AccT<V, 3>::type;
             MT* Mf = (MT*)c.M;
-            if (ni) LOVE_LAUNCH((moments_kernel<V, 3, MT>), gi, 256, 0, s, ni, c.item_start, f0, f1, f2, q, ref, Mf);
+            if (ni) {
+                const int tb = item_block3();
+                LOVE_LAUNCH((moments_kernel<V, 3, MT>), (int)ceil_div(ni, tb), tb, 0, s, ni, c.item_start, f0, f1, f2, q,
+                            ref, Mf);
+            }
             constexpr int SG = LOVE_PULL3_SG;
             // fp32 moments: the per-slot last-axis sums T are stored in fp32 too (half the bytes of
             // the T round trip; u is summed in fp64 by the next pull); LOVE_PULL_T64=1: fp64 T
@@ -781,7 +799,14 @@ void launch_gather(const Cache& c, const double* z, const V* q, StepRef ref, V* 
     switch (c.g.d) {
         case 1: LOVE_GATHER(1); break;
         case 2: LOVE_GATHER(2); break;
-        default: LOVE_GATHER(3); break;
+        default: {
+            const int tb = item_block3();
+            const int g3 = (int)ceil_div(ni, tb);
+            const int ex3 = rsp != nullptr ? (int)std::min<int64_t>(ceil_div(rs.m, tb), 148 * 2 * (256 / tb)) : 0;
+            LOVE_LAUNCH((gather_kernel<V, 3>), g3 + ex3, tb, 0, s, c.g, ni, c.item_cell, c.item_start, f0, f1, f2, z, q,
+                        ref, c.sigma2, r, alpha_base, rs, g3);
+            break;
+        }
     }
 #undef LOVE_GATHER
 }
