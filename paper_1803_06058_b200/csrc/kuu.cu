@@ -490,10 +490,15 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+// T3 != nullptr (first axis of a 3-D grid, LOVE_FUSE_PULL3): the X tile is the scatter's node
+// sums u = s_j sum_a sum_b T3[a*4 + b][x + (1 - a) s0 + (1 - b) s1] formed on the fly from the
+// fp32 last-axis sums (pull_mid_first_kernel's order: bitwise the same u), so u never goes
+// through global memory and the pull_mid_first launch goes away
 template <bool LFAST, int NT, bool MMA>
 __global__ void __launch_bounds__(256) axis_mma_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                        const double* __restrict__ col, int L, int I, int64_t O,
-                                                       double scale, const int* __restrict__ done) {
+                                                       double scale, const int* __restrict__ done,
+                                                       const float* __restrict__ T3, int m1, int m2, StepRef ref3) {
     pdl_wait();
     LOVE_TRACE(LFAST ? kTrFft2 : (O == 1 ? kTrFft0 : kTrFft1), done != nullptr ? done[4] : 0);
     if (done != nullptr && *done) return;       // the Lanczos has stopped (breakdown or k)
@@ -514,6 +519,30 @@ __global__ void __launch_bounds__(256) axis_mma_kernel(const double* __restrict_
         for (int e = threadIdx.x; e < NT * L; e += blockDim.x) {
             const int n = e / L, l = e - n * L;
             Xs[l * LD + n] = n0 + n < O ? in[(n0 + n) * L + l] : 0.0;
+        }
+    } else if (T3 != nullptr) {
+        const int64_t m = (int64_t)L * I;
+        const double sj = ref3.scale[step_j(ref3)];
+        for (int e = threadIdx.x; e < NT * L; e += blockDim.x) {
+            const int l = e / NT, n = e - l * NT;
+            const int64_t x = (int64_t)l * I + i0 + n;
+            const int i1 = ((i0 + n) / m2) % m1;
+            double sum = 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int c0 = l - a + 1;
+                if (c0 < 0 || c0 >= L) continue;
+                const int64_t xa = x + (int64_t)(1 - a) * I;
+                double va = 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const int c1 = i1 - b + 1;
+                    if (c1 < 0 || c1 >= m1) continue;
+                    va += (double)T3[(int64_t)(a * 4 + b) * m + xa + (1 - b) * m2];
+                }
+                sum += va;
+            }
+            Xs[l * LD + n] = sum * sj;
         }
     } else {
         for (int e = threadIdx.x; e < NT * L; e += blockDim.x) {
@@ -883,7 +912,7 @@ void fft_run(const Cache& c, const double* u, const double* Mc, int m, double* z
     }
 }
 
-void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
+void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s, const StepRef* pull3) {
     const GridDev& g = c.g;
     const double* in = u;
     int off = 0;
@@ -913,16 +942,24 @@ void kuu_axes(const Cache& c, const double* u, double* z, cudaStream_t s) {
             while (NT > 8 && ncols / NT * (L / 64) < 4 * 148) NT /= 2;
             if (nt_env == 8 || nt_env == 16 || nt_env == 32) NT = nt_env;
             if (I != 1 && I % NT != 0) NT = 32;
+            // the first axis of a 3-D grid can read the scatter's last-axis sums directly
+            const bool from_t = pull3 != nullptr && d == 0 && g.d == 3 && I > 1;
+            if (pull3 != nullptr && d == 0 && !from_t) throw LoveError{LOVE_ERR_CUDA, "fused pull: axis 0 not on DMMA"};
+            const float* T3 = from_t ? (const float*)c.pullT : nullptr;
+            const int m1v = g.m[1], m2v = g.m[2];
+            const StepRef ref3 = from_t ? *pull3 : StepRef{nullptr, 0, nullptr, nullptr};
             const size_t sm = sizeof(double) * ((size_t)L + (size_t)std::max(L, 64) * (NT + 1));
             dim3 grid((unsigned)ceil_div(ncols, NT), (unsigned)(L / 64));
 #define LOVE_AXMMA(LF, NT_)                                                                                  \
     do {                                                                                                     \
         if (mma_mode == 2) {                                                                                 \
             ensure_smem((const void*)axis_mma_kernel<LF, NT_, false>, sm);                                   \
-            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, false>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done); \
+            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, false>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done, \
+                        T3, m1v, m2v, ref3);                                                                 \
         } else {                                                                                             \
             ensure_smem((const void*)axis_mma_kernel<LF, NT_, true>, sm);                                    \
-            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, true>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done); \
+            LOVE_LAUNCH((axis_mma_kernel<LF, NT_, true>), grid, 256, sm, s, in, out, col, L, I, (int64_t)O, scale, t_done, \
+                        T3, m1v, m2v, ref3);                                                                 \
         }                                                                                                    \
     } while (0)
             if (I == 1) {
@@ -1098,12 +1135,23 @@ void setup_kuu(Cache& c, cudaStream_t s) {
     cuda_check(cudaFreeAsync(X, s), "lam free");
 }
 
-void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc) {
+bool fuse_pull3(const Cache& c) {
+    static const bool on = std::getenv("LOVE_FUSE_PULL3") == nullptr || std::atoi(std::getenv("LOVE_FUSE_PULL3")) != 0;
+    if (!on || c.additive || c.g.d != 3 || c.comm != nullptr || c.precision != LOVE_FP32 || c.fused) return false;
+    if (std::getenv("LOVE_PULL_T64") != nullptr || std::getenv("LOVE_PULL_MF") != nullptr) return false;
+    // the first axis must take the DMMA path (kuu_axes' rule)
+    const char* mma_env = std::getenv("LOVE_AXIS_MMA");
+    const int mma_mode = mma_env ? std::atoi(mma_env) : -1;
+    const int L = c.g.m[0], I = c.g.m[1] * c.g.m[2];
+    return mma_mode != 0 && (mma_mode > 0 || L <= 256) && L % 64 == 0 && L <= 512 && I % 32 == 0;
+}
+
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc, const StepRef* pull3) {
     if (c.additive) {
         add_kuu(c, u, z, s);
         return;
     }
-    if (c.g.d > 1) kuu_axes(c, u, z, s);
+    if (c.g.d > 1) kuu_axes(c, u, z, s, pull3);
     else fft_run(c, u, Mc, c.g.m[0], z, (C*)c.fft_buf, nullptr, 0, s);
 }
 

@@ -848,6 +848,7 @@ struct StepPlan {
     bool fold;                    // single GPU: scalars in the update's last CTA, cache column in the gather
     RcStream rs;
     bool mfuse;                   // d = 1, one GPU: the FFT's first pass reads the scatter moments
+    bool pfuse3 = false;          // d = 3 fp32, one GPU: the first axis product reads the last-axis sums
     bool partial;                 // partial reorthogonalisation (single GPU)
     bool one_sync;                // several GPUs, fp32, one CGS pass: the one-sync step (reorth_dots3)
     int64_t ldq;
@@ -882,7 +883,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     }
     {
         ProfScope ps(LOVE_PROF_SCATTER, s);
-        launch_scatter<V>(c, Q, ref, u, s, pl.mfuse);
+        launch_scatter<V>(c, Q, ref, u, s, pl.mfuse || pl.pfuse3);
     }
     if (c.comm != nullptr) {
         ProfScope ps(LOVE_PROF_COMM, s);
@@ -892,7 +893,7 @@ void enqueue_step(const StepPlan<V>& pl, int j_host, cudaStream_t s) {
     {
         ProfScope ps(LOVE_PROF_KUU, s);
         DoneScope ds(st.flags);
-        launch_kuu(c, u, zj, s, pl.mfuse ? (const double*)c.Mc : nullptr);
+        launch_kuu(c, u, zj, s, pl.mfuse ? (const double*)c.Mc : nullptr, pl.pfuse3 ? &ref : nullptr);
     }
     {
         ProfScope ps(LOVE_PROF_GATHER, s);
@@ -981,6 +982,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.P = c.reorth_passes;
     pl.mean_y = c.probe == LOVE_PROBE_Y;
     pl.mfuse = c.Mc != nullptr && c.comm == nullptr;
+    pl.pfuse3 = sizeof(V) == 4 && fuse_pull3(c);
     pl.fold = c.comm == nullptr && std::getenv("LOVE_NO_FOLD") == nullptr;
     pl.partial = c.partial;
     // the one-sync step needs 3 (k+1) fp64 partial dots per warp in shared memory

@@ -278,7 +278,11 @@ template <typename V> void launch_permute(const Cache& c, const V* in, V* out, b
 // kuu.cu
 void setup_kuu(Cache& c, cudaStream_t s);
 // z = K_UU u; for d = 1, u may instead be given as the per-cell moments Mc of launch_scatter
-void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr);
+// pull3 (d = 3, fuse_pull3): u is not materialised -- the first axis product forms it from the
+// scatter's fp32 last-axis sums (c.pullT) and the step's scale
+void launch_kuu(const Cache& c, const double* u, double* z, cudaStream_t s, const double* Mc = nullptr,
+                const StepRef* pull3 = nullptr);
+bool fuse_pull3(const Cache& c);
 // lanczos.cu
 void run_lanczos(Cache& c, cudaStream_t s);
 // L2 residency of Q~'s first columns for one build (nullptr: not used); end after the build's

@@ -740,6 +740,8 @@ void launch_scatter(const Cache& c, const V* q, StepRef ref, double* u, cudaStre
                 LOVE_LAUNCH(pull_mid_kernel, (int)ceil_div(4 * (int64_t)m, 256), 256, 0, s, c.g,
                             (const double*)c.pullT, ref, (double*)c.pullV);
                 LOVE_LAUNCH(pull_first_kernel, (int)ceil_div(m, 256), 256, 0, s, c.g, (const double*)c.pullV, ref, u);
+            } else if (moments_only && tf32) {
+                // fuse_pull3: the first K_UU axis product forms u from T itself (launch_kuu(..., pull3))
             } else {
                 if (tf32)
                     LOVE_LAUNCH(pull_mid_first_kernel<float>, (int)ceil_div(m, 256), 256, 0, s, c.g,
