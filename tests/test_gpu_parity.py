@@ -238,6 +238,7 @@ def test_scaled_cfg2_probe_avgcol(mode):
 @pytest.mark.parametrize("ci,n,m,k,t", [
     (2, 60_001, (6000,), 40, 3001),          # 1-D four-step FFT, ragged n and t
     (3, 30_007, (48, 48), 40, 2003),         # 2-D Kronecker
+    (3, 30_007, (64, 64), 40, 2003),         # 2-D, both axes on DMMA
     (4, 60_013, (24, 24, 24), 40, 2005),     # 3-D Kronecker
     (4, 60_013, (64, 32, 32), 40, 2005),     # 3-D, first axis on DMMA reading the scatter's sums (fuse_pull3)
     (5, 20_011, (2000,), 30, 1999),          # config-5 data, shorter grid
