@@ -795,8 +795,8 @@ __device__ __forceinline__ double sorted3_dot(const Stencil& A, const V* rows, i
     return dot;
 }
 
-template <typename V>
-__global__ void __launch_bounds__(256, LOVE_SORTED3_MINB) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
+template <typename V, int TPB = 256>
+__global__ void __launch_bounds__(TPB, TPB == 256 ? LOVE_SORTED3_MINB : 4) predict_sorted3_kernel(GridDev g, C4 c4, double s2, double l0, double l1,
                                                               double l2, int prior_mode, const V* __restrict__ Rc,
                                                               int k_pad, const double* __restrict__ amean,
                                                               const double* __restrict__ Xs,
@@ -1035,11 +1035,23 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
         for (int d = 0; d < 3; ++d)
             for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
         const int cpc = 8;
-        ensure_smem((const void*)predict_sorted3_kernel<V>, sm3);
-        LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm3, s, c.g, c4, c.rbf.outputscale,
-                    c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                    c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
-                    kLanePerQuery);
+        // 4 warps per CTA (LOVE_Q3_TPB=256: 8): the per-cell barrier idles fewer warps in the many
+        // cells with few queries, and 128 registers drop the 64-register spills; measured cfg4
+        // 27.50 -> 27.19 ms (same box, three interleaved repeats)
+        static const int tpb = std::getenv("LOVE_Q3_TPB") ? std::atoi(std::getenv("LOVE_Q3_TPB")) : 128;
+        if (tpb == 128) {
+            ensure_smem((const void*)predict_sorted3_kernel<V, 128>, sm3);
+            LOVE_LAUNCH((predict_sorted3_kernel<V, 128>), (int)ceil_div(m, cpc), 128, sm3, s, c.g, c4, c.rbf.outputscale,
+                        c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
+                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
+                        kLanePerQuery);
+        } else {
+            ensure_smem((const void*)predict_sorted3_kernel<V>, sm3);
+            LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm3, s, c.g, c4, c.rbf.outputscale,
+                        c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
+                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
+                        kLanePerQuery);
+        }
         LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, tm.qstart, m, tm.perm, out, mean_out, c.counters);
         return;
     }
