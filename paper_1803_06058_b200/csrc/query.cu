@@ -1034,7 +1034,10 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
         C4 c4{};
         for (int d = 0; d < 3; ++d)
             for (int e = 0; e < 4; ++e) c4.c[d][e] = c.h_cols64[d][e];
-        const int cpc = 8;
+        // cells per CTA and the lane-mode threshold (measurement switches LOVE_Q3_CPC / LOVE_Q3_LMIN)
+        static const int cpc = std::getenv("LOVE_Q3_CPC") ? std::max(1, std::atoi(std::getenv("LOVE_Q3_CPC"))) : 8;
+        static const int lmin = std::getenv("LOVE_Q3_LMIN") ? std::max(1, std::atoi(std::getenv("LOVE_Q3_LMIN")))
+                                                            : kLanePerQuery;
         // 4 warps per CTA (LOVE_Q3_TPB=256: 8): the per-cell barrier idles fewer warps in the many
         // cells with few queries, and 128 registers drop the 64-register spills; measured cfg4
         // 27.50 -> 27.19 ms (same box, three interleaved repeats)
@@ -1043,14 +1046,12 @@ void launch_predict(const Cache& c, const double* Xa, const double* Xb, int64_t 
             ensure_smem((const void*)predict_sorted3_kernel<V, 128>, sm3);
             LOVE_LAUNCH((predict_sorted3_kernel<V, 128>), (int)ceil_div(m, cpc), 128, sm3, s, c.g, c4, c.rbf.outputscale,
                         c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
-                        kLanePerQuery);
+                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters, lmin);
         } else {
             ensure_smem((const void*)predict_sorted3_kernel<V>, sm3);
             LOVE_LAUNCH(predict_sorted3_kernel<V>, (int)ceil_div(m, cpc), 256, sm3, s, c.g, c4, c.rbf.outputscale,
                         c.rbf.lengthscale[0], c.rbf.lengthscale[1], c.rbf.lengthscale[2], c.prior, (const V*)c.Rc,
-                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters,
-                        kLanePerQuery);
+                        c.k_pad, (const double*)c.a, Xa, tm.qstart, tm.perm, cpc, out, mean_out, c.counters, lmin);
         }
         LOVE_LAUNCH(nan_fill_kernel<V>, 64, 256, 0, s, tm.qstart, m, tm.perm, out, mean_out, c.counters);
         return;
