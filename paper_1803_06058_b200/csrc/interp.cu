@@ -8,6 +8,7 @@
 // kItemMax consecutive points of one cell: every later pass streams them in that order.
 #include <cuda_runtime.h>
 
+#include <climits>
 #include <cstdlib>
 
 #include "love_internal.h"
@@ -160,6 +161,36 @@ __global__ void sort_within_cells_kernel(const int* __restrict__ start, int m_to
     }
 }
 
+// The same order (ascending original index within each cell) by rank instead of insertion:
+// a warp per cell, every entry's rank = the count of smaller entries of its cell (entries are
+// distinct point indices), written to out.  O(n^2 / 32) per cell against the insertion sort's
+// dependent O(n^2) global moves on one thread (cfg4's densest cells hold ~330 points).
+__global__ void rank_within_cells_kernel(const int* __restrict__ start, int m_total, const int* __restrict__ perm,
+                                         int* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (c >= m_total) return;
+    const int b = start[c], e = start[c + 1], n = e - b;
+    if (n <= 32) {
+        const int v = lane < n ? perm[b + lane] : INT_MAX;
+        int rank = 0;
+#pragma unroll 8
+        for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, v, j) < v;
+        if (lane < n) out[b + rank] = v;
+        return;
+    }
+    if (n > 4096) {                                   // as the insertion sort: left in place order
+        for (int i = lane; i < n; i += 32) out[b + i] = perm[b + i];
+        return;
+    }
+    for (int i = lane; i < n; i += 32) {
+        const int v = perm[b + i];
+        int rank = 0;
+        for (int j = 0; j < n; ++j) rank += perm[b + j] < v;
+        out[b + rank] = v;
+    }
+}
+
 template <typename V>
 __global__ void gather_sorted_kernel(int d, const int* __restrict__ perm, int64_t n,
                                      const double* __restrict__ frac64, const double* __restrict__ y,
@@ -239,8 +270,16 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
     cuda_check(cudaMemsetAsync(count, 0, sizeof(int) * (M + 1), s), "sort memset");
     if (n > 0) {
         LOVE_LAUNCH(place_kernel, grid_for(n, 256), 256, 0, s, cell, n, c.cell_start, count, c.perm);
-        LOVE_LAUNCH(sort_within_cells_kernel, (int)ceil_div(M, 128), 128, 0, s, c.cell_start, M,
-                    c.perm);
+        if (std::getenv("LOVE_INSERTION_SORT") != nullptr) {
+            LOVE_LAUNCH(sort_within_cells_kernel, (int)ceil_div(M, 128), 128, 0, s, c.cell_start, M, c.perm);
+        } else {
+            int* ranked = nullptr;
+            cuda_check(cudaMallocAsync((void**)&ranked, sizeof(int) * n, s), "rank alloc");
+            LOVE_LAUNCH(rank_within_cells_kernel, (int)ceil_div((int64_t)M * 32, 256), 256, 0, s, c.cell_start, M,
+                        c.perm, ranked);
+            cuda_check(cudaMemcpyAsync(c.perm, ranked, sizeof(int) * n, cudaMemcpyDeviceToDevice, s), "rank copy");
+            cuda_check(cudaFreeAsync(ranked, s), "rank free");
+        }
         if (c.precision == LOVE_FP64)
             LOVE_LAUNCH(gather_sorted_kernel<double>, grid_for(n, 256), 256, 0, s, c.g.d, c.perm, n,
                         frac64, y, (double*)c.frac[0], (double*)c.frac[1], (double*)c.frac[2],
