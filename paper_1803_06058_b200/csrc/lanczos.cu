@@ -999,6 +999,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     pl.smu = sizeof(double) * (pl.k + 1);
     ensure_smem((const void*)reorth_dots_sweep_kernel<V, 1>, sizeof(double) * 8 * (pl.k + 1));
 
+    host_mark("plan");
     const LanczosState& st = c.st;
     {
         ProfScope ps(LOVE_PROF_SETUP, s);
@@ -1019,6 +1020,7 @@ void lanczos_impl(Cache& c, cudaStream_t s) {
     // one GPU: early stop of the replays at breakdown (the device sets a mapped host flag; on
     // several GPUs every rank must issue the same collectives, so they replay to k)
     std::unique_ptr<ReplayThrottle> thr;
+    host_mark("q0");
     if (graph && c.comm == nullptr && pl.fold) {
         thr.reset(new ReplayThrottle(c.device));
         c.st.hdone = thr->d;

@@ -384,6 +384,7 @@ void finish_build(Cache* c, const love_opts& o, int32_t k, cudaStream_t s) {
         void* h;
         ~L2Scope() { l2_persist_end(h); }
     } l2{c->fused ? nullptr : l2_persist_begin(*c, s)};
+    host_mark("l2_persist");
     if (c->fused) run_lanczos_fused(*c, s);
     else run_lanczos(*c, s);
     host_mark("lanczos_enqueued");
