@@ -162,28 +162,22 @@ __global__ void sort_within_cells_kernel(const int* __restrict__ start, int m_to
 }
 
 // The same order (ascending original index within each cell) by rank instead of insertion:
-// a warp per cell, every entry's rank = the count of smaller entries of its cell (entries are
-// distinct point indices), written to out.  O(n^2 / 32) per cell against the insertion sort's
-// dependent O(n^2) global moves on one thread (cfg4's densest cells hold ~330 points).
+// a group of 8 lanes per cell, every entry's rank = the count of smaller entries of its cell
+// (entries are distinct point indices), written to out.  O(n^2 / 8) per cell against the
+// insertion sort's dependent O(n^2) global moves on one thread (cfg4's densest cells hold ~330
+// points); 8-lane groups keep the grid small for the many empty and few-point cells.
+constexpr int kRankLanes = 8;
 __global__ void rank_within_cells_kernel(const int* __restrict__ start, int m_total, const int* __restrict__ perm,
                                          int* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (c >= m_total) return;
+    const int sub = threadIdx.x & (kRankLanes - 1);
+    const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kRankLanes;
+    if (c >= m_total) return;                         // whole groups leave together
     const int b = start[c], e = start[c + 1], n = e - b;
-    if (n <= 32) {
-        const int v = lane < n ? perm[b + lane] : INT_MAX;
-        int rank = 0;
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) rank += __shfl_sync(0xffffffffu, v, j) < v;
-        if (lane < n) out[b + rank] = v;
-        return;
-    }
     if (n > 4096) {                                   // as the insertion sort: left in place order
-        for (int i = lane; i < n; i += 32) out[b + i] = perm[b + i];
+        for (int i = sub; i < n; i += kRankLanes) out[b + i] = perm[b + i];
         return;
     }
-    for (int i = lane; i < n; i += 32) {
+    for (int i = sub; i < n; i += kRankLanes) {
         const int v = perm[b + i];
         int rank = 0;
         for (int j = 0; j < n; ++j) rank += perm[b + j] < v;
@@ -275,8 +269,8 @@ void launch_counting_sort(Cache& c, const int* cell, const double* frac64, const
         } else {
             int* ranked = nullptr;
             cuda_check(cudaMallocAsync((void**)&ranked, sizeof(int) * n, s), "rank alloc");
-            LOVE_LAUNCH(rank_within_cells_kernel, (int)ceil_div((int64_t)M * 32, 256), 256, 0, s, c.cell_start, M,
-                        c.perm, ranked);
+            LOVE_LAUNCH(rank_within_cells_kernel, (int)ceil_div((int64_t)M * kRankLanes, 256), 256, 0, s, c.cell_start,
+                        M, c.perm, ranked);
             cuda_check(cudaMemcpyAsync(c.perm, ranked, sizeof(int) * n, cudaMemcpyDeviceToDevice, s), "rank copy");
             cuda_check(cudaFreeAsync(ranked, s), "rank free");
         }
